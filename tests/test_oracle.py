@@ -1,0 +1,128 @@
+"""CPU tests: the numpy oracle restatement is pinned to the reference.
+
+Two anchors (task ③): the committed golden fixtures (generated from the
+unmodified reference by tests/golden/gen_golden.py) and, when present, the
+compiled reference library oracle/_ref/libhexmg_ref.so itself."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import hexmg_np as H
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, name))
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("p,q", [(1, 2), (2, 3), (3, 4), (4, 5), (1, 3), (1, 4), (1, 5), (2, 4), (2, 5)])
+def test_basis_matches_golden(p, q):
+    g = load("basis.npz")
+    b = H.build_lagrange_basis(p, q)
+    for k in ("nodes", "points", "weights", "interp", "deriv", "pinv", "colloc"):
+        np.testing.assert_allclose(getattr(b, k), g[f"p{p}q{q}_{k}"], atol=2e-15, rtol=0)
+
+
+def test_quadrature_properties():
+    # test_basis.cpp:48-77
+    for q in range(1, 9):
+        x, w = H.gauss_legendre(q)
+        assert abs(w.sum() - 2.0) < 1e-14
+        for k in range(2 * q):
+            exact = 2.0 / (k + 1) if k % 2 == 0 else 0.0
+            assert abs((w * x**k).sum() - exact) < 1e-13
+    with pytest.raises(ValueError):
+        H.gauss_legendre(0)
+    with pytest.raises(ValueError):
+        H.gauss_lobatto_nodes(0)
+
+
+def _problem_from_meta(g):
+    meta = g["meta"]
+    order = int(meta[0])
+    cells = tuple(int(c) for c in meta[1:4])
+    ext = tuple(float(e) for e in meta[4:7])
+    return H.make_problem(ext, cells, order, traction_face=1, traction=(0, 0, -0.02)), order, cells, ext
+
+
+@pytest.mark.parametrize("name", ["q1_bar", "q2_bar", "q3_cube", "q4_cube"])
+def test_operator_matches_golden(name):
+    g = load(f"{name}.npz")
+    P, order, cells, ext = _problem_from_meta(g)
+    assert rel(P.load, g["load"]) < 1e-13
+    f = P.op.apply_residual(g["u"])
+    assert rel(f, g["f"]) < 1e-12
+    assert np.abs(P.op.state - g["state"]).max() < 1e-12
+    assert rel(P.op.apply_jacobian(g["x"]), g["jx"]) < 1e-12
+    assert rel(P.op.extract_diagonal(), g["diag"]) < 1e-12
+
+
+@pytest.mark.parametrize("name", ["q2_bar", "q3_cube", "q4_cube"])
+def test_multigrid_matches_golden(name):
+    g = load(f"{name}.npz")
+    P, order, cells, ext = _problem_from_meta(g)
+    P.op.apply_residual(g["u"])
+    hier = H.Hierarchy(ext, cells, order, order + 1, (0,), P.mu, P.lam, P.op)
+    hier.setup_numeric()
+    L = len(hier.levels)
+    for k in range(L - 1):
+        assert rel(hier.transfers[k + 1].apply(g[f"P{k}_xc"]), g[f"P{k}_pxc"]) < 1e-13
+        assert rel(hier.transfers[k + 1].apply_transpose(g[f"P{k}_xf"]), g[f"P{k}_rxf"]) < 1e-13
+    for k in range(1, L):
+        assert abs(hier.smoothers[k].lambda_max - float(g[f"lam{k}"])) < 1e-12
+        assert rel(hier.levels[k].extract_diagonal(), g[f"diag_level{k}"]) < 1e-12
+    import scipy.sparse as sp
+    A0 = sp.csr_matrix((g["coarse_vals"], g["coarse_cols"], g["coarse_rowptr"])).toarray()
+    assert np.abs(A0 - hier.coarse_matrix).max() < 1e-13
+    assert rel(hier.precondition(g["vcycle_b"]), g["vcycle_x"]) < 1e-12
+    for tag, rtol in (("1e-3", 1e-3), ("1e-8", 1e-8)):
+        r = H.cg_solve(P.op.apply_jacobian, hier.precondition, g["vcycle_b"],
+                       np.zeros(P.op.size), rtol, 500)
+        assert abs(r.iterations - int(g[f"mgcg_its_{tag}"])) <= 1
+
+
+def test_cfg1_jacobi_cg_matches_golden():
+    g = load("cfg1_q1_8.npz")
+    P = H.make_problem((1, 1, 1), (8, 8, 8), 1, traction_face=1, traction=(0, 0, -0.02))
+    f = P.op.apply_residual(np.zeros(P.op.size))
+    assert rel(f, g["f0"]) < 1e-12
+    d = P.op.extract_diagonal()
+    for tag, rtol, its in (("1e-3", 1e-3, 44), ("1e-8", 1e-8, 72)):
+        assert int(g[f"its_{tag}"]) == its  # SURVEY.md §8(c) goldens
+        x = np.zeros(P.op.size)
+        r = H.cg_solve(P.op.apply_jacobian, lambda r: r / d, -f, x, rtol, 5000)
+        assert abs(r.iterations - its) <= 1
+        assert rel(x, g[f"x_{tag}"]) < 1e-9
+    assert abs(np.linalg.norm(g["x_1e-8"]) - 2.102035211278199) < 1e-9
+
+
+def test_verify_suite_golden():
+    g = load("verify.npz")
+    res = dict(zip(g["names"], g["passed"]))
+    # reference defect: galerkin-identity fails as shipped
+    assert not res["galerkin-identity"]
+    assert all(v for k, v in res.items() if k != "galerkin-identity")
+    pert = dict(zip(g["names"], g["passed_perturbed"]))
+    assert not pert["jacobian-fd"]
+
+
+def test_oracle_against_compiled_reference():
+    from oracle import ref_lib as R
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    rp = R.RefProblem(extents=(1, 1, 1), cells=(3, 2, 2), order=3, traction_face="+x",
+                      traction=(0, 0, -0.02))
+    P = H.make_problem((1, 1, 1), (3, 2, 2), 3, traction_face=1, traction=(0, 0, -0.02))
+    u = 1e-2 * np.cos(np.arange(rp.n) * 0.01)
+    m, _ = rp.constraints()
+    u[m != 0] = 0
+    assert rel(P.op.apply_residual(u), rp.apply_residual(u)) < 1e-12
+    x = np.sin(np.arange(rp.n))
+    assert rel(P.op.apply_jacobian(x), rp.apply_jacobian(x)) < 1e-12
+    assert np.array_equal(H.rough_seed(50, None), R.rough_seed(50))
