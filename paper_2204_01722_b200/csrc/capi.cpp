@@ -1,0 +1,415 @@
+// extern "C" boundary (include/hexmg_b200.h).  Every entry point catches
+// and maps exceptions to codes + thread-local detail.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "operator.hpp"
+#include "setup.hpp"
+#include "solver.hpp"
+#include "vector.hpp"
+
+struct hxg_state_s {
+  std::shared_ptr<hxg::State> s;
+};
+struct hxg_op_s {
+  std::unique_ptr<hxg::Operator> owned;
+  hxg::Operator* op = nullptr;
+};
+struct hxg_mg_s {
+  std::unique_ptr<hxg::Hierarchy> h;
+  std::vector<hxg_op_s> level_handles;
+};
+
+namespace {
+
+thread_local hxg_error g_err{0, -1, -1, 0.0, {0}};
+
+void set_error(int code, const char* msg, int element = -1, int point = -1, double j = 0.0) {
+  g_err.code = code;
+  g_err.element = element;
+  g_err.point = point;
+  g_err.jacobian = j;
+  std::snprintf(g_err.message, sizeof(g_err.message), "%s", msg);
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HXG_OK;
+  } catch (const hxg::Error& e) {
+    set_error(e.code, e.what(), e.element, e.point, e.jacobian);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_error(HXG_ERR_GENERIC, "out of host memory");
+    return HXG_ERR_GENERIC;
+  } catch (const std::exception& e) {
+    set_error(HXG_ERR_GENERIC, e.what());
+    return HXG_ERR_GENERIC;
+  }
+}
+
+hxg::Operator& OP(hxg_op_t h) {
+  if (!h || !h->op) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "null operator handle");
+  return *h->op;
+}
+
+hxg::Hierarchy& MG(hxg_mg_t h) {
+  if (!h || !h->h) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "null hierarchy handle");
+  return *h->h;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hxg_last_error(hxg_error* out) {
+  if (out) *out = g_err;
+  return g_err.code;
+}
+
+const char* hxg_version(void) { return "hexmg-b200 0.1 (sm_100a, FP64)"; }
+
+int hxg_state_create(hxg_state_t* out) {
+  return guarded([&] {
+    auto* s = new hxg_state_s();
+    s->s = std::make_shared<hxg::State>();
+    *out = s;
+  });
+}
+
+int hxg_state_release(hxg_state_t s) {
+  delete s;
+  return HXG_OK;
+}
+
+int hxg_op_create(const hxg_op_desc* d, hxg_state_t state, hxg_op_t* out) {
+  return guarded([&] {
+    if (!d) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "null descriptor");
+    if (d->storage != 0)
+      throw hxg::Error(HXG_ERR_UNSUPPORTED, "only JacobianStorage::Current is implemented");
+    int n = d->order + 1, q = d->qpts;
+    std::vector<double> interp(d->interp, d->interp + q * n);
+    std::vector<double> deriv(d->deriv, d->deriv + q * n);
+    std::vector<double> colloc(d->colloc, d->colloc + q * q);
+    std::shared_ptr<hxg::Geometry> geo;
+    if (d->dxidX && d->weight) geo = hxg::Operator::make_geometry(d->cells, q, d->dxidX, d->weight);
+    auto* h = new hxg_op_s();
+    h->owned = std::make_unique<hxg::Operator>(d->order, q, d->cells, interp, deriv, colloc, d->mu,
+                                               d->lambda, d->mask, state ? state->s : nullptr, geo);
+    h->op = h->owned.get();
+    *out = h;
+  });
+}
+
+int hxg_op_destroy(hxg_op_t op) {
+  delete op;
+  return HXG_OK;
+}
+
+int hxg_op_size(hxg_op_t op, int64_t* n) { return guarded([&] { *n = OP(op).size(); }); }
+int hxg_op_num_elements(hxg_op_t op, int64_t* ne) {
+  return guarded([&] { *ne = OP(op).num_elements(); });
+}
+int hxg_op_set_stream(hxg_op_t op, void* stream) {
+  return guarded([&] { OP(op).set_stream((cudaStream_t)stream); });
+}
+int hxg_op_set_external_load(hxg_op_t op, const double* load) {
+  return guarded([&] { OP(op).set_external_load(load); });
+}
+int hxg_op_set_load_scale(hxg_op_t op, double s) {
+  return guarded([&] { OP(op).set_load_scale(s); });
+}
+int hxg_op_set_jacobian_perturbation(hxg_op_t op, double eps) {
+  return guarded([&] { OP(op).set_jacobian_perturbation(eps); });
+}
+int hxg_op_stored_bytes_per_dof(hxg_op_t op, double* out) {
+  return guarded([&] { *out = OP(op).stored_bytes_per_dof(); });
+}
+int hxg_op_counters(hxg_op_t op, int64_t* r, int64_t* j) {
+  return guarded([&] {
+    *r = OP(op).residual_applies();
+    *j = OP(op).jacobian_applies();
+  });
+}
+int hxg_op_set_variant(hxg_op_t op, int v) { return guarded([&] { OP(op).set_variant(v); }); }
+
+int hxg_op_apply_residual(hxg_op_t op, const double* u, double* f) {
+  return guarded([&] { OP(op).apply_residual(u, f); });
+}
+int hxg_op_apply_jacobian(hxg_op_t op, const double* du, double* y) {
+  return guarded([&] { OP(op).apply_jacobian(du, y); });
+}
+
+namespace {
+struct Pinned {
+  double* p = nullptr;
+  size_t n = 0;
+  ~Pinned() {
+    if (p) cudaFreeHost(p);
+  }
+};
+}  // namespace
+
+int hxg_op_apply_jacobian_host(hxg_op_t op, const double* du_host, double* y_host) {
+  return guarded([&] {
+    auto& o = OP(op);
+    size_t n = (size_t)o.size();
+    hxg::DevBuf<double> x(n), y(n);
+    cudaStream_t s = o.stream();
+    HXG_CUDA(cudaMemcpyAsync(x.p, du_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    o.apply_jacobian(x.p, y.p);
+    HXG_CUDA(cudaMemcpyAsync(y_host, y.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    HXG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int hxg_op_apply_residual_host(hxg_op_t op, const double* u_host, double* f_host) {
+  return guarded([&] {
+    auto& o = OP(op);
+    size_t n = (size_t)o.size();
+    hxg::DevBuf<double> x(n), y(n);
+    cudaStream_t s = o.stream();
+    HXG_CUDA(cudaMemcpyAsync(x.p, u_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    o.apply_residual(x.p, y.p);
+    HXG_CUDA(cudaMemcpyAsync(f_host, y.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    HXG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int hxg_op_extract_diagonal(hxg_op_t op, double* d) {
+  return guarded([&] { OP(op).extract_diagonal(d); });
+}
+int hxg_op_total_strain_energy(hxg_op_t op, const double* u, double* energy) {
+  return guarded([&] { *energy = OP(op).total_strain_energy(u); });
+}
+int hxg_op_export_state(hxg_op_t op, double* host) {
+  return guarded([&] {
+    if (!OP(op).state()->valid)
+      throw hxg::Error(HXG_ERR_STATE_NOT_INITIALIZED, "quadrature state not initialized");
+    OP(op).export_state(host);
+  });
+}
+int hxg_op_gather(hxg_op_t op, const double* l, double* e) {
+  return guarded([&] { OP(op).gather(l, e); });
+}
+int hxg_op_scatter_add(hxg_op_t op, const double* e, double* l) {
+  return guarded([&] { OP(op).scatter_add(e, l); });
+}
+
+int hxg_op_time_jacobian(hxg_op_t op, const double* x, double* y, int warmup, int repeats,
+                         double* ms) {
+  return guarded([&] {
+    auto& o = OP(op);
+    cudaStream_t s = o.stream();
+    for (int w = 0; w < warmup; ++w) o.apply_jacobian(x, y);
+    cudaEvent_t a, b;
+    HXG_CUDA(cudaEventCreate(&a));
+    HXG_CUDA(cudaEventCreate(&b));
+    HXG_CUDA(cudaStreamSynchronize(s));
+    HXG_CUDA(cudaEventRecord(a, s));
+    for (int r = 0; r < repeats; ++r) o.apply_jacobian(x, y);
+    HXG_CUDA(cudaEventRecord(b, s));
+    HXG_CUDA(cudaEventSynchronize(b));
+    float f = 0.f;
+    HXG_CUDA(cudaEventElapsedTime(&f, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms = f;
+  });
+}
+
+// ---- multigrid -------------------------------------------------------------
+
+int hxg_mg_create(hxg_op_t fine, int fixed_face_mask, const int* schedule, int num_levels,
+                  int pre_smooth, int post_smooth, hxg_mg_t* out) {
+  return guarded([&] {
+    std::vector<int> sched;
+    if (schedule) sched.assign(schedule, schedule + num_levels);
+    auto* h = new hxg_mg_s();
+    h->h = std::make_unique<hxg::Hierarchy>(&OP(fine), fixed_face_mask, sched, pre_smooth,
+                                            post_smooth);
+    h->level_handles.resize((size_t)h->h->num_levels());
+    for (int k = 0; k < h->h->num_levels(); ++k) h->level_handles[(size_t)k].op = h->h->level(k).op;
+    *out = h;
+  });
+}
+
+int hxg_mg_destroy(hxg_mg_t mg) {
+  delete mg;
+  return HXG_OK;
+}
+int hxg_mg_num_levels(hxg_mg_t mg, int* n) { return guarded([&] { *n = MG(mg).num_levels(); }); }
+int hxg_mg_level_size(hxg_mg_t mg, int level, int64_t* n) {
+  return guarded([&] { *n = MG(mg).level(level).op->size(); });
+}
+int hxg_mg_level_op(hxg_mg_t mg, int level, hxg_op_t* op) {
+  return guarded([&] {
+    if (level < 0 || level >= MG(mg).num_levels())
+      throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "level out of range");
+    *op = &mg->level_handles[(size_t)level];
+  });
+}
+int hxg_mg_setup_numeric(hxg_mg_t mg) { return guarded([&] { MG(mg).setup_numeric(); }); }
+int hxg_mg_lambda_max(hxg_mg_t mg, int level, double* out) {
+  return guarded([&] { *out = MG(mg).level(level).smoother.lambda_max; });
+}
+int hxg_mg_prolong(hxg_mg_t mg, int coarse_level, const double* xc, double* xf) {
+  return guarded([&] { MG(mg).prolong(coarse_level, xc, xf); });
+}
+int hxg_mg_restrict(hxg_mg_t mg, int coarse_level, const double* xf, double* xc) {
+  return guarded([&] { MG(mg).restrict_to(coarse_level, xf, xc); });
+}
+int hxg_mg_vcycle(hxg_mg_t mg, const double* b, double* x) {
+  return guarded([&] { MG(mg).v_cycle(b, x, false); });
+}
+int hxg_mg_smooth(hxg_mg_t mg, int level, const double* b, double* x) {
+  return guarded([&] {
+    auto& lv = MG(mg).level(level);
+    if (!lv.smoother.ready) throw hxg::Error(HXG_ERR_GENERIC, "smoother not set up");
+    lv.smoother.apply(*lv.op, b, x, false);
+  });
+}
+int hxg_mg_coarse_nnz(hxg_mg_t mg, int64_t* nnz) {
+  return guarded([&] { *nnz = MG(mg).coarse_matrix().nnz(); });
+}
+int hxg_mg_coarse_csr_host(hxg_mg_t mg, int* row_ptr, int* cols, double* vals) {
+  return guarded([&] {
+    const auto& a = MG(mg).coarse_matrix();
+    std::memcpy(row_ptr, a.row_ptr_h.data(), sizeof(int) * a.row_ptr_h.size());
+    std::memcpy(cols, a.cols_h.data(), sizeof(int) * a.cols_h.size());
+    HXG_CUDA(cudaMemcpy(vals, a.vals.p, sizeof(double) * a.cols_h.size(), cudaMemcpyDeviceToHost));
+  });
+}
+int hxg_mg_coarse_solve(hxg_mg_t mg, const double* b, double* x) {
+  return guarded([&] { MG(mg).coarse_solve(b, x); });
+}
+
+int hxg_cg_solve(hxg_op_t op, hxg_mg_t mg, int precond, const double* b, double* x, double rtol,
+                 int max_iterations, hxg_cg_report* report, double* history, int cap) {
+  return guarded([&] {
+    auto& o = OP(op);
+    long long n = o.size();
+    cudaStream_t s = o.stream();
+    hxg::DevOp a = [&o](const double* xx, double* yy) { o.apply_jacobian(xx, yy); };
+    hxg::DevOp m;
+    hxg::DevBuf<double> inv;
+    if (precond == 0) {
+      m = [n, s](const double* r, double* z) { hxg::vcopy(z, r, n, s); };
+    } else if (precond == 1) {
+      hxg::DevBuf<double> d((size_t)n);
+      o.extract_diagonal(d.p);
+      inv.alloc((size_t)n);
+      hxg::vreciprocal(inv.p, d.p, n, s);
+      const double* ip = inv.p;
+      m = [n, s, ip](const double* r, double* z) { hxg::vscale_mul(z, ip, r, n, s); };
+    } else {
+      auto& h = MG(mg);
+      m = [&h, n, s](const double* r, double* z) {
+        hxg::vzero(z, n, s);
+        h.v_cycle(r, z, true);
+      };
+    }
+    hxg::CgResult res = hxg::cg_solve(n, a, m, b, x, rtol, max_iterations, s);
+    if (report) {
+      report->iterations = res.iterations;
+      report->converged = res.converged ? 1 : 0;
+      report->eig_min = res.eig_min;
+      report->eig_max = res.eig_max;
+      report->initial_natural_norm = res.history.empty() ? 0.0 : res.history.front();
+      report->final_natural_norm = res.history.empty() ? 0.0 : res.history.back();
+    }
+    if (history)
+      for (int i = 0; i < cap && i < (int)res.history.size(); ++i) history[i] = res.history[(size_t)i];
+  });
+}
+
+int hxg_lambda_max_jacobi(hxg_op_t op, int iterations, double* out) {
+  return guarded([&] {
+    auto& o = OP(op);
+    long long n = o.size();
+    cudaStream_t s = o.stream();
+    hxg::DevBuf<double> d((size_t)n), inv((size_t)n);
+    o.extract_diagonal(d.p);
+    hxg::vreciprocal(inv.p, d.p, n, s);
+    auto seed_h = hxg::rough_seed(n, o.mask_host());
+    hxg::DevBuf<double> seed;
+    seed.upload(seed_h);
+    *out = hxg::estimate_lambda_max(
+        n, [&o](const double* x, double* y) { o.apply_jacobian(x, y); }, inv.p, seed.p, iterations,
+        s);
+  });
+}
+
+int hxg_dot(const double* x, const double* y, int64_t n, void* stream, double* out) {
+  return guarded([&] {
+    hxg::DotWorkspace ws;
+    *out = hxg::dot(x, y, n, ws, (cudaStream_t)stream);
+  });
+}
+
+int hxg_malloc(void** p, size_t bytes) { return guarded([&] { HXG_CUDA(cudaMalloc(p, bytes)); }); }
+int hxg_free(void* p) { return guarded([&] { HXG_CUDA(cudaFree(p)); }); }
+int hxg_memcpy_h2d(void* dst, const void* src, size_t bytes) {
+  return guarded([&] { HXG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice)); });
+}
+int hxg_memcpy_d2h(void* dst, const void* src, size_t bytes) {
+  return guarded([&] { HXG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)); });
+}
+int hxg_device_synchronize(void) { return guarded([&] { HXG_CUDA(cudaDeviceSynchronize()); }); }
+
+// ---- host setup ------------------------------------------------------------
+
+int hxg_setup_basis(int p, int q, double* nodes, double* points, double* weights, double* interp,
+                    double* deriv, double* pinv, double* colloc) {
+  return guarded([&] {
+    hxg::Basis b = hxg::build_basis(p, q);
+    auto cp = [](double* dst, const std::vector<double>& v) {
+      if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+    };
+    cp(nodes, b.nodes);
+    cp(points, b.rule.points);
+    cp(weights, b.rule.weights);
+    cp(interp, b.interp);
+    cp(deriv, b.deriv);
+    cp(pinv, b.pinv);
+    cp(colloc, b.colloc);
+  });
+}
+
+int hxg_setup_geometry(const double extents[3], const int cells[3], int p, int q, double* dxidX,
+                       double* weight) {
+  return guarded([&] {
+    hxg::Basis b = hxg::build_basis(p, q);
+    std::vector<double> dx, w;
+    hxg::geometry(extents, cells, p, b, dx, w);
+    std::memcpy(dxidX, dx.data(), dx.size() * sizeof(double));
+    std::memcpy(weight, w.data(), w.size() * sizeof(double));
+  });
+}
+
+int hxg_setup_constraints(const int cells[3], int p, int fixed_face_mask, uint8_t* mask) {
+  return guarded([&] {
+    std::vector<uint8_t> m;
+    hxg::face_mask(cells, p, fixed_face_mask, m);
+    std::memcpy(mask, m.data(), m.size());
+  });
+}
+
+int hxg_setup_traction_load(const double extents[3], const int cells[3], int p, int q, int face,
+                            const double traction[3], double* load) {
+  return guarded([&] {
+    hxg::Basis b = hxg::build_basis(p, q);
+    std::vector<double> l;
+    hxg::traction_load(extents, cells, p, b, face, traction, l);
+    std::memcpy(load, l.data(), l.size() * sizeof(double));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// Shared definitions for the B200 FP64 matrix-free p-multigrid library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "hexmg_b200.h"
+
+namespace hxg {
+
+// Error carried across the C-ABI (hxg_last_error); the C++ drop-in layer
+// rethrows the reference's exception types from it (errors.hpp:9-104).
+struct Error : std::runtime_error {
+  int code;
+  int element = -1, point = -1;
+  double jacobian = 0.0;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(HXG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define HXG_CUDA(x) ::hxg::cuda_check((x), #x)
+
+// Supported (P, Q) pairs: fine levels (p, p+1) and the coarse levels the
+// p-halving schedule builds on the fine rule (multigrid.hpp:15-19, :244).
+constexpr int kMaxP = 4;
+constexpr int kMaxQ = 5;
+
+// Per-qpt scalars of the Current storage (material.hpp:70-78, :145-148):
+// [w detJ, dxi/dx (9, row-major), tau (00,11,22,01,02,12), lambda log J].
+constexpr int kStateStride = 17;
+// Geometry per qpt: dxi/dX (9, row-major) then w * detJ (mesh.hpp:169-189).
+constexpr int kGeoStride = 10;
+
+// Brick of elements processed by one CTA; depends only on Q so every level
+// of a hierarchy (which shares the fine quadrature, multigrid.hpp:229-249)
+// shares one quadrature-data layout.
+__host__ __device__ constexpr int brick_x(int q) { return q == 2 ? 4 : q == 3 ? 4 : q == 4 ? 4 : 2; }
+__host__ __device__ constexpr int brick_y(int q) { return q == 2 ? 4 : q == 3 ? 4 : q == 4 ? 2 : 2; }
+__host__ __device__ constexpr int brick_z(int q) { return q == 2 ? 4 : q == 3 ? 2 : q == 4 ? 2 : 2; }
+
+// Quadrature-data layout in HBM: brick-blocked structure-of-arrays so that
+// the thread owning column (element, qx, qy) reads one coalesced double per
+// (brick, qz, scalar) row:
+//   offset(brick, qz, s, t) = ((brick * Q + qz) * S + s) * T + t,
+//   t = local_element * Q^2 + qy * Q + qx,  T = BX*BY*BZ*Q^2.
+struct QLayout {
+  int cells[3] = {1, 1, 1};
+  int Q = 2;
+  int B[3] = {1, 1, 1};
+  int nb[3] = {1, 1, 1};
+  int T = 0;
+
+  __host__ __device__ long long num_bricks() const { return (long long)nb[0] * nb[1] * nb[2]; }
+  // Doubles per scalar-stride unit of one brick (Q * T).
+  __host__ __device__ long long brick_points() const { return (long long)Q * T; }
+  __host__ __device__ long long total_points() const { return num_bricks() * brick_points(); }
+
+  static QLayout make(const int cells_[3], int q) {
+    QLayout l;
+    l.Q = q;
+    l.B[0] = brick_x(q);
+    l.B[1] = brick_y(q);
+    l.B[2] = brick_z(q);
+    for (int d = 0; d < 3; ++d) {
+      l.cells[d] = cells_[d];
+      l.nb[d] = (cells_[d] + l.B[d] - 1) / l.B[d];
+    }
+    l.T = l.B[0] * l.B[1] * l.B[2] * q * q;
+    return l;
+  }
+
+  // Element (reference order e = ex + cx (ey + cy ez)) and point q (x-fastest)
+  // -> (brick, qz, t) coordinates for host-side permutations.
+  void locate(long long e, int qpt, long long& brick, int& qz, int& t) const {
+    long long ex = e % cells[0], ey = (e / cells[0]) % cells[1], ez = e / ((long long)cells[0] * cells[1]);
+    long long bx = ex / B[0], by = ey / B[1], bz = ez / B[2];
+    int lx = (int)(ex - bx * B[0]), ly = (int)(ey - by * B[1]), lz = (int)(ez - bz * B[2]);
+    brick = bx + nb[0] * (by + (long long)nb[1] * bz);
+    int le = lx + B[0] * (ly + B[1] * lz);
+    int qx = qpt % Q, qy = (qpt / Q) % Q;
+    qz = qpt / (Q * Q);
+    t = le * Q * Q + qy * Q + qx;
+  }
+};
+
+// Box-mesh description on device: element counts, order, nodes per dim
+// (BoxMesh, mesh.hpp:19-33); restriction indices are analytic
+// (build_restriction, mesh.hpp:119-138).
+struct BoxDev {
+  int cells[3];
+  int p;
+  int npd[3];
+  __host__ __device__ long long num_nodes() const { return (long long)npd[0] * npd[1] * npd[2]; }
+  __host__ __device__ long long num_elements() const {
+    return (long long)cells[0] * cells[1] * cells[2];
+  }
+};
+
+inline BoxDev make_box(const int cells[3], int p) {
+  BoxDev b;
+  b.p = p;
+  for (int d = 0; d < 3; ++d) {
+    b.cells[d] = cells[d];
+    b.npd[d] = p * cells[d] + 1;
+  }
+  return b;
+}
+
+}  // namespace hxg

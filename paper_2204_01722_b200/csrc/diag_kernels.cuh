@@ -1,0 +1,142 @@
+// Jacobi diagonal (extract_diagonal, operator.hpp:247-283) and element
+// matrices for the assembled coarse operator (coo_numeric,
+// assembly.hpp:188-230): pointwise 9x9 tensors by probing the linear
+// Jacobian q-function (pointwise_jacobian_tensor, operator.hpp:233-243),
+// contracted with the dense tabulation (dense_tabulation, basis.hpp:424-451).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+#include "element.cuh"
+#include "qfunction.cuh"
+
+namespace hxg {
+
+struct DiagParams {
+  BoxDev box;
+  QLayout lay;
+  const double* interp;  // Q x N
+  const double* deriv;   // Q x N
+  const double* state;
+  double mu, lambda, perturb;
+  double* out;  // diag: E-vector (e, c, a); assembly: (e, 3N^3, 3N^3)
+};
+
+__device__ __forceinline__ long long state_offset(const QLayout& lay, long long e, int qpt) {
+  long long ex = e % lay.cells[0], ey = (e / lay.cells[0]) % lay.cells[1],
+            ez = e / ((long long)lay.cells[0] * lay.cells[1]);
+  long long bx = ex / lay.B[0], by = ey / lay.B[1], bz = ez / lay.B[2];
+  int lx = (int)(ex - bx * lay.B[0]), ly = (int)(ey - by * lay.B[1]), lz = (int)(ez - bz * lay.B[2]);
+  long long brick = bx + lay.nb[0] * (by + (long long)lay.nb[1] * bz);
+  int le = lx + lay.B[0] * (ly + lay.B[1] * lz);
+  int Q = lay.Q;
+  int qx = qpt % Q, qy = (qpt / Q) % Q, qz = qpt / (Q * Q);
+  int t = le * Q * Q + qy * Q + qx;
+  return ((brick * Q + qz) * kStateStride) * (long long)lay.T + t;
+}
+
+// D[(c1,d1),(c2,d2)] at one point: 9 probes of the Jacobian q-function.
+__device__ __forceinline__ void point_tensor(const DiagParams& prm, long long e, int qpt,
+                                             double* d81) {
+  long long off = state_offset(prm.lay, e, qpt);
+  double st[kStateStride];
+#pragma unroll
+  for (int s = 0; s < kStateStride; ++s) st[s] = prm.state[off + (long long)s * prm.lay.T];
+  for (int u = 0; u < 9; ++u) {
+    double G[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, H[9];
+    G[u] = 1.0;
+    jacobian_qf(prm.mu, prm.lambda, G, st, H);
+    if (prm.perturb != 0.0) H[u] += prm.perturb * st[0];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) d81[k * 9 + u] = H[k];
+  }
+}
+
+// Dense-tabulation gradient of node a at point q (basis.hpp:439-447).
+template <int N, int Q>
+__device__ __forceinline__ void tab_grad(const double* sI, const double* sDv, int a, int qpt,
+                                         double ga[3]) {
+  int i = a % N, j = (a / N) % N, k = a / (N * N);
+  int qa = qpt % Q, qb = (qpt / Q) % Q, qc = qpt / (Q * Q);
+  double bi = sI[qa * N + i], bj = sI[qb * N + j], bk = sI[qc * N + k];
+  double di = sDv[qa * N + i], dj = sDv[qb * N + j], dk = sDv[qc * N + k];
+  ga[0] = di * bj * bk;
+  ga[1] = bi * dj * bk;
+  ga[2] = bi * bj * dk;
+}
+
+// One CTA per element.  Shared: interp, deriv, then per point the 27 entries
+// D[(c,d1),(c,d2)].
+template <int P, int Q>
+__global__ void diag_element_kernel(DiagParams prm) {
+  constexpr int N = P + 1, N3 = N * N * N, Q3 = Q * Q * Q;
+  extern __shared__ double smem[];
+  double* sI = smem;
+  double* sDv = smem + Q * N;
+  double* sT = smem + 2 * Q * N;  // Q3 * 27
+  long long e = blockIdx.x;
+  for (int r = threadIdx.x; r < Q * N; r += blockDim.x) {
+    sI[r] = prm.interp[r];
+    sDv[r] = prm.deriv[r];
+  }
+  for (int qpt = threadIdx.x; qpt < Q3; qpt += blockDim.x) {
+    double d81[81];
+    point_tensor(prm, e, qpt, d81);
+    for (int c = 0; c < 3; ++c)
+      for (int d1 = 0; d1 < 3; ++d1)
+        for (int d2 = 0; d2 < 3; ++d2)
+          sT[qpt * 27 + (c * 3 + d1) * 3 + d2] = d81[(c * 3 + d1) * 9 + c * 3 + d2];
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < 3 * N3; r += blockDim.x) {
+    int a = r / 3, c = r % 3;
+    double sum = 0.0;
+    for (int qpt = 0; qpt < Q3; ++qpt) {
+      double ga[3];
+      tab_grad<N, Q>(sI, sDv, a, qpt, ga);
+      const double* d = sT + qpt * 27 + c * 9;
+#pragma unroll
+      for (int d1 = 0; d1 < 3; ++d1)
+#pragma unroll
+        for (int d2 = 0; d2 < 3; ++d2) sum += ga[d1] * d[d1 * 3 + d2] * ga[d2];
+    }
+    prm.out[(e * 3 + c) * N3 + a] = sum;
+  }
+}
+
+// Element matrix entries (a, ca, b, cb) in the reference COO order
+// (coo_numeric, assembly.hpp:202-224).  One CTA per element; shared holds
+// the full 81-entry tensor per point.
+template <int P, int Q>
+__global__ void assemble_element_kernel(DiagParams prm) {
+  constexpr int N = P + 1, N3 = N * N * N, Q3 = Q * Q * Q, M = 3 * N3;
+  extern __shared__ double smem[];
+  double* sI = smem;
+  double* sDv = smem + Q * N;
+  double* sT = smem + 2 * Q * N;  // Q3 * 81
+  long long e = blockIdx.x;
+  for (int r = threadIdx.x; r < Q * N; r += blockDim.x) {
+    sI[r] = prm.interp[r];
+    sDv[r] = prm.deriv[r];
+  }
+  for (int qpt = threadIdx.x; qpt < Q3; qpt += blockDim.x) point_tensor(prm, e, qpt, sT + qpt * 81);
+  __syncthreads();
+  for (int r = threadIdx.x; r < M * M; r += blockDim.x) {
+    int row = r / M, col = r % M;
+    int a = row / 3, ca = row % 3, b = col / 3, cb = col % 3;
+    double sum = 0.0;
+    for (int qpt = 0; qpt < Q3; ++qpt) {
+      double ga[3], gb[3];
+      tab_grad<N, Q>(sI, sDv, a, qpt, ga);
+      tab_grad<N, Q>(sI, sDv, b, qpt, gb);
+      const double* drow = sT + qpt * 81 + (ca * 3) * 9 + cb * 3;
+      sum += ga[0] * (drow[0] * gb[0] + drow[1] * gb[1] + drow[2] * gb[2]);
+      sum += ga[1] * (drow[9] * gb[0] + drow[10] * gb[1] + drow[11] * gb[2]);
+      sum += ga[2] * (drow[18] * gb[0] + drow[19] * gb[1] + drow[20] * gb[2]);
+    }
+    prm.out[e * (long long)(M * M) + r] = sum;
+  }
+}
+
+}  // namespace hxg

@@ -1,0 +1,8 @@
+// Fused brick Jacobian apply (declared here, defined in fused_apply.cu).
+#pragma once
+
+namespace hxg {
+class Operator;
+bool fused_supported(int p, int q);
+void fused_jacobian(Operator& op, const double* du, double* y);
+}  // namespace hxg

@@ -1,0 +1,84 @@
+// Host orchestration of the device p-multigrid solver: Chebyshev smoother,
+// Lanczos lambda_max, PCG and the V-cycle (smoother.hpp, cg.hpp,
+// multigrid.hpp).  All vectors are device pointers; control scalars (dots)
+// come back to the host once per reduction, as in the reference.
+#pragma once
+
+#include <functional>
+#include <memory>
+#include <vector>
+
+#include "coarse.hpp"
+#include "operator.hpp"
+#include "transfer.hpp"
+#include "vector.hpp"
+
+namespace hxg {
+
+// LinearOperator (cg.hpp:16-19) over device vectors.
+using DevOp = std::function<void(const double*, double*)>;
+
+struct CgResult {
+  int iterations = 0;
+  bool converged = false;
+  std::vector<double> history;
+  double eig_min = 0.0, eig_max = 0.0;
+};
+
+// Extremal Ritz values of the CG/Lanczos tridiagonal (cg.hpp:56-73).
+void lanczos_eigs(const std::vector<double>& alphas, const std::vector<double>& betas,
+                  double& eig_min, double& eig_max);
+// rough_seed (cg.hpp:138-147): mt19937(0x9e3779b9) stream, constrained zeroed.
+std::vector<double> rough_seed(long long n, const std::vector<uint8_t>& mask);
+
+// cg_solve (cg.hpp:81-134).
+CgResult cg_solve(long long n, const DevOp& a, const DevOp& m, const double* b, double* x,
+                  double rtol, int max_iterations, cudaStream_t s);
+// estimate_lambda_max (cg.hpp:152-184).
+double estimate_lambda_max(long long n, const DevOp& a, const double* inv_diag,
+                           const double* seed, int iterations, cudaStream_t s);
+
+// ChebyshevSmoother (smoother.hpp:15-63), degree 2 on [0.1, 1.1] lambda_max.
+struct Chebyshev {
+  int degree = 2;
+  double lambda_max = 0.0, lo = 0.0, hi = 0.0;
+  DevBuf<double> inv_diag, r, d;
+  bool ready = false;
+  void create(Operator& op, int degree_);
+  // One sweep; x_zero = x is known to be exactly zero (A x = 0 is skipped,
+  // bitwise-identical: SURVEY.md Appendix A).
+  void apply(Operator& op, const double* b, double* x, bool x_zero);
+};
+
+struct Level {
+  int order = 0;
+  std::unique_ptr<Operator> owned;
+  Operator* op = nullptr;
+  std::unique_ptr<Transfer> from_coarser;  // levels > 0
+  Chebyshev smoother;
+  DevBuf<double> residual, correction, restricted;
+};
+
+class Hierarchy {
+ public:
+  Hierarchy(Operator* fine, int fixed_face_mask, std::vector<int> schedule, int pre_smooth,
+            int post_smooth);
+  int num_levels() const { return (int)levels_.size(); }
+  Level& level(int k) { return *levels_[(size_t)k]; }
+  void setup_numeric();
+  void prolong(int coarse_level, const double* xc, double* xf);
+  void restrict_to(int coarse_level, const double* xf, double* xc);
+  void v_cycle(const double* b, double* x, bool x_zero = false);
+  void coarse_solve(const double* b, double* x);
+  const CsrMatrix& coarse_matrix() const { return assembly_->matrix(); }
+  cudaStream_t stream() const { return levels_.back()->op->stream(); }
+
+ private:
+  void cycle(int k, const double* b, double* x, bool x_zero);
+  std::vector<std::unique_ptr<Level>> levels_;
+  std::unique_ptr<CoarseAssembly> assembly_;
+  CoarseSolver coarse_;
+  int pre_ = 1, post_ = 1, degree_ = 2;
+};
+
+}  // namespace hxg

@@ -1,0 +1,178 @@
+// p-level transfer (Prolongation, multigrid.hpp:25-74): P = diag(1/m_f) E_f^T
+// (C x C x C) E_c with C the 1D coarse-on-fine-GLL tabulation; R = P^T.
+// Element kernels evaluate each output entry with the reference's
+// contraction order; the node-ordered sum (node_kernels.cuh) scatters.
+#include "transfer.hpp"
+
+#include "dispatch.hpp"
+#include "node_kernels.cuh"
+
+namespace hxg {
+
+namespace {
+
+struct TransferParams {
+  BoxDev fine, coarse;
+  const double* ctof;  // Nf x Nc
+  const double* in;    // L-vector (coarse for prolong, fine for restrict)
+  double* evec;        // output E-vector (fine for prolong, coarse for restrict)
+};
+
+__device__ __forceinline__ long long lattice_node(const BoxDev& b, long long e, int i, int j, int k) {
+  long long ex = e % b.cells[0], ey = (e / b.cells[0]) % b.cells[1],
+            ez = e / ((long long)b.cells[0] * b.cells[1]);
+  return (b.p * ex + i) + b.npd[0] * ((b.p * ey + j) + (long long)b.npd[1] * (b.p * ez + k));
+}
+
+// Multiplicity of a lattice node (build_restriction, mesh.hpp:136-137).
+__device__ __forceinline__ int multiplicity(const BoxDev& b, long long node) {
+  int g[3] = {(int)(node % b.npd[0]), (int)((node / b.npd[0]) % b.npd[1]),
+              (int)(node / ((long long)b.npd[0] * b.npd[1]))};
+  int m = 1;
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    if (g[d] % b.p == 0 && g[d] > 0 && g[d] < b.npd[d] - 1) m *= 2;
+  return m;
+}
+
+// Prolong: out[e][c][k][j][i] = sum_kc C[k][kc] sum_jc C[j][jc] sum_ic C[i][ic] xc[..]
+template <int NF, int NC>
+__global__ void prolong_element_kernel(TransferParams prm) {
+  constexpr int NF3 = NF * NF * NF, NC3 = NC * NC * NC;
+  long long total = prm.fine.num_elements() * 3 * NF3;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < total;
+       r += (long long)gridDim.x * blockDim.x) {
+    long long e = r / (3 * NF3);
+    int rem = (int)(r % (3 * NF3));
+    int c = rem / NF3, a = rem % NF3;
+    int i = a % NF, j = (a / NF) % NF, k = a / (NF * NF);
+    double xc[NC3];
+#pragma unroll
+    for (int kc = 0; kc < NC; ++kc)
+#pragma unroll
+      for (int jc = 0; jc < NC; ++jc)
+#pragma unroll
+        for (int ic = 0; ic < NC; ++ic)
+          xc[(kc * NC + jc) * NC + ic] = prm.in[3 * lattice_node(prm.coarse, e, ic, jc, kc) + c];
+    double out = 0.0;
+#pragma unroll
+    for (int kc = 0; kc < NC; ++kc) {
+      double t2 = 0.0;
+#pragma unroll
+      for (int jc = 0; jc < NC; ++jc) {
+        double t1 = 0.0;
+#pragma unroll
+        for (int ic = 0; ic < NC; ++ic) t1 += prm.ctof[i * NC + ic] * xc[(kc * NC + jc) * NC + ic];
+        t2 += prm.ctof[j * NC + jc] * t1;
+      }
+      out += prm.ctof[k * NC + kc] * t2;
+    }
+    prm.evec[(e * 3 + c) * NF3 + a] = out;
+  }
+}
+
+// Restrict (exact transpose, contraction order z, y, x as apply_transpose):
+// out[e][c][kc][jc][ic] = sum_if C[if][ic] sum_jf C[jf][jc] sum_kf C[kf][kc] s[..]
+// with s = x_f / m_f gathered on the fine lattice.
+template <int NF, int NC>
+__global__ void restrict_element_kernel(TransferParams prm) {
+  constexpr int NC3 = NC * NC * NC;
+  long long total = prm.coarse.num_elements() * 3 * NC3;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < total;
+       r += (long long)gridDim.x * blockDim.x) {
+    long long e = r / (3 * NC3);
+    int rem = (int)(r % (3 * NC3));
+    int c = rem / NC3, a = rem % NC3;
+    int ic = a % NC, jc = (a / NC) % NC, kc = a / (NC * NC);
+    double out = 0.0;
+#pragma unroll
+    for (int iff = 0; iff < NF; ++iff) {
+      double t2 = 0.0;
+#pragma unroll
+      for (int jf = 0; jf < NF; ++jf) {
+        double t1 = 0.0;
+#pragma unroll
+        for (int kf = 0; kf < NF; ++kf) {
+          long long node = lattice_node(prm.fine, e, iff, jf, kf);
+          double s = prm.in[3 * node + c] * (1.0 / (double)multiplicity(prm.fine, node));
+          t1 += prm.ctof[kf * NC + kc] * s;
+        }
+        t2 += prm.ctof[jf * NC + jc] * t1;
+      }
+      out += prm.ctof[iff * NC + ic] * t2;
+    }
+    prm.evec[(e * 3 + c) * NC3 + a] = out;
+  }
+}
+
+template <class F>
+void dispatch_transfer(int pf, int pc, F&& f) {
+  switch (pf * 10 + pc) {
+    case 21: f(IC<3>{}, IC<2>{}); return;
+    case 31: f(IC<4>{}, IC<2>{}); return;
+    case 32: f(IC<4>{}, IC<3>{}); return;
+    case 41: f(IC<5>{}, IC<2>{}); return;
+    case 42: f(IC<5>{}, IC<3>{}); return;
+    case 43: f(IC<5>{}, IC<4>{}); return;
+    default:
+      throw Error(HXG_ERR_UNSUPPORTED, "unsupported transfer orders");
+  }
+}
+
+}  // namespace
+
+Transfer::Transfer(const int cells[3], int fine_order, int coarse_order)
+    : pf_(fine_order), pc_(coarse_order) {
+  fine_ = make_box(cells, fine_order);
+  coarse_ = make_box(cells, coarse_order);
+  std::vector<double> ctof;
+  lagrange_tabulate(gauss_lobatto(coarse_order), gauss_lobatto(fine_order), &ctof, nullptr);
+  ctof_.upload(ctof);
+  dispatch_transfer(pf_, pc_, [](auto, auto) {});
+}
+
+void Transfer::prolong(const double* xc, double* xf, cudaStream_t s) {
+  int nf = pf_ + 1;
+  size_t need = (size_t)fine_.num_elements() * 3 * nf * nf * nf;
+  if (evf_.n != need) evf_.alloc(need);
+  TransferParams prm{fine_, coarse_, ctof_.p, xc, evf_.p};
+  dispatch_transfer(pf_, pc_, [&](auto NFc, auto NCc) {
+    constexpr int NF = decltype(NFc)::value, NC = decltype(NCc)::value;
+    prolong_element_kernel<NF, NC><<<grid_for((long long)need, 128), 128, 0, s>>>(prm);
+  });
+  HXG_CUDA(cudaGetLastError());
+  NodeParams np{};
+  np.box = fine_;
+  np.evec = evf_.p;
+  np.out = xf;
+  np.epilogue = kEpiInvMult;
+  dispatch_p(pf_, [&](auto Pc) {
+    constexpr int P = decltype(Pc)::value;
+    node_sum_kernel<P><<<grid_for(fine_.num_nodes(), 256), 256, 0, s>>>(np);
+  });
+  HXG_CUDA(cudaGetLastError());
+}
+
+void Transfer::restrict_to(const double* xf, double* xc, cudaStream_t s) {
+  int nc = pc_ + 1;
+  size_t need = (size_t)coarse_.num_elements() * 3 * nc * nc * nc;
+  if (evc_.n != need) evc_.alloc(need);
+  TransferParams prm{fine_, coarse_, ctof_.p, xf, evc_.p};
+  dispatch_transfer(pf_, pc_, [&](auto NFc, auto NCc) {
+    constexpr int NF = decltype(NFc)::value, NC = decltype(NCc)::value;
+    restrict_element_kernel<NF, NC><<<grid_for((long long)need, 128), 128, 0, s>>>(prm);
+  });
+  HXG_CUDA(cudaGetLastError());
+  NodeParams np{};
+  np.box = coarse_;
+  np.evec = evc_.p;
+  np.out = xc;
+  np.epilogue = kEpiNone;
+  dispatch_p(pc_, [&](auto Pc) {
+    constexpr int P = decltype(Pc)::value;
+    node_sum_kernel<P><<<grid_for(coarse_.num_nodes(), 256), 256, 0, s>>>(np);
+  });
+  HXG_CUDA(cudaGetLastError());
+}
+
+}  // namespace hxg

@@ -1,0 +1,365 @@
+"""Python mirror of the reference ``hexmg`` operator API over the C-ABI.
+
+Names, argument meaning and error behaviour follow the reference headers
+(/root/reference/proj/include/hexmg): ``MatrixFreeOperator`` (operator.hpp:70),
+``MultigridHierarchy`` / ``build_hierarchy`` (multigrid.hpp:88, :212),
+``cg_solve`` (cg.hpp:81), ``FemProblem`` (problem.hpp:19).  Vectors are CUDA
+``torch.float64`` tensors (torch is only the device-memory plumbing); every
+operation is a call into libhexmg_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import capi
+from .capi import check, lib
+
+FACES = {"-x": 0, "+x": 1, "-y": 2, "+y": 3, "-z": 4, "+z": 5}
+
+
+def _ptr(a) -> ctypes.c_void_p:
+    if isinstance(a, torch.Tensor):
+        return ctypes.c_void_p(a.data_ptr())
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(ctypes.c_void_p)
+    if a is None:
+        return ctypes.c_void_p(None)
+    raise TypeError(type(a))
+
+
+def _dev(t, n=None) -> torch.Tensor:
+    t = torch.as_tensor(t, dtype=torch.float64)
+    if not t.is_cuda:
+        t = t.cuda()
+    t = t.contiguous()
+    if n is not None and t.numel() != n:
+        raise ValueError("nodal field size mismatch")
+    return t
+
+
+@dataclass
+class Basis1D:
+    """basis.hpp:117-130 (host tabulations from the library's setup)."""
+
+    order: int
+    q: int
+    nodes: np.ndarray
+    points: np.ndarray
+    weights: np.ndarray
+    interp: np.ndarray
+    deriv: np.ndarray
+    pinv: np.ndarray
+    colloc: np.ndarray
+
+
+def build_lagrange_basis(p: int, q: int | None = None) -> Basis1D:
+    q = q or p + 1
+    n = p + 1
+    arr = dict(nodes=np.zeros(n), points=np.zeros(q), weights=np.zeros(q), interp=np.zeros((q, n)),
+               deriv=np.zeros((q, n)), pinv=np.zeros((n, q)), colloc=np.zeros((q, q)))
+    check(lib().hxg_setup_basis(p, q, *[_ptr(arr[k]) for k in
+                                        ("nodes", "points", "weights", "interp", "deriv", "pinv",
+                                         "colloc")]))
+    return Basis1D(p, q, **arr)
+
+
+def lame_from_young_poisson(young: float, poisson: float):
+    """material.hpp:27-36."""
+    if not young > 0.0:
+        raise ValueError("Young's modulus must be positive")
+    if poisson == 0.5:
+        raise ValueError("incompressible limit nu = 0.5 is unsupported")
+    if not (-1.0 < poisson < 0.5):
+        raise ValueError("Poisson ratio must lie in (-1, 0.5)")
+    mu = young / (2.0 * (1.0 + poisson))
+    lam = young * poisson / ((1.0 + poisson) * (1.0 - 2.0 * poisson))
+    return mu, lam
+
+
+def num_nodes(cells, order):
+    return (order * cells[0] + 1) * (order * cells[1] + 1) * (order * cells[2] + 1)
+
+
+def geometric_factors(extents, cells, order, q):
+    """compute_geometric_factors (mesh.hpp:193-232): (E, q^3, 3, 3), (E, q^3)."""
+    E = cells[0] * cells[1] * cells[2]
+    dx = np.zeros((E, q**3, 3, 3))
+    w = np.zeros((E, q**3))
+    check(lib().hxg_setup_geometry(_ptr(np.asarray(extents, np.float64)),
+                                   _ptr(np.asarray(cells, np.int32)), order, q, _ptr(dx), _ptr(w)))
+    return dx, w
+
+
+def constraint_mask(cells, order, fixed_faces):
+    """build_constraints (operator.hpp:36-55) for whole-face Dirichlet sets."""
+    m = np.zeros(3 * num_nodes(cells, order), dtype=np.uint8)
+    fm = 0
+    for f in fixed_faces:
+        fm |= 1 << FACES[f]
+    check(lib().hxg_setup_constraints(_ptr(np.asarray(cells, np.int32)), order, fm, _ptr(m)))
+    return m, fm
+
+
+def traction_load(extents, cells, order, q, face, traction):
+    """assemble_traction_load (operator.hpp:381-443)."""
+    load = np.zeros(3 * num_nodes(cells, order))
+    if face is None:
+        return load
+    check(lib().hxg_setup_traction_load(_ptr(np.asarray(extents, np.float64)),
+                                        _ptr(np.asarray(cells, np.int32)), order, q, FACES[face],
+                                        _ptr(np.asarray(traction, np.float64)), _ptr(load)))
+    return load
+
+
+class MatrixFreeOperator:
+    """MatrixFreeOperator (operator.hpp:70-373) on the GPU."""
+
+    def __init__(self, cells, basis: Basis1D, dxidX, weight, mu, lam, mask=None, state=None,
+                 _handle=None):
+        self._owner = _handle is None
+        if _handle is not None:
+            self.h = _handle
+        else:
+            self._keep = [np.ascontiguousarray(basis.interp), np.ascontiguousarray(basis.deriv),
+                          np.ascontiguousarray(basis.colloc)]
+            desc = capi.OpDesc()
+            desc.order, desc.qpts = basis.order, basis.q
+            desc.cells[:] = list(cells)
+            desc.interp, desc.deriv, desc.colloc = [_ptr(a).value for a in self._keep]
+            if dxidX is not None:
+                dx = np.ascontiguousarray(dxidX, np.float64)
+                w = np.ascontiguousarray(weight, np.float64)
+                self._keep += [dx, w]
+                desc.dxidX, desc.weight = _ptr(dx).value, _ptr(w).value
+            desc.mu, desc.lam, desc.storage = mu, lam, 0
+            if mask is not None:
+                m = np.ascontiguousarray(mask, np.uint8)
+                self._keep.append(m)
+                desc.mask = _ptr(m).value
+            h = ctypes.c_void_p()
+            check(lib().hxg_op_create(ctypes.byref(desc), state, ctypes.byref(h)))
+            self.h = h
+        n = ctypes.c_int64()
+        check(lib().hxg_op_size(self.h, ctypes.byref(n)))
+        self._size = n.value
+
+    def __del__(self):
+        if getattr(self, "_owner", False) and getattr(self, "h", None):
+            try:
+                lib().hxg_op_destroy(self.h)
+            except Exception:  # interpreter shutdown
+                pass
+            self.h = None
+
+    def size(self) -> int:
+        return self._size
+
+    def set_external_load(self, load):
+        load = np.ascontiguousarray(load, np.float64) if load is not None else None
+        check(lib().hxg_op_set_external_load(self.h, _ptr(load)))
+
+    def set_load_scale(self, s):
+        check(lib().hxg_op_set_load_scale(self.h, float(s)))
+
+    def set_jacobian_perturbation(self, eps):
+        check(lib().hxg_op_set_jacobian_perturbation(self.h, float(eps)))
+
+    def set_variant(self, v: int):
+        check(lib().hxg_op_set_variant(self.h, int(v)))
+
+    def stored_bytes_per_dof(self) -> float:
+        out = ctypes.c_double()
+        check(lib().hxg_op_stored_bytes_per_dof(self.h, ctypes.byref(out)))
+        return out.value
+
+    def counters(self):
+        r, j = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().hxg_op_counters(self.h, ctypes.byref(r), ctypes.byref(j)))
+        return r.value, j.value
+
+    def apply_residual(self, u, out=None):
+        u = _dev(u, self._size)
+        out = torch.empty_like(u) if out is None else out
+        check(lib().hxg_op_apply_residual(self.h, _ptr(u), _ptr(out)))
+        return out
+
+    def apply_jacobian(self, du, out=None):
+        du = _dev(du, self._size)
+        out = torch.empty_like(du) if out is None else out
+        check(lib().hxg_op_apply_jacobian(self.h, _ptr(du), _ptr(out)))
+        return out
+
+    def apply_jacobian_host(self, du: np.ndarray, out: np.ndarray | None = None):
+        du = np.ascontiguousarray(du, np.float64)
+        out = np.empty_like(du) if out is None else out
+        check(lib().hxg_op_apply_jacobian_host(self.h, _ptr(du), _ptr(out)))
+        return out
+
+    def extract_diagonal(self, out=None):
+        out = torch.empty(self._size, dtype=torch.float64, device="cuda") if out is None else out
+        check(lib().hxg_op_extract_diagonal(self.h, _ptr(out)))
+        return out
+
+    def total_strain_energy(self, u) -> float:
+        u = _dev(u, self._size)
+        e = ctypes.c_double()
+        check(lib().hxg_op_total_strain_energy(self.h, _ptr(u), ctypes.byref(e)))
+        return e.value
+
+    def export_state(self, num_elements, nq):
+        out = np.zeros((num_elements, nq, 17))
+        check(lib().hxg_op_export_state(self.h, _ptr(out)))
+        return out
+
+    def gather(self, u, num_elements, npe):
+        u = _dev(u, self._size)
+        ev = torch.empty(num_elements * 3 * npe, dtype=torch.float64, device="cuda")
+        check(lib().hxg_op_gather(self.h, _ptr(u), _ptr(ev)))
+        return ev
+
+    def scatter_add(self, ev, out):
+        check(lib().hxg_op_scatter_add(self.h, _ptr(_dev(ev)), _ptr(out)))
+        return out
+
+    def time_jacobian(self, x, y, warmup=3, repeats=20) -> float:
+        ms = ctypes.c_double()
+        check(lib().hxg_op_time_jacobian(self.h, _ptr(x), _ptr(y), warmup, repeats, ctypes.byref(ms)))
+        return ms.value
+
+
+class MultigridHierarchy:
+    """MultigridHierarchy + build_hierarchy (multigrid.hpp:88-268)."""
+
+    def __init__(self, fine: MatrixFreeOperator, fixed_face_mask: int, schedule=None,
+                 pre_smooth=1, post_smooth=1):
+        self.fine = fine
+        h = ctypes.c_void_p()
+        sched = None if schedule is None else np.asarray(schedule, np.int32)
+        check(lib().hxg_mg_create(fine.h, fixed_face_mask, _ptr(sched),
+                                  0 if sched is None else len(sched), pre_smooth, post_smooth,
+                                  ctypes.byref(h)))
+        self.h = h
+        n = ctypes.c_int()
+        check(lib().hxg_mg_num_levels(self.h, ctypes.byref(n)))
+        self._levels = n.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib().hxg_mg_destroy(self.h)
+            except Exception:  # interpreter shutdown
+                pass
+            self.h = None
+
+    def num_levels(self):
+        return self._levels
+
+    def level_size(self, k):
+        n = ctypes.c_int64()
+        check(lib().hxg_mg_level_size(self.h, k, ctypes.byref(n)))
+        return n.value
+
+    def level_operator(self, k) -> MatrixFreeOperator:
+        h = ctypes.c_void_p()
+        check(lib().hxg_mg_level_op(self.h, k, ctypes.byref(h)))
+        op = MatrixFreeOperator(None, None, None, None, 0, 0, _handle=h)
+        op._hier = self  # keep the hierarchy alive
+        return op
+
+    def setup_numeric(self):
+        check(lib().hxg_mg_setup_numeric(self.h))
+
+    def lambda_max(self, k):
+        out = ctypes.c_double()
+        check(lib().hxg_mg_lambda_max(self.h, k, ctypes.byref(out)))
+        return out.value
+
+    def prolong(self, coarse_level, xc):
+        xc = _dev(xc, self.level_size(coarse_level))
+        xf = torch.empty(self.level_size(coarse_level + 1), dtype=torch.float64, device="cuda")
+        check(lib().hxg_mg_prolong(self.h, coarse_level, _ptr(xc), _ptr(xf)))
+        return xf
+
+    def restrict_to(self, coarse_level, xf):
+        xf = _dev(xf, self.level_size(coarse_level + 1))
+        xc = torch.empty(self.level_size(coarse_level), dtype=torch.float64, device="cuda")
+        check(lib().hxg_mg_restrict(self.h, coarse_level, _ptr(xf), _ptr(xc)))
+        return xc
+
+    def v_cycle(self, b, x=None):
+        b = _dev(b)
+        x = torch.zeros_like(b) if x is None else x
+        check(lib().hxg_mg_vcycle(self.h, _ptr(b), _ptr(x)))
+        return x
+
+    def smooth(self, k, b, x):
+        check(lib().hxg_mg_smooth(self.h, k, _ptr(_dev(b)), _ptr(x)))
+        return x
+
+    def coarse_csr(self):
+        nnz = ctypes.c_int64()
+        check(lib().hxg_mg_coarse_nnz(self.h, ctypes.byref(nnz)))
+        n = self.level_size(0)
+        rp = np.zeros(n + 1, np.int32)
+        cols = np.zeros(nnz.value, np.int32)
+        vals = np.zeros(nnz.value)
+        check(lib().hxg_mg_coarse_csr_host(self.h, _ptr(rp), _ptr(cols), _ptr(vals)))
+        return rp, cols, vals
+
+    def coarse_solve(self, b):
+        b = _dev(b, self.level_size(0))
+        x = torch.empty_like(b)
+        check(lib().hxg_mg_coarse_solve(self.h, _ptr(b), _ptr(x)))
+        return x
+
+
+def cg_solve(op: MatrixFreeOperator, b, x=None, rtol=1e-8, max_iterations=500,
+             precond="mg", mg: MultigridHierarchy | None = None):
+    """cg_solve (cg.hpp:81-134); precond in {"none", "jacobi", "mg"}."""
+    pc = {"none": 0, "jacobi": 1, "mg": 2}[precond]
+    b = _dev(b, op.size())
+    x = torch.zeros_like(b) if x is None else x
+    rep = capi.CgReport()
+    hist = np.zeros(max_iterations + 2)
+    check(lib().hxg_cg_solve(op.h, mg.h if mg is not None else None, pc, _ptr(b), _ptr(x), rtol,
+                             max_iterations, ctypes.byref(rep), _ptr(hist), len(hist)))
+    return dict(x=x, iterations=rep.iterations, converged=bool(rep.converged),
+                eig_min=rep.eig_min, eig_max=rep.eig_max,
+                history=hist[: rep.iterations + 1].copy())
+
+
+class FemProblem:
+    """The configured pieces of FemProblem (problem.hpp:19-58): box mesh,
+    basis on q Gauss-Legendre points, geometry, whole-face Dirichlet sets,
+    traction load, operator and (lazily) the p-MG hierarchy."""
+
+    def __init__(self, extents=(1.0, 1.0, 1.0), cells=(2, 2, 2), order=2, q=0,
+                 fixed_faces=("-x",), traction_face=None, traction=(0.0, 0.0, 0.0), young=1.0,
+                 poisson=0.3, geometry=True):
+        self.extents, self.cells, self.order = tuple(extents), tuple(cells), order
+        self.q = q or order + 1
+        self.basis = build_lagrange_basis(order, self.q)
+        self.mu, self.lam = lame_from_young_poisson(young, poisson)
+        self.mask, self.fixed_face_mask = constraint_mask(cells, order, fixed_faces)
+        dx = w = None
+        if geometry:
+            dx, w = geometric_factors(extents, cells, order, self.q)
+        self.op = MatrixFreeOperator(cells, self.basis, dx, w, self.mu, self.lam, self.mask)
+        self.load = traction_load(extents, cells, order, self.q, traction_face, traction)
+        self.op.set_external_load(self.load)
+        self.num_elements = cells[0] * cells[1] * cells[2]
+        self.nq = self.q**3
+        self._mg = None
+
+    def size(self):
+        return self.op.size()
+
+    @property
+    def hierarchy(self) -> MultigridHierarchy:
+        if self._mg is None:
+            self._mg = MultigridHierarchy(self.op, self.fixed_face_mask)
+        return self._mg

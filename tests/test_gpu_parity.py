@@ -1,0 +1,209 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the golden
+fixtures generated from the unmodified reference, and against the numpy
+oracle.  Tolerances: 1e-12 relative L2 on applies (BASELINE.json north_star),
+CG iteration counts within +-1."""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import hexmg_np as H  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def problem(name):
+    from paper_2204_01722_b200.hexmg import FemProblem
+    g = np.load(os.path.join(GOLD, f"{name}.npz"))
+    meta = g["meta"]
+    order = int(meta[0])
+    cells = tuple(int(c) for c in meta[1:4])
+    ext = tuple(float(e) for e in meta[4:7])
+    prob = FemProblem(extents=ext, cells=cells, order=order, fixed_faces=("-x",),
+                      traction_face="+x", traction=(0.0, 0.0, -0.02))
+    return prob, g
+
+
+NAMES = ["q1_bar", "q2_bar", "q3_cube", "q4_cube"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("variant", [0, 1])
+def test_operator_parity(name, variant):
+    prob, g = problem(name)
+    prob.op.set_variant(variant)
+    f = prob.op.apply_residual(cuda(g["u"]))
+    assert rel(f, g["f"]) < 1e-12
+    st = prob.op.export_state(prob.num_elements, prob.nq)
+    assert np.abs(st - g["state"]).max() < 1e-12
+    assert rel(prob.op.apply_jacobian(cuda(g["x"])), g["jx"]) < 1e-12
+    assert rel(prob.op.extract_diagonal(), g["diag"]) < 1e-12
+
+
+@pytest.mark.parametrize("name", ["q2_bar", "q3_cube", "q4_cube"])
+def test_multigrid_parity(name):
+    prob, g = problem(name)
+    prob.op.apply_residual(cuda(g["u"]))
+    mg = prob.hierarchy
+    mg.setup_numeric()
+    L = mg.num_levels()
+    for k in range(L - 1):
+        assert rel(mg.prolong(k, cuda(g[f"P{k}_xc"])), g[f"P{k}_pxc"]) < 1e-13
+        assert rel(mg.restrict_to(k, cuda(g[f"P{k}_xf"])), g[f"P{k}_rxf"]) < 1e-13
+    for k in range(1, L):
+        assert abs(mg.lambda_max(k) - float(g[f"lam{k}"])) < 1e-11 * float(g[f"lam{k}"])
+        op_k = mg.level_operator(k)
+        n_k = mg.level_size(k)
+        xk = np.cos(0.3 * np.arange(n_k))
+        assert rel(op_k.apply_jacobian(cuda(xk)), g[f"jx_level{k}"]) < 1e-12
+        assert rel(op_k.extract_diagonal(), g[f"diag_level{k}"]) < 1e-12
+    rp, cols, vals = mg.coarse_csr()
+    assert np.array_equal(rp, g["coarse_rowptr"]) and np.array_equal(cols, g["coarse_cols"])
+    assert np.abs(vals - g["coarse_vals"]).max() < 1e-13 * max(1.0, np.abs(g["coarse_vals"]).max())
+    v = mg.v_cycle(cuda(g["vcycle_b"]))
+    assert rel(v, g["vcycle_x"]) < 1e-11
+    from paper_2204_01722_b200.hexmg import cg_solve
+    for tag, rtol in (("1e-3", 1e-3), ("1e-8", 1e-8)):
+        r = cg_solve(prob.op, cuda(g["vcycle_b"]), rtol=rtol, precond="mg", mg=mg)
+        assert abs(r["iterations"] - int(g[f"mgcg_its_{tag}"])) <= 1
+        assert r["converged"]
+        assert rel(r["x"], g[f"mgcg_x_{tag}"]) < 10 * rtol
+        cond = r["eig_max"] / r["eig_min"]
+        assert abs(cond - float(g[f"mgcg_cond_{tag}"])) < 1e-6 * cond
+
+
+def test_cfg1_jacobi_cg():
+    """BASELINE.json configs[0]: Q1 8^3, Jacobi-CG; reference 44 / 72 its."""
+    from paper_2204_01722_b200.hexmg import FemProblem, cg_solve
+    g = np.load(os.path.join(GOLD, "cfg1_q1_8.npz"))
+    prob = FemProblem(extents=(1, 1, 1), cells=(8, 8, 8), order=1, fixed_faces=("-x",),
+                      traction_face="+x", traction=(0.0, 0.0, -0.02))
+    f = prob.op.apply_residual(torch.zeros(prob.size(), dtype=torch.float64, device="cuda"))
+    assert rel(f, g["f0"]) < 1e-12
+    assert rel(prob.op.extract_diagonal(), g["diag"]) < 1e-12
+    for tag, rtol, its in (("1e-3", 1e-3, 44), ("1e-8", 1e-8, 72)):
+        r = cg_solve(prob.op, -f, rtol=rtol, max_iterations=5000, precond="jacobi")
+        assert abs(r["iterations"] - its) <= 1
+        assert rel(r["x"], g[f"x_{tag}"]) < 1e-9
+        # Lanczos Ritz values after tens of iterations are roundoff-sensitive
+        # (the reference's own FMA/no-FMA builds differ).
+        cond = float(g[f"cond_{tag}"])
+        assert abs(r["eig_max"] / r["eig_min"] - cond) < 1e-3 * cond
+
+
+def test_inverted_element_reports_first_point():
+    from paper_2204_01722_b200.capi import InvertedElementError
+    from paper_2204_01722_b200.hexmg import FemProblem
+    cells, order = (3, 2, 2), 2
+    prob = FemProblem(extents=(1, 1, 1), cells=cells, order=order)
+    ref = H.make_problem((1, 1, 1), cells, order)
+    u = 0.4 * np.sin(0.37 * np.arange(prob.size()))
+    with pytest.raises(H.InvertedElementError) as er:
+        ref.op.apply_residual(u)
+    with pytest.raises(InvertedElementError) as eg:
+        prob.op.apply_residual(cuda(u))
+    assert (eg.value.element, eg.value.point) == (er.value.element, er.value.point)
+    assert abs(eg.value.jacobian - er.value.jacobian) < 1e-12
+
+
+def test_state_not_initialized():
+    from paper_2204_01722_b200.capi import StateNotInitializedError
+    from paper_2204_01722_b200.hexmg import FemProblem
+    prob = FemProblem(cells=(2, 2, 2), order=2)
+    with pytest.raises(StateNotInitializedError):
+        prob.op.apply_jacobian(torch.zeros(prob.size(), dtype=torch.float64, device="cuda"))
+    with pytest.raises(StateNotInitializedError):
+        prob.op.extract_diagonal()
+
+
+def test_energy_and_gather_scatter():
+    from paper_2204_01722_b200.hexmg import FemProblem
+    cells, order = (3, 2, 2), 3
+    prob = FemProblem(extents=(1, 1, 1), cells=cells, order=order)
+    ref = H.make_problem((1, 1, 1), cells, order)
+    u = 1e-2 * np.cos(np.arange(prob.size()) * 0.01)
+    u[ref.op.mask != 0] = 0
+    # energy vs oracle restatement of total_strain_energy (operator.hpp:287-315)
+    ev = H.gather(ref.op.idx, u, ref.basis.n)
+    G = H._qgrad_to_pts(H.grad_ref(ref.basis, ev))
+    gu = G @ ref.op.dxidX
+    F = np.eye(3) + gu
+    J = np.linalg.det(F)
+    psi = 0.5 * ref.lam * np.log(J) ** 2 - ref.mu * np.log(J) + ref.mu * 0.5 * ((F * F).sum((-1, -2)) - 3)
+    e_ref = (ref.op.weight * psi).sum()
+    assert abs(prob.op.total_strain_energy(cuda(u)) - e_ref) < 1e-12 * abs(e_ref)
+    # restriction round trip E^T E u = m * u (verify.hpp:122-137)
+    npe = (order + 1) ** 3
+    evd = prob.op.gather(cuda(u), prob.num_elements, npe)
+    out = torch.zeros(prob.size(), dtype=torch.float64, device="cuda")
+    prob.op.scatter_add(evd, out)
+    mult = np.bincount(ref.op.idx.ravel(), minlength=ref.mesh.num_nodes)
+    assert np.abs(out.cpu().numpy() - np.repeat(mult, 3) * u).max() < 1e-15
+
+
+def test_jacobian_perturbation_hook_breaks_fd():
+    """verify.hpp:20-25 fault injection: the perturbed Jacobian must fail the
+    central-difference check, the unperturbed one must pass it."""
+    from paper_2204_01722_b200.hexmg import FemProblem
+    prob = FemProblem(extents=(2, 1, 1), cells=(2, 1, 1), order=2, traction_face="+x",
+                      traction=(0, 0, -0.02))
+    n = prob.size()
+    rng = np.random.RandomState(31)
+    u = 0.02 * rng.uniform(-1, 1, n)
+    u[prob.mask != 0] = 0
+    du = rng.uniform(-1, 1, n)
+    du[prob.mask != 0] = 0
+    h = 1e-6
+
+    def fd_err(eps):
+        prob.op.set_jacobian_perturbation(eps)
+        prob.op.apply_residual(cuda(u))
+        ju = prob.op.apply_jacobian(cuda(du)).cpu().numpy()
+        fp = prob.op.apply_residual(cuda(u + h * du)).cpu().numpy()
+        fm = prob.op.apply_residual(cuda(u - h * du)).cpu().numpy()
+        return np.linalg.norm((fp - fm) / (2 * h) - ju) / np.linalg.norm(ju)
+
+    assert fd_err(0.0) < 1e-6
+    assert fd_err(1e-3) > 1e-6
+    prob.op.set_jacobian_perturbation(0.0)
+
+
+@pytest.mark.parametrize("order,n", [(2, 64), (3, 43), (4, 32)])
+def test_full_size_properties(order, n):
+    """BASELINE sizes: symmetry, linearity, A.0 = 0, run-to-run bitwise
+    determinism, fused == two-pass, and one random element spot-checked
+    against the oracle's dense element action."""
+    from paper_2204_01722_b200.hexmg import FemProblem
+    prob = FemProblem(extents=(1, 1, 1), cells=(n, n, n), order=order, geometry=True)
+    N = prob.size()
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    u = torch.zeros(N, dtype=torch.float64, device="cuda")
+    prob.op.apply_residual(u)
+    x = torch.rand(N, generator=gen, device="cuda", dtype=torch.float64) - 0.5
+    y = torch.rand(N, generator=gen, device="cuda", dtype=torch.float64) - 0.5
+    ax = prob.op.apply_jacobian(x)
+    ay = prob.op.apply_jacobian(y)
+    g1, g2 = torch.dot(ax, y).item(), torch.dot(x, ay).item()
+    assert abs(g1 - g2) < 1e-11 * max(1.0, abs(g1))
+    a2 = prob.op.apply_jacobian(2.0 * x - 3.0 * y)
+    assert (a2 - (2.0 * ax - 3.0 * ay)).norm().item() < 1e-12 * a2.norm().item()
+    z = prob.op.apply_jacobian(torch.zeros_like(x))
+    assert z.abs().max().item() == 0.0
+    ax2 = prob.op.apply_jacobian(x)
+    assert torch.equal(ax, ax2)
+    prob.op.set_variant(1)
+    ax3 = prob.op.apply_jacobian(x)
+    prob.op.set_variant(0)
+    assert (ax3 - ax).norm().item() < 1e-13 * ax.norm().item()
