@@ -1,0 +1,348 @@
+"""Benchmark: FP64 Neo-Hookean Q2 matrix-free Jacobian apply (BASELINE.json
+metric, configs[1]: Q2 hex cube 64^3 elements per GPU), GDoF/s.
+
+One step = one Jacobian apply y = J x over the whole mesh (operator.hpp:184,
+the reference perf-harness unit, study.hpp:203-212), linearised at u = 0 with
+Dirichlet lifting on -x like the harness (study.hpp:198-201), x_i = 1e-3
+sin(0.7 i).  N GPUs: weak scaling, the box is split into N slabs along x
+(64^3 elements each) and the shared interface planes are summed over NCCL
+after every apply (the halo exchange of SURVEY.md §8(e)).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0 (contract in the task statement): value is the
+device-timed whole-job GDoF/s; e2e is the same metric through the C-ABI
+host-buffer entry point (hxg_op_apply_jacobian_host: H2D of x, apply, D2H of
+y); roofline / cpu_baseline / clocks as documented in DESIGN.md.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 Q2 Neo-Hookean matrix-free Jacobian apply throughput"
+UNIT = "GDoF/s"
+ORDER, CELLS = 2, 64
+
+
+def algorithmic_bytes(num_elements, q, ndof):
+    """Reference byte model (operator.hpp:137-141 = PAPER.md:476):
+    8 (17 E q^3 + 2 N_dof) per Jacobian apply."""
+    return 8.0 * (17.0 * num_elements * q**3 + 2.0 * ndof)
+
+
+# --------------------------------------------------------------------------
+# clocks (NVML sampled DURING the timed region)
+# --------------------------------------------------------------------------
+_REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    def __init__(self, device_index=0, period=0.005):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.period = period
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for b, n in _REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------
+# CPU baseline / reference arm: the unmodified reference compiled into
+# oracle/_ref (kind "reference"), else the numpy port (kind "port").
+# --------------------------------------------------------------------------
+def cpu_reference_time(order, cells, applies, threads, warmup=1):
+    """Seconds for `applies` Jacobian applies after `warmup`, reference perf
+    harness method (study.hpp:196-212)."""
+    import numpy as np
+    from oracle import ref_lib as R
+    if R.available():
+        rp = R.RefProblem(extents=(1.0, 1.0, 1.0), cells=(cells,) * 3, order=order,
+                          fixed=("-x",), threads=threads)
+        rp.set_threads(threads)
+        u = rp.impose_dirichlet(np.zeros(rp.n))
+        rp.apply_residual(u)
+        x = 1e-3 * np.sin(0.7 * np.arange(rp.n))
+        sec = rp.time_jacobian(x, warmup=warmup, repeats=applies)
+        return rp.n, sec, "reference", threads
+    from oracle import hexmg_np as H
+    P = H.make_problem((1.0, 1.0, 1.0), (cells,) * 3, order)
+    P.op.apply_residual(np.zeros(P.op.size))
+    x = 1e-3 * np.sin(0.7 * np.arange(P.op.size))
+    for _ in range(warmup):
+        P.op.apply_jacobian(x)
+    t0 = time.perf_counter()
+    for _ in range(applies):
+        P.op.apply_jacobian(x)
+    return P.op.size, time.perf_counter() - t0, "port", 1
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    t_start = time.perf_counter()
+    ndof, sec, kind, cores = cpu_reference_time(ORDER, CELLS, args.steps, threads,
+                                                warmup=args.warmup)
+    value = ndof * args.steps / sec / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (u = 0 linearisation, x_i = 1e-3 sin(0.7 i))",
+        "config": {"workload": f"Q{ORDER} Neo-Hookean cube {CELLS}^3 elements, Jacobian apply",
+                   "order": ORDER, "cells": [CELLS] * 3, "dofs": ndof},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{args.steps} Jacobian applies of the full {CELLS}^3 Q{ORDER} "
+                                   f"problem, {cores} threads (MatrixFreeOperator::set_threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t_start,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def exchange_faces(y, npd, rank, world, dist):
+    """Sum the shared x-interface planes with the neighbouring slabs (NCCL).
+    Both sides add lower-rank partial + upper-rank partial, so the shared
+    entries are bitwise identical on the two ranks."""
+    import torch
+    nx, ny, nz = npd
+    v = y.view(nz, ny, nx, 3)
+    ops, bufs = [], {}
+    if rank + 1 < world:
+        send_hi = v[:, :, nx - 1, :].contiguous()
+        recv_hi = torch.empty_like(send_hi)
+        ops += [dist.P2POp(dist.isend, send_hi, rank + 1), dist.P2POp(dist.irecv, recv_hi, rank + 1)]
+        bufs["hi"] = (send_hi, recv_hi)
+    if rank > 0:
+        send_lo = v[:, :, 0, :].contiguous()
+        recv_lo = torch.empty_like(send_lo)
+        ops += [dist.P2POp(dist.isend, send_lo, rank - 1), dist.P2POp(dist.irecv, recv_lo, rank - 1)]
+        bufs["lo"] = (send_lo, recv_lo)
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    if "hi" in bufs:
+        s, r = bufs["hi"]
+        v[:, :, nx - 1, :] = s + r
+    if "lo" in bufs:
+        s, r = bufs["lo"]
+        v[:, :, 0, :] = r + s
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    from paper_2204_01722_b200.hexmg import FemProblem
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    # Slab `rank` of a (64 N) x 64 x 64 box; only the global -x face is fixed.
+    fixed = ("-x",) if rank == 0 else ()
+    prob = FemProblem(extents=(1.0, 1.0, 1.0), cells=(CELLS,) * 3, order=ORDER, fixed_faces=fixed)
+    op = prob.op
+    N = prob.size()
+    npd = (ORDER * CELLS + 1,) * 3
+    u = torch.zeros(N, dtype=torch.float64, device="cuda")
+    op.apply_residual(u)  # linearisation state at u = 0 (study.hpp:198-201)
+    gidx = torch.arange(N, dtype=torch.float64, device="cuda") + rank * N
+    x = 1e-3 * torch.sin(0.7 * gidx)
+    y = torch.empty_like(x)
+    ndof_job = N * world  # per-rank DoF incl. the shared planes, as study.hpp:196 counts
+    stream = torch.cuda.current_stream()
+
+    def step():
+        op.apply_jacobian(x, y)
+        if dist is not None:
+            exchange_faces(y, npd, rank, world, dist)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local_rank)
+    with sampler:
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        end.record(stream)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    ms_per_step = ms / args.steps
+    value = ndof_job / (ms_per_step * 1e-3) / 1e9
+
+    # Dominant kernel: the apply itself (one fused kernel), timed per launch
+    # with events on the launching stream.
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(20)]
+    for a, b in ev:
+        a.record(stream)
+        op.apply_jacobian(x, y)
+        b.record(stream)
+    torch.cuda.synchronize()
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    alg_bytes = algorithmic_bytes(prob.num_elements, prob.q, N)
+    achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_apply_summary.json")))
+        traffic = prof.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # End-to-end through the C-ABI host-buffer entry point (pinned host x/y).
+    xh = x.cpu().pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    xh_np, yh_np = xh.numpy(), yh.numpy()
+    for _ in range(2):
+        op.apply_jacobian_host(xh_np, yh_np)
+    torch.cuda.synchronize()
+    e2e_steps = max(5, min(args.steps, 50))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        op.apply_jacobian_host(xh_np, yh_np)
+        if dist is not None:
+            yd = yh.cuda(non_blocking=False)
+            exchange_faces(yd, npd, rank, world, dist)
+            yh.copy_(yd)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = t.item()
+    e2e_value = ndof_job / e2e_s / 1e9
+
+    # CPU baseline: the reference on the host cores, rank 0, N = 1 only.
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        try:
+            ndof_c, sec, kind, cores = cpu_reference_time(ORDER, CELLS, args.cpu_applies, threads)
+            cpu = {"value": ndof_c * args.cpu_applies / sec / 1e9, "unit": UNIT, "cores": cores,
+                   "kind": kind,
+                   "sample": f"{args.cpu_applies} Jacobian applies of the same {CELLS}^3 "
+                             f"Q{ORDER} problem after 1 warm-up, {cores} threads"}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (u = 0 linearisation, x_i = 1e-3 sin(0.7 i))",
+            "config": {"workload": f"Q{ORDER} Neo-Hookean cube {CELLS}^3 elements per GPU, "
+                                   "Jacobian apply", "order": ORDER, "q": prob.q,
+                       "cells_per_gpu": [CELLS] * 3, "dofs_per_gpu": N,
+                       "parallelism": f"slab x{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (state 963 MB/GPU)",
+                       "bytes_per_dof_model": alg_bytes / N},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel_ms": kern_ms, "algorithmic_bytes": alg_bytes,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * N,
+                    "d2h_bytes_per_step": 8 * N, "ms_per_step": e2e_s * 1e3,
+                    "path": "hxg_op_apply_jacobian_host (pinned host buffers)"},
+            "gpu_launches": args.steps * op.kernel_launches(),
+            "clocks": sampler.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-applies", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        print(json.dumps({"error": "launch N>1 under torch.distributed.run"}))
+        return
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

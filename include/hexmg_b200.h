@@ -123,6 +123,8 @@ int hxg_op_export_state(hxg_op_t op, double* state_host);
 /* Apply kernel variant: 0 = fused brick kernel (default), 1 = two-pass
  * (element kernel + node-ordered sum; reference summation order). */
 int hxg_op_set_variant(hxg_op_t op, int variant);
+/* Number of kernels one Jacobian apply launches with the current variant. */
+int hxg_op_kernel_launches(hxg_op_t op, int* n);
 
 /* ElementRestriction gather / scatter_add (mesh.hpp:88-116) on the
  * operator's lattice: E-vector layout (e, c, a), x-fastest a. */

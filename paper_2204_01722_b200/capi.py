@@ -104,6 +104,7 @@ SIGNATURES = {
     "hxg_op_total_strain_energy": [_vp, _vp, _P(_d)],
     "hxg_op_export_state": [_vp, _vp],
     "hxg_op_set_variant": [_vp, _i],
+    "hxg_op_kernel_launches": [_vp, _P(_i)],
     "hxg_op_gather": [_vp, _vp, _vp],
     "hxg_op_scatter_add": [_vp, _vp, _vp],
     "hxg_mg_create": [_vp, _i, _vp, _i, _i, _i, _vp],

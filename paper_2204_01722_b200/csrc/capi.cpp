@@ -139,6 +139,9 @@ int hxg_op_counters(hxg_op_t op, int64_t* r, int64_t* j) {
   });
 }
 int hxg_op_set_variant(hxg_op_t op, int v) { return guarded([&] { OP(op).set_variant(v); }); }
+int hxg_op_kernel_launches(hxg_op_t op, int* n) {
+  return guarded([&] { *n = OP(op).kernel_launches(); });
+}
 
 int hxg_op_apply_residual(hxg_op_t op, const double* u, double* f) {
   return guarded([&] { OP(op).apply_residual(u, f); });

@@ -4,6 +4,7 @@
 
 namespace hxg {
 bool fused_supported(int, int) { return false; }
+int fused_launches(int, int) { return 1; }
 void fused_jacobian(Operator&, const double*, double*) {
   throw Error(HXG_ERR_UNSUPPORTED, "fused apply not available");
 }

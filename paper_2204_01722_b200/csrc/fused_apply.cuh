@@ -4,5 +4,6 @@
 namespace hxg {
 class Operator;
 bool fused_supported(int p, int q);
+int fused_launches(int p, int q);
 void fused_jacobian(Operator& op, const double* du, double* y);
 }  // namespace hxg

@@ -183,6 +183,10 @@ void Operator::apply_residual(const double* u, double* f) {
   launch_node_sum(evec_.p, f, nullptr, kEpiResidual);
 }
 
+int Operator::kernel_launches() const {
+  return (variant_ == 0 && fused_supported(p_, q_)) ? fused_launches(p_, q_) : 2;
+}
+
 void Operator::apply_jacobian(const double* du, double* y) {
   if (!state_->valid) throw Error(HXG_ERR_STATE_NOT_INITIALIZED,
                                   "quadrature state not initialized: evaluate the residual at the "

@@ -89,6 +89,7 @@ class Operator {
   void set_jacobian_perturbation(double eps) { perturb_ = eps; }
   void set_variant(int v) { variant_ = v; }
   int variant() const { return variant_; }
+  int kernel_launches() const;
 
   double stored_bytes_per_dof() const;
   long long residual_applies() const { return residual_applies_; }

@@ -171,6 +171,11 @@ class MatrixFreeOperator:
     def set_variant(self, v: int):
         check(lib().hxg_op_set_variant(self.h, int(v)))
 
+    def kernel_launches(self) -> int:
+        n = ctypes.c_int()
+        check(lib().hxg_op_kernel_launches(self.h, ctypes.byref(n)))
+        return n.value
+
     def stored_bytes_per_dof(self) -> float:
         out = ctypes.c_double()
         check(lib().hxg_op_stored_bytes_per_dof(self.h, ctypes.byref(out)))
