@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-library_path = os.path.join(_HERE, "libhexmg_b200.so")
+library_path = os.environ.get("HXG_LIBRARY", os.path.join(_HERE, "libhexmg_b200.so"))
 
 HXG_OK = 0
 ERR_GENERIC = 1

@@ -31,7 +31,9 @@ struct Dims {
 // Forward: nodal U (N^3, x-fastest) of one component -> reference gradient
 // g[d][qz] at this thread's column.  interp (x, y, z), then the collocated
 // derivative per direction (basis.hpp:319-335).
-template <int P, int Q>
+// U(k, j, i) = U[k * KS + j * JS + i * IS]: compact per-element storage
+// (KS, JS, IS) = (N^2, N, 1) or a view into a brick node block.
+template <int P, int Q, int KS = (P + 1) * (P + 1), int JS = P + 1, int IS = 1>
 __device__ __forceinline__ void grad_column(const double* __restrict__ sB,
                                             const double* __restrict__ sD,
                                             const double* U, double* S1, double* S2, int qx,
@@ -39,11 +41,15 @@ __device__ __forceinline__ void grad_column(const double* __restrict__ sB,
   constexpr int N = P + 1;
   // x: S1[k][j][a] = sum_i B[a][i] U[k][j][i]
   if (qy < N) {
+    double b[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) b[i] = sB[qx * N + i];
+    const double* Uj = U + qy * JS;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       double s = 0.0;
 #pragma unroll
-      for (int i = 0; i < N; ++i) s += sB[qx * N + i] * U[(k * N + qy) * N + i];
+      for (int i = 0; i < N; ++i) s += b[i] * Uj[k * KS + i * IS];
       S1[(k * N + qy) * Q + qx] = s;
     }
   }

@@ -105,6 +105,8 @@ class Operator {
   // Element matrices (e, 3N^3, 3N^3) of the assembled operator.
   void element_matrices(double* out);
 
+  friend void fused_jacobian(Operator& op, const double* du, double* y);
+
  private:
   void launch_element(int mode, const double* x, bool mask_input);
   void launch_node_sum(const double* evec, double* out, const double* x, int epilogue);
@@ -123,6 +125,7 @@ class Operator {
   DevBuf<uint8_t> mask_;
   DevBuf<double> load_;
   DevBuf<double> evec_;    // E-vector scratch for the two-pass path
+  DevBuf<double> partial_; // brick-boundary partial sums for the fused path
   DevBuf<unsigned long long> fail_;
   std::shared_ptr<State> state_;
   std::shared_ptr<Geometry> geometry_;
