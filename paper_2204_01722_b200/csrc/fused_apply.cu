@@ -3,24 +3,34 @@
 //
 // One CTA per brick of BX x BY x BZ elements (the QLayout brick), one thread
 // per quadrature column (element, qx, qy):
-//   1. the brick's node block of x is loaded once (coalesced rows, masked
-//      entries zeroed: operator.hpp:189-193) into shared memory;
-//   2. per element: sum-factorised gradient (basis.hpp:319-335), Neo-Hookean
-//      Jacobian q-function on the streamed 17-scalar state
-//      (material.hpp:179-194), transpose (basis.hpp:339-355);
-//   3. element outputs are summed per node inside the brick in a fixed
-//      element order (scatter_add, mesh.hpp:105-116);
+//   1. the brick's node block of x is loaded once (coalesced rows; masked
+//      entries zeroed, operator.hpp:189-193) into shared memory, one plane
+//      per component;
+//   2. per element, all three components per phase: sum-factorised gradient
+//      (basis.hpp:319-335) with every contraction reading its operand rows
+//      from registers, Neo-Hookean Jacobian q-function on the streamed
+//      17-scalar state (material.hpp:179-194), exact transpose
+//      (basis.hpp:339-355);
+//   3. the element patches are overlap-added onto the brick's node block,
+//      separably in x, y, z, in a fixed order (scatter_add, mesh.hpp:105-116);
 //   4. nodes interior to the brick are final and stored to y (constrained
 //      entries pass x through, operator.hpp:212-214); nodes on brick
 //      boundary planes store their partial sum to a per-brick buffer;
 //   5. a light second kernel sums the boundary partials of the (<= 8)
 //      bricks sharing each such node in increasing brick order.
-// Both steps use fixed summation orders, so y is bitwise reproducible.
+// Every sum has a fixed order, so y is bitwise reproducible run to run.
 #include "fused_apply.cuh"
 
 #include "apply_kernels.cuh"
 #include "dispatch.hpp"
 #include "operator.hpp"
+
+#ifndef HXG_EXPERIMENT
+#define HXG_EXPERIMENT 0
+#endif
+#ifndef HXG_FUSED_MINB
+#define HXG_FUSED_MINB 2
+#endif
 
 namespace hxg {
 
@@ -32,35 +42,39 @@ struct FusedParams {
   const double* x;
   double* y;
   const uint8_t* mask;
-  const double* tab;
+  const double* tab;  // B (Q x N) then Dc (Q x Q)
   const double* state;
   double mu, lambda, perturb;
   double* partial;
+  // Uniform copies of the 1D tables for the z-direction contractions
+  // (constant-bank operands).
+  double B[kMaxQ * (kMaxP + 1)];
+  double Dc[kMaxQ * kMaxQ];
 };
 
 template <int P, int Q>
 struct FDims : Dims<P, Q> {
   using D = Dims<P, Q>;
+  static constexpr int N = P + 1;
   static constexpr int NBX = P * D::BX + 1, NBY = P * D::BY + 1, NBZ = P * D::BZ + 1;
   static constexpr int NB = NBX * NBY * NBZ;  // nodes per (full) brick block
+  static constexpr int A = 3 * D::Q3;         // per-element slab A / B (3 components)
   static constexpr int EO = 3 * D::N3;        // element outputs [c][k][j][i]
-  static constexpr int ELEM = EO + 2 * D::Q3; // per-element shared scratch
-  // Separable overlap-add buffers (x pass, y pass).
-  static constexpr int AXN = D::BZ * D::BY * 3 * D::N * D::N * NBX;
-  static constexpr int AYN = D::BZ * 3 * D::N * NBY * NBX;
-  static constexpr int SMEM = D::TAB + NB * 3 + D::NE * ELEM + AXN + AYN;
-};
-
-// Minimum resident CTAs per SM requested from ptxas (register budget).
-#ifndef HXG_EXPERIMENT
-#define HXG_EXPERIMENT 0
-#endif
-#ifndef HXG_FUSED_MINB
-#define HXG_FUSED_MINB 2
-#endif
-template <int Q>
-struct MinBlocks {
-  static constexpr int value = HXG_FUSED_MINB;
+  // Element stride == Q^2 (mod 16 doubles): a thread's slab address is then
+  // == its thread index (mod 16) for the column-contiguous accesses, so every
+  // half-warp hits 16 distinct bank pairs (conflict-free 64-bit accesses).
+  static constexpr int ELEM0 = 2 * A + EO;
+  static constexpr int ELEM = ELEM0 + (((D::Q2 - ELEM0) % 16) + 16) % 16;
+  // Overlap-add rows (NBX doubles each) packed into the elements' A/B
+  // slabs, which are free by then: RPS rows per slab.
+  static constexpr int RX = D::BZ * D::BY * 3 * N * N;  // x-pass rows [lz][ly][c][k][j]
+  static constexpr int RY = D::BZ * 3 * N * NBY;        // y-pass rows [lz][c][k][iy]
+  static constexpr int RPS = 2 * A / NBX;
+  static_assert(RX + RY <= D::NE * RPS, "overlap-add rows must fit the element slabs");
+  static constexpr int SMEM = D::TAB + 3 * NB + D::NE * ELEM;
+  // Register cap for two resident CTAs per SM.
+  static constexpr int REGS0 = 65536 / (HXG_FUSED_MINB * ((D::T + 31) / 32 * 32)) / 8 * 8 - 8;
+  static constexpr int REGS = REGS0 > 255 ? 255 : REGS0;
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
@@ -68,15 +82,17 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
 }
 
 template <int P, int Q>
-__global__ void __launch_bounds__(Dims<P, Q>::T, MinBlocks<Q>::value)
-    fused_jacobian_kernel(FusedParams prm) {
+__global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
+    fused_jacobian_kernel(const __grid_constant__ FusedParams prm) {
   using D = FDims<P, Q>;
-  constexpr int N = D::N, N3 = D::N3, T = D::T;
-  constexpr int NBX = D::NBX, NBY = D::NBY, NB = D::NB, ROW3 = 3 * NBX;
+  constexpr int N = D::N, N3 = D::N3, Q3 = D::Q3, T = D::T;
+  constexpr int NBX = D::NBX, NBY = D::NBY, NB = D::NB;
+  constexpr int BX = D::BX, BY = D::BY, BZ = D::BZ;
   extern __shared__ double smem[];
-  double* sB = smem;
-  double* sD = smem + Q * N;
-  double* Xs = smem + D::TAB;  // node block [iz][iy][ix][c]
+  const double* sB = smem;          // Q x N
+  const double* sD = smem + Q * N;  // Q x Q
+  double* Xs = smem + D::TAB;       // node block [c][iz][iy][ix]
+  double* Ebase = Xs + 3 * NB;      // per-element slabs
   const int tid = threadIdx.x;
   const int brick = blockIdx.x;
   const QLayout& lay = prm.lay;
@@ -86,50 +102,123 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, MinBlocks<Q>::value)
   // The brick's quadrature state is one contiguous run: start pulling it
   // into L2 now so the q-function loads below hit L2.
   const double* st_brick = prm.state + (size_t)lay.brick_points() * brick * kStateStride;
+#if HXG_EXPERIMENT != 1
   if (tid == 0) {
     constexpr unsigned bytes = (unsigned)(sizeof(double) * Q * kStateStride * T);
     constexpr unsigned chunk = 32768;
 #pragma unroll
     for (unsigned off = 0; off < bytes; off += chunk)
-      prefetch_l2(reinterpret_cast<const char*>(st_brick) + off, off + chunk <= bytes ? chunk : bytes - off);
+      prefetch_l2(reinterpret_cast<const char*>(st_brick) + off,
+                  off + chunk <= bytes ? chunk : bytes - off);
   }
-  // Elements of this brick (clipped at the domain) and its node block.
-  const int ecx = min(D::BX, box.cells[0] - bx * D::BX);
-  const int ecy = min(D::BY, box.cells[1] - by * D::BY);
-  const int ecz = min(D::BZ, box.cells[2] - bz * D::BZ);
+#endif
+  const int ecx = min(BX, box.cells[0] - bx * BX);
+  const int ecy = min(BY, box.cells[1] - by * BY);
+  const int ecz = min(BZ, box.cells[2] - bz * BZ);
   const int nbx = P * ecx + 1, nby = P * ecy + 1, nbz = P * ecz + 1;
   const int npx = box.npd[0], npy = box.npd[1];
-  const int node0 = P * bx * D::BX + npx * (P * by * D::BY + npy * (P * bz * D::BZ));
+  const int node0 = P * bx * BX + npx * (P * by * BY + npy * (P * bz * BZ));
 
   load_tables<P, Q>(prm.tab, smem);
-  // 1. node block of x: rows of 3 * nbx contiguous doubles.
+  // 1. node block of x: global rows of 3 nbx contiguous doubles, stored one
+  // plane per component.
+  constexpr int ROW3 = 3 * NBX;
   for (int r = tid; r < NB * 3; r += T) {
     const int c3 = r % ROW3, row = r / ROW3;
     const int iy = row % NBY, iz = row / NBY;
-    if (c3 < 3 * nbx && iy < nby && iz < nbz) {
+    const int ix = c3 / 3, c = c3 - 3 * ix;
+    if (ix < nbx && iy < nby && iz < nbz) {
       const int dof = 3 * (node0 + npx * (iy + npy * iz)) + c3;
       double v = prm.x[dof];
       if (prm.mask && prm.mask[dof]) v = 0.0;
-      Xs[r] = v;
+      Xs[c * NB + (iz * NBY + iy) * NBX + ix] = v;
+    }
+  }
+  const int le = tid / D::Q2, qx = tid % Q, qy = (tid / Q) % Q;
+  const int lx = le % BX, ly = (le / BX) % BY, lz = le / (BX * BY);
+  const bool valid = lx < ecx && ly < ecy && lz < ecz;
+  double* SA = Ebase + le * D::ELEM;  // 3 Q^3
+  double* SB = SA + D::A;             // 3 Q^3
+  double* EOe = SB + D::A;            // 3 N^3
+  __syncthreads();
+
+  // ---- forward: G = (D (x) B (x) B, ...) U, all components per phase ----
+  // F1: x-contraction T1[c][k][j][a] = sum_i B[a][i] U[c][k][j][i] (slab A).
+  if (qy < N) {
+    double bx_[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) bx_[i] = sB[qx * N + i];
+    const double* Xe = Xs + ((P * lz * NBY + P * ly + qy) * NBX + P * lx);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) s += bx_[i] * Xe[c * NB + k * NBY * NBX + i];
+        SA[((c * N + k) * N + qy) * Q + qx] = s;
+      }
+  }
+  __syncthreads();
+  // F2: y then z in registers; values V[c][qz][b][a] -> slab B; z-derivative.
+  double g[3][3][Q];
+  {
+    double by_[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) by_[j] = sB[qy * N + j];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double t2[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) s += by_[j] * SA[((c * N + k) * N + j) * Q + qx];
+        t2[k] = s;
+      }
+      double v[Q];
+#pragma unroll
+      for (int z = 0; z < Q; ++z) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) s += prm.B[z * N + k] * t2[k];
+        v[z] = s;
+        SB[((c * Q + z) * Q + qy) * Q + qx] = s;
+      }
+#pragma unroll
+      for (int z = 0; z < Q; ++z) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < Q; ++r) s += prm.Dc[z * Q + r] * v[r];
+        g[c][2][z] = s;
+      }
     }
   }
   __syncthreads();
-
-  const int le = tid / D::Q2, qx = tid % Q, qy = (tid / Q) % Q;
-  const int lx = le % D::BX, ly = (le / D::BX) % D::BY, lz = le / (D::BX * D::BY);
-  const bool valid = lx < ecx && ly < ecy && lz < ecz;
-  double* EOe = smem + D::TAB + D::NB * 3 + le * D::ELEM;
-  double* S1 = EOe + D::EO;
-  double* S2 = S1 + D::Q3;
-  // 2. gradient straight from the node block (no per-element copy).
-  const double* Xe = Xs + ((P * lz * NBY + P * ly) * NBX + P * lx) * 3;
-  double g[3][3][Q];
+  // F3: x and y collocated derivatives from slab B.
+  {
+    double dx_[Q], dy_[Q];
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
-    grad_column<P, Q, NBY * NBX * 3, NBX * 3, 3>(sB, sD, Xe + c, S1, S2, qx, qy, g[c]);
-  __syncthreads();
+    for (int r = 0; r < Q; ++r) {
+      dx_[r] = sD[qx * Q + r];
+      dy_[r] = sD[qy * Q + r];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int z = 0; z < Q; ++z) {
+        double sx = 0.0, sy = 0.0;
+#pragma unroll
+        for (int r = 0; r < Q; ++r) {
+          sx += dx_[r] * SB[((c * Q + z) * Q + qy) * Q + r];
+          sy += dy_[r] * SB[((c * Q + z) * Q + r) * Q + qx];
+        }
+        g[c][0][z] = sx;
+        g[c][1][z] = sy;
+      }
+  }
 
-  // 3. q-function on the streamed state.
+  // ---- q-function on the streamed state --------------------------------
   const double* sp0 = st_brick + tid;
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
@@ -140,7 +229,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, MinBlocks<Q>::value)
 #pragma unroll
       for (int s = 0; s < kStateStride; ++s) {
 #if HXG_EXPERIMENT == 1
-        st[s] = 1.0 + 0.01 * s + 1e-3 * tid;  // compute-only timing experiment
+        st[s] = 1.0 + 0.01 * s + 1e-3 * tid + 0.0 * sp[0];
 #else
         st[s] = __ldcs(sp + s * T);
 #endif
@@ -164,76 +253,148 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, MinBlocks<Q>::value)
 #pragma unroll
       for (int d = 0; d < 3; ++d) g[c][d][qz] = H[3 * c + d];
   }
+  __syncthreads();  // slabs A/B free
 
-  // 4. transpose into per-element outputs [c][k][j][i].
-  // Padding elements of a clipped brick contribute exact zeros.
+  // ---- backward: exact adjoint ------------------------------------------
+  // B1: Hx -> A, Hy -> B.
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    double* Oc = EOe + c * N3;
-    grad_transpose_column<P, Q>(sB, sD, S1, S2, qx, qy, g[c], [&](int k, int j, int i, double v) {
-      Oc[(k * N + j) * N + i] = valid ? v : 0.0;
-    });
-  }
-
-  // 5. Overlap-add of the element patches onto the brick's node block,
-  // separably x, then y, then z.  A shared node takes (lower element +
-  // upper element) in each direction: a fixed order, so the sums are
-  // bitwise reproducible.
-  constexpr int BX = D::BX, BY = D::BY, BZ = D::BZ;
-  double* AX = smem + D::TAB + D::NB * 3 + D::NE * D::ELEM;  // [lz][ly][c][k][j][ix]
-  double* AY = AX + D::AXN;                                   // [lz][c][k][iy][ix]
-  const double* Ebase = smem + D::TAB + D::NB * 3;
-  constexpr int NAX = BZ * BY * 3 * N * N * NBX;
-#pragma unroll 1
-  for (int r = tid; r < NAX; r += T) {
-    const int ix = r % NBX, rest = r / NBX;  // rest = ((lz*BY + ly)*3 + c)*N*N + k*N + j
-    const int kj = rest % (N * N), lzlyc = rest / (N * N);
-    const int c = lzlyc % 3, lzly = lzlyc / 3;
-    const int lxh = ix / P < BX ? ix / P : BX - 1;
-    const int i = ix - P * lxh;
-    const double* e = Ebase + (lzly * BX + lxh) * D::ELEM + c * N3 + kj * N;
-    double v = e[i];
-    if (i == 0 && lxh > 0) v = e[P - D::ELEM] + v;
-    AX[r] = v;
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int z = 0; z < Q; ++z) {
+      SA[((c * Q + z) * Q + qy) * Q + qx] = g[c][0][z];
+      SB[((c * Q + z) * Q + qy) * Q + qx] = g[c][1][z];
+    }
+  __syncthreads();
+  // B2: acc = Dx^T Hx + Dy^T Hy + Dz^T Hz (reference order), then z interp^T.
+  double w[3][N];
+  {
+    double dxt[Q], dyt[Q];
+#pragma unroll
+    for (int r = 0; r < Q; ++r) {
+      dxt[r] = sD[r * Q + qx];
+      dyt[r] = sD[r * Q + qy];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double acc[Q];
+#pragma unroll
+      for (int z = 0; z < Q; ++z) {
+        double sx = 0.0, sy = 0.0, sz = 0.0;
+#pragma unroll
+        for (int r = 0; r < Q; ++r) {
+          sx += dxt[r] * SA[((c * Q + z) * Q + qy) * Q + r];
+          sy += dyt[r] * SB[((c * Q + z) * Q + r) * Q + qx];
+          sz += prm.Dc[r * Q + z] * g[c][2][r];
+        }
+        acc[z] = (sx + sy) + sz;
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int z = 0; z < Q; ++z) s += prm.B[z * N + k] * acc[z];
+        w[c][k] = s;
+      }
+    }
   }
   __syncthreads();
-  constexpr int NAY = BZ * 3 * N * NBY * NBX;
-#pragma unroll 1
-  for (int r = tid; r < NAY; r += T) {
-    const int ix = r % NBX, rest = r / NBX;  // rest = ((lz*3 + c)*N + k)*NBY + iy
-    const int iy = rest % NBY, lzck = rest / NBY;
+  // B3: W[c][k][b][a] -> A.
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int k = 0; k < N; ++k) SA[((c * N + k) * Q + qy) * Q + qx] = w[c][k];
+  __syncthreads();
+  // B4: y interp^T: T[c][k][j][a] = sum_b B[b][j] W[c][k][b][a] -> B.
+  if (qy < N) {
+    double bcy[Q];
+#pragma unroll
+    for (int b = 0; b < Q; ++b) bcy[b] = sB[b * N + qy];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < Q; ++b) s += bcy[b] * SA[((c * N + k) * Q + b) * Q + qx];
+        SB[((c * N + k) * N + qy) * Q + qx] = s;
+      }
+  }
+  __syncthreads();
+  // B5: x interp^T: EO[c][k][j][i] = sum_a B[a][i] T[c][k][j][a].
+  if (qx < N && qy < N) {
+    double bcx[Q];
+#pragma unroll
+    for (int a = 0; a < Q; ++a) bcx[a] = sB[a * N + qx];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < Q; ++a) s += bcx[a] * SB[((c * N + k) * N + qy) * Q + a];
+        EOe[(c * N + k) * N * N + qy * N + qx] = valid ? s : 0.0;  // padding elements add 0
+      }
+  }
+  __syncthreads();
+
+  // ---- overlap-add onto the node block: x, then y, then z ---------------
+  // A shared node takes (lower element + upper element) in each direction.
+  // AX [lz][ly][c][k][j][ix] and AY [lz][c][k][iy][ix] live in the elements'
+  // A/B slabs (free now; the EO regions they read from stay untouched):
+  // slab index r -> element r / 2A, offset r % 2A.
+  auto rowp = [&](int r) { return Ebase + (r / D::RPS) * D::ELEM + (r % D::RPS) * NBX; };
+  // x pass: one thread per (lz, ly, c, k, j) row of NBX nodes.
+  constexpr int RX = D::RX;
+  for (int row = tid; row < RX; row += T) {
+    const int kj = row % (N * N), lzlyc = row / (N * N);
+    const int c = lzlyc % 3, lzly = lzlyc / 3;
+    const double* e = Ebase + lzly * BX * D::ELEM + 2 * D::A + c * N3 + kj * N;
+    double* out = rowp(row);
+#pragma unroll
+    for (int ix = 0; ix < NBX; ++ix) {
+      const int lxh = ix / P < BX ? ix / P : BX - 1;
+      const int i = ix - P * lxh;
+      double v = e[lxh * D::ELEM + i];
+      if (i == 0 && lxh > 0) v = e[(lxh - 1) * D::ELEM + P] + v;
+      out[ix] = v;
+    }
+  }
+  __syncthreads();
+  // y pass: one thread per (lz, c, k, iy) row.
+  constexpr int RY = D::RY;
+  for (int row = tid; row < RY; row += T) {
+    const int iy = row % NBY, lzck = row / NBY;
     const int k = lzck % N, lzc = lzck / N;
     const int c = lzc % 3, lz = lzc / 3;
     const int lyh = iy / P < BY ? iy / P : BY - 1;
     const int j = iy - P * lyh;
-    // AX index: ((((lz*BY + ly)*3 + c)*N + k)*N + j)*NBX + ix
-    const double* a = AX + ((((lz * BY + lyh) * 3 + c) * N + k) * N + j) * NBX + ix;
-    double v = a[0];
-    if (j == 0 && lyh > 0) v = a[(P - 3 * N * N) * NBX] + v;  // ly - 1, j = P
-    AY[r] = v;
+    const int ra = (((lz * BY + lyh) * 3 + c) * N + k) * N + j;
+    const double* a = rowp(ra);
+    const bool two = j == 0 && lyh > 0;
+    const double* b = rowp(ra + P - 3 * N * N);  // ly - 1, j = P
+    double* out = rowp(RX + row);
+#pragma unroll
+    for (int ix = 0; ix < NBX; ++ix) out[ix] = two ? b[ix] + a[ix] : a[ix];
   }
   __syncthreads();
-  // z, fused with the stores: node block in [iz][iy][ix][c] order.
+  // z pass fused with the stores: consecutive threads walk the global node
+  // rows (3 nbx interleaved doubles, contiguous) for coalesced stores.
   double* part = prm.partial + (size_t)brick * (D::NB * 3);
-#pragma unroll 1
-  for (int r = tid; r < NB * 3; r += T) {
-    const int c3 = r % ROW3, row = r / ROW3;
+  for (int w = tid; w < NB * 3; w += T) {
+    const int c3 = w % ROW3, row = w / ROW3;
     const int iy = row % NBY, iz = row / NBY;
     const int ix = c3 / 3, c = c3 - 3 * ix;
-    if (!(ix < nbx && iy < nby && iz < nbz)) continue;
+    if (ix >= nbx || iy >= nby || iz >= nbz) continue;
     const int lzh = iz / P < BZ ? iz / P : BZ - 1;
     const int k = iz - P * lzh;
-    // AY index: (((lz*3 + c)*N + k)*NBY + iy)*NBX + ix
-    const double* a = AY + (((lzh * 3 + c) * N + k) * NBY + iy) * NBX + ix;
-    double s = a[0];
-    if (k == 0 && lzh > 0) s = a[(P - 3 * N) * NBY * NBX] + s;  // lz - 1, k = P
-    const bool boundary = ix == 0 || iy == 0 || iz == 0 || ix == nbx - 1 || iy == nby - 1 || iz == nbz - 1;
-    if (boundary) {
-      __stcg(part + r, s);
+    const int ra = RX + ((lzh * 3 + c) * N + k) * NBY + iy;
+    double s = rowp(ra)[ix];
+    if (k == 0 && lzh > 0) s = rowp(ra + (P - 3 * N) * NBY)[ix] + s;  // lz - 1, k = P
+    if (ix == 0 || iy == 0 || iz == 0 || ix == nbx - 1 || iy == nby - 1 || iz == nbz - 1) {
+      __stcg(part + w, s);
     } else {
       const int dof = 3 * (node0 + npx * (iy + npy * iz)) + c3;
-      if (prm.mask && prm.mask[dof]) s = prm.x[dof];
-      prm.y[dof] = s;
+      prm.y[dof] = (prm.mask && prm.mask[dof]) ? prm.x[dof] : s;
     }
   }
 }
@@ -241,16 +402,17 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, MinBlocks<Q>::value)
 // Sums brick-boundary partials: nodes on planes g_d = k P B_d (or the domain's
 // far face) in increasing brick order.
 template <int P, int Q>
-__global__ void fused_fixup_kernel(FusedParams prm) {
+__global__ void fused_fixup_kernel(const __grid_constant__ FusedParams prm) {
   using D = FDims<P, Q>;
-  constexpr int PB[3] = {P * D::BX, P * D::BY, P * D::BZ};
+  const int PB0 = P * D::BX, PB1 = P * D::BY, PB2 = P * D::BZ;
   const BoxDev& box = prm.box;
   const QLayout& lay = prm.lay;
-  long long nn = box.num_nodes();
+  const long long nn = box.num_nodes();
   for (long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x; node < nn;
        node += (long long)gridDim.x * blockDim.x) {
-    int g[3] = {(int)(node % box.npd[0]), (int)((node / box.npd[0]) % box.npd[1]),
-                (int)(node / ((long long)box.npd[0] * box.npd[1]))};
+    const int g[3] = {(int)(node % box.npd[0]), (int)((node / box.npd[0]) % box.npd[1]),
+                      (int)(node / ((long long)box.npd[0] * box.npd[1]))};
+    const int PB[3] = {PB0, PB1, PB2};
     bool on = false;
 #pragma unroll
     for (int d = 0; d < 3; ++d) on = on || g[d] % PB[d] == 0 || g[d] == box.npd[d] - 1;
@@ -258,7 +420,7 @@ __global__ void fused_fixup_kernel(FusedParams prm) {
     int lo[3], hi[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      int b = g[d] / PB[d];
+      const int b = g[d] / PB[d];
       if (g[d] % PB[d] == 0) {
         lo[d] = b > 0 ? b - 1 : 0;
         hi[d] = b < lay.nb[d] ? b : lay.nb[d] - 1;
@@ -270,18 +432,18 @@ __global__ void fused_fixup_kernel(FusedParams prm) {
     for (int b2 = lo[2]; b2 <= hi[2]; ++b2)
       for (int b1 = lo[1]; b1 <= hi[1]; ++b1)
         for (int b0 = lo[0]; b0 <= hi[0]; ++b0) {
-          long long brick = b0 + lay.nb[0] * (b1 + (long long)lay.nb[1] * b2);
-          int ix = g[0] - PB[0] * b0, iy = g[1] - PB[1] * b1, iz = g[2] - PB[2] * b2;
+          const long long brick = b0 + lay.nb[0] * (b1 + (long long)lay.nb[1] * b2);
+          const int ix = g[0] - PB0 * b0, iy = g[1] - PB1 * b1, iz = g[2] - PB2 * b2;
           const double* p = prm.partial + brick * (long long)(D::NB * 3) +
                             ((iz * D::NBY + iy) * D::NBX + ix) * 3;
           s0 += __ldcg(p);
           s1 += __ldcg(p + 1);
           s2 += __ldcg(p + 2);
         }
-    double s[3] = {s0, s1, s2};
+    const double s[3] = {s0, s1, s2};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      long long dof = 3 * node + c;
+      const long long dof = 3 * node + c;
       double v = s[c];
       if (prm.mask && prm.mask[dof]) v = prm.x[dof];
       prm.y[dof] = v;
@@ -315,6 +477,8 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
   prm.mu = op.mu_;
   prm.lambda = op.lambda_;
   prm.perturb = op.perturb_;
+  for (size_t i = 0; i < op.interp_.size(); ++i) prm.B[i] = op.interp_[i];
+  for (size_t i = 0; i < op.colloc_.size(); ++i) prm.Dc[i] = op.colloc_[i];
   dispatch_pq(op.p_, op.q_, [&](auto Pc, auto Qc) {
     constexpr int P = decltype(Pc)::value, Q = decltype(Qc)::value;
     using D = FDims<P, Q>;
@@ -324,6 +488,8 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
     size_t smem = sizeof(double) * D::SMEM;
     auto k = fused_jacobian_kernel<P, Q>;
     HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
     k<<<(unsigned)op.lay_.num_bricks(), D::T, smem, op.stream_>>>(prm);
     HXG_CUDA(cudaGetLastError());
     fused_fixup_kernel<P, Q><<<grid_for(op.box_.num_nodes(), 256), 256, 0, op.stream_>>>(prm);
