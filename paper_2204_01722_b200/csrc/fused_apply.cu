@@ -81,6 +81,37 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// L2 eviction policies: the quadrature state is streamed once per apply
+// (evict first, no L1 allocation); the brick-boundary partials are re-read
+// by the fix-up kernel right after (keep them in L2).
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_stream(const double* a, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_keep(double* a, double v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double ld_once(const double* a, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v)
+               : "l"(a), "l"(pol));
+  return v;
+}
+
 template <int P, int Q>
 __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
     fused_jacobian_kernel(const __grid_constant__ FusedParams prm) {
@@ -220,6 +251,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
 
   // ---- q-function on the streamed state --------------------------------
   const double* sp0 = st_brick + tid;
+  const unsigned long long pol_stream = policy_evict_first();
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
     double H[9];
@@ -231,7 +263,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
 #if HXG_EXPERIMENT == 1
         st[s] = 1.0 + 0.01 * s + 1e-3 * tid + 0.0 * sp[0];
 #else
-        st[s] = __ldcs(sp + s * T);
+        st[s] = ld_stream(sp + s * T, pol_stream);
 #endif
       }
       double G[9];
@@ -380,6 +412,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
   // z pass fused with the stores: consecutive threads walk the global node
   // rows (3 nbx interleaved doubles, contiguous) for coalesced stores.
   double* part = prm.partial + (size_t)brick * (D::NB * 3);
+  const unsigned long long pol_keep = policy_evict_last();
   for (int w = tid; w < NB * 3; w += T) {
     const int c3 = w % ROW3, row = w / ROW3;
     const int iy = row % NBY, iz = row / NBY;
@@ -391,7 +424,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
     double s = rowp(ra)[ix];
     if (k == 0 && lzh > 0) s = rowp(ra + (P - 3 * N) * NBY)[ix] + s;  // lz - 1, k = P
     if (ix == 0 || iy == 0 || iz == 0 || ix == nbx - 1 || iy == nby - 1 || iz == nbz - 1) {
-      __stcg(part + w, s);
+      st_keep(part + w, s, pol_keep);
     } else {
       const int dof = 3 * (node0 + npx * (iy + npy * iz)) + c3;
       prm.y[dof] = (prm.mask && prm.mask[dof]) ? prm.x[dof] : s;
@@ -401,52 +434,51 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
 
 // Sums brick-boundary partials: nodes on planes g_d = k P B_d (or the domain's
 // far face) in increasing brick order.
+// One warp per (gy, gz) node row (blockDim = 32 x 4, grid = (ceil(npy/4), npz)).
+// Rows on a y or z brick plane are boundary along their whole length; other
+// rows only at the x brick planes.
 template <int P, int Q>
 __global__ void fused_fixup_kernel(const __grid_constant__ FusedParams prm) {
   using D = FDims<P, Q>;
-  const int PB0 = P * D::BX, PB1 = P * D::BY, PB2 = P * D::BZ;
+  constexpr int PB0 = P * D::BX, PB1 = P * D::BY, PB2 = P * D::BZ;
   const BoxDev& box = prm.box;
   const QLayout& lay = prm.lay;
-  const long long nn = box.num_nodes();
-  for (long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x; node < nn;
-       node += (long long)gridDim.x * blockDim.x) {
-    const int g[3] = {(int)(node % box.npd[0]), (int)((node / box.npd[0]) % box.npd[1]),
-                      (int)(node / ((long long)box.npd[0] * box.npd[1]))};
-    const int PB[3] = {PB0, PB1, PB2};
-    bool on = false;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) on = on || g[d] % PB[d] == 0 || g[d] == box.npd[d] - 1;
-    if (!on) continue;
-    int lo[3], hi[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const int b = g[d] / PB[d];
-      if (g[d] % PB[d] == 0) {
-        lo[d] = b > 0 ? b - 1 : 0;
-        hi[d] = b < lay.nb[d] ? b : lay.nb[d] - 1;
-      } else {
-        lo[d] = hi[d] = b;
-      }
-    }
+  const int gy = blockIdx.x * blockDim.y + threadIdx.y, gz = blockIdx.y;
+  const int npx = box.npd[0], npy = box.npd[1];
+  if (gy >= npy) return;
+  const bool yb = gy % PB1 == 0 || gy == npy - 1;
+  const bool zb = gz % PB2 == 0 || gz == box.npd[2] - 1;
+  const bool full = yb || zb;
+  // y / z brick ranges of this row.
+  const int b1 = gy / PB1, b2 = gz / PB2;
+  const int lo1 = (gy % PB1 == 0 && b1 > 0) ? b1 - 1 : b1, hi1 = min(b1, lay.nb[1] - 1);
+  const int lo2 = (gz % PB2 == 0 && b2 > 0) ? b2 - 1 : b2, hi2 = min(b2, lay.nb[2] - 1);
+  const unsigned long long pol = policy_evict_first();
+  const int nx_planes = (npx - 1 + PB0 - 1) / PB0 + 1;  // x brick planes incl. far face
+  const int count = full ? npx : nx_planes;
+  for (int t = threadIdx.x; t < count; t += 32) {
+    const int gx = full ? t : min(t * PB0, npx - 1);
+    const int b0 = gx / PB0;
+    const int lo0 = (gx % PB0 == 0 && b0 > 0) ? b0 - 1 : b0, hi0 = min(b0, lay.nb[0] - 1);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int b2 = lo[2]; b2 <= hi[2]; ++b2)
-      for (int b1 = lo[1]; b1 <= hi[1]; ++b1)
-        for (int b0 = lo[0]; b0 <= hi[0]; ++b0) {
-          const long long brick = b0 + lay.nb[0] * (b1 + (long long)lay.nb[1] * b2);
-          const int ix = g[0] - PB0 * b0, iy = g[1] - PB1 * b1, iz = g[2] - PB2 * b2;
-          const double* p = prm.partial + brick * (long long)(D::NB * 3) +
-                            ((iz * D::NBY + iy) * D::NBX + ix) * 3;
-          s0 += __ldcg(p);
-          s1 += __ldcg(p + 1);
-          s2 += __ldcg(p + 2);
+    for (int c2 = lo2; c2 <= hi2; ++c2)
+      for (int c1 = lo1; c1 <= hi1; ++c1)
+        for (int c0 = lo0; c0 <= hi0; ++c0) {
+          const size_t brick = c0 + (size_t)lay.nb[0] * (c1 + (size_t)lay.nb[1] * c2);
+          const int ix = gx - PB0 * c0, iy = gy - PB1 * c1, iz = gz - PB2 * c2;
+          const double* p =
+              prm.partial + brick * (D::NB * 3) + ((iz * D::NBY + iy) * D::NBX + ix) * 3;
+          s0 += ld_once(p, pol);
+          s1 += ld_once(p + 1, pol);
+          s2 += ld_once(p + 2, pol);
         }
+    const size_t dof0 = 3 * ((size_t)gx + (size_t)npx * (gy + (size_t)npy * gz));
     const double s[3] = {s0, s1, s2};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const long long dof = 3 * node + c;
       double v = s[c];
-      if (prm.mask && prm.mask[dof]) v = prm.x[dof];
-      prm.y[dof] = v;
+      if (prm.mask && prm.mask[dof0 + c]) v = prm.x[dof0 + c];
+      prm.y[dof0 + c] = v;
     }
   }
 }
@@ -492,7 +524,8 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
                                   cudaSharedmemCarveoutMaxShared));
     k<<<(unsigned)op.lay_.num_bricks(), D::T, smem, op.stream_>>>(prm);
     HXG_CUDA(cudaGetLastError());
-    fused_fixup_kernel<P, Q><<<grid_for(op.box_.num_nodes(), 256), 256, 0, op.stream_>>>(prm);
+    dim3 fb(32, 4), fg((op.box_.npd[1] + 3) / 4, op.box_.npd[2]);
+    fused_fixup_kernel<P, Q><<<fg, fb, 0, op.stream_>>>(prm);
     HXG_CUDA(cudaGetLastError());
   });
 }
