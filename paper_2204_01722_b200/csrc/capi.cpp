@@ -161,16 +161,7 @@ struct Pinned {
 }  // namespace
 
 int hxg_op_apply_jacobian_host(hxg_op_t op, const double* du_host, double* y_host) {
-  return guarded([&] {
-    auto& o = OP(op);
-    size_t n = (size_t)o.size();
-    hxg::DevBuf<double> x(n), y(n);
-    cudaStream_t s = o.stream();
-    HXG_CUDA(cudaMemcpyAsync(x.p, du_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
-    o.apply_jacobian(x.p, y.p);
-    HXG_CUDA(cudaMemcpyAsync(y_host, y.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
-    HXG_CUDA(cudaStreamSynchronize(s));
-  });
+  return guarded([&] { OP(op).apply_jacobian_host(du_host, y_host); });
 }
 
 int hxg_op_apply_residual_host(hxg_op_t op, const double* u_host, double* f_host) {

@@ -46,6 +46,8 @@ struct FusedParams {
   const double* state;
   double mu, lambda, perturb;
   double* partial;
+  int brick0;  // first brick of this launch (pipelined host path)
+  int gz0;     // first node plane of this fix-up launch
   // Uniform copies of the 1D tables for the z-direction contractions
   // (constant-bank operands).
   double B[kMaxQ * (kMaxP + 1)];
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
   double* Xs = smem + D::TAB;       // node block [c][iz][iy][ix]
   double* Ebase = Xs + 3 * NB;      // per-element slabs
   const int tid = threadIdx.x;
-  const int brick = blockIdx.x;
+  const int brick = blockIdx.x + prm.brick0;
   const QLayout& lay = prm.lay;
   const BoxDev& box = prm.box;
   const int bx = brick % lay.nb[0], by = (brick / lay.nb[0]) % lay.nb[1],
@@ -443,7 +445,7 @@ __global__ void fused_fixup_kernel(const __grid_constant__ FusedParams prm) {
   constexpr int PB0 = P * D::BX, PB1 = P * D::BY, PB2 = P * D::BZ;
   const BoxDev& box = prm.box;
   const QLayout& lay = prm.lay;
-  const int gy = blockIdx.x * blockDim.y + threadIdx.y, gz = blockIdx.y;
+  const int gy = blockIdx.x * blockDim.y + threadIdx.y, gz = blockIdx.y + prm.gz0;
   const int npx = box.npd[0], npy = box.npd[1];
   if (gy >= npy) return;
   const bool yb = gy % PB1 == 0 || gy == npy - 1;
@@ -527,6 +529,86 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
     dim3 fb(32, 4), fg((op.box_.npd[1] + 3) / 4, op.box_.npd[2]);
     fused_fixup_kernel<P, Q><<<fg, fb, 0, op.stream_>>>(prm);
     HXG_CUDA(cudaGetLastError());
+  });
+}
+
+// Host buffers: the box is cut into C chunks of brick layers along z.  Chunk
+// i's x planes go up on the H2D stream; its bricks and the fix-up of the node
+// planes it finalises run on the compute stream once those planes have
+// landed; its finished y planes go down on the D2H stream.  The three
+// engines overlap, so the copies hide the apply (and vice versa).
+void fused_jacobian_host(Operator& op, const double* xh, double* yh) {
+  if (!op.pipe_) op.pipe_ = std::make_unique<HostPipe>();
+  HostPipe& pp = *op.pipe_;
+  const size_t n = (size_t)op.size();
+  if (pp.x.n != n) {
+    pp.x.alloc(n);
+    pp.y.alloc(n);
+  }
+  FusedParams prm{};
+  prm.box = op.box_;
+  prm.lay = op.lay_;
+  prm.x = pp.x.p;
+  prm.y = pp.y.p;
+  prm.mask = op.mask();
+  prm.tab = op.tab_.p;
+  prm.state = op.state_->data.p;
+  prm.mu = op.mu_;
+  prm.lambda = op.lambda_;
+  prm.perturb = op.perturb_;
+  for (size_t i = 0; i < op.interp_.size(); ++i) prm.B[i] = op.interp_[i];
+  for (size_t i = 0; i < op.colloc_.size(); ++i) prm.Dc[i] = op.colloc_[i];
+  dispatch_pq(op.p_, op.q_, [&](auto Pc, auto Qc) {
+    constexpr int P = decltype(Pc)::value, Q = decltype(Qc)::value;
+    using D = FDims<P, Q>;
+    size_t need = (size_t)op.lay_.num_bricks() * D::NB * 3;
+    if (op.partial_.n != need) op.partial_.alloc(need);
+    prm.partial = op.partial_.p;
+    size_t smem = sizeof(double) * D::SMEM;
+    auto k = fused_jacobian_kernel<P, Q>;
+    HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+    const int nbz = op.lay_.nb[2], layer = op.lay_.nb[0] * op.lay_.nb[1];
+    const int pb2 = P * D::BZ, npz = op.box_.npd[2];
+    const size_t plane = (size_t)op.box_.npd[0] * op.box_.npd[1] * 3;
+    const int C = nbz < HostPipe::kMaxChunks / 2 ? nbz : HostPipe::kMaxChunks / 2;
+    // Order after earlier work on the operator's stream.
+    HXG_CUDA(cudaEventRecord(pp.done_evt, op.stream_));
+    HXG_CUDA(cudaStreamWaitEvent(pp.h2d, pp.done_evt, 0));
+    HXG_CUDA(cudaStreamWaitEvent(pp.comp, pp.done_evt, 0));
+    int sent = 0;  // planes [0, sent) uploaded
+    for (int i = 0; i < C; ++i) {
+      const int le = (int)((long long)(i + 1) * nbz / C);
+      const int upto = (pb2 * le < npz - 1 ? pb2 * le : npz - 1) + 1;
+      HXG_CUDA(cudaMemcpyAsync(pp.x.p + sent * plane, xh + sent * plane,
+                               (size_t)(upto - sent) * plane * sizeof(double),
+                               cudaMemcpyHostToDevice, pp.h2d));
+      sent = upto;
+      HXG_CUDA(cudaEventRecord(pp.in_ready[i], pp.h2d));
+    }
+    for (int i = 0; i < C; ++i) {
+      const int lb = (int)((long long)i * nbz / C), le = (int)((long long)(i + 1) * nbz / C);
+      HXG_CUDA(cudaStreamWaitEvent(pp.comp, pp.in_ready[i], 0));
+      FusedParams pc = prm;
+      pc.brick0 = lb * layer;
+      k<<<(unsigned)((le - lb) * layer), D::T, smem, pp.comp>>>(pc);
+      HXG_CUDA(cudaGetLastError());
+      const int zs = i == 0 ? 0 : pb2 * lb;
+      const int ze = i == C - 1 ? npz : pb2 * le;
+      pc.gz0 = zs;
+      dim3 fb(32, 4), fg((op.box_.npd[1] + 3) / 4, ze - zs);
+      fused_fixup_kernel<P, Q><<<fg, fb, 0, pp.comp>>>(pc);
+      HXG_CUDA(cudaGetLastError());
+      HXG_CUDA(cudaEventRecord(pp.out_ready[i], pp.comp));
+      HXG_CUDA(cudaStreamWaitEvent(pp.d2h, pp.out_ready[i], 0));
+      HXG_CUDA(cudaMemcpyAsync(yh + zs * plane, pp.y.p + zs * plane,
+                               (size_t)(ze - zs) * plane * sizeof(double), cudaMemcpyDeviceToHost,
+                               pp.d2h));
+    }
+    HXG_CUDA(cudaEventRecord(pp.done_evt, pp.d2h));
+    HXG_CUDA(cudaStreamWaitEvent(op.stream_, pp.done_evt, 0));
+    HXG_CUDA(cudaStreamSynchronize(pp.d2h));
   });
 }
 

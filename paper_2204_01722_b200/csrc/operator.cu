@@ -183,6 +183,27 @@ void Operator::apply_residual(const double* u, double* f) {
   launch_node_sum(evec_.p, f, nullptr, kEpiResidual);
 }
 
+void Operator::apply_jacobian_host(const double* xh, double* yh) {
+  if (!state_->valid) throw Error(HXG_ERR_STATE_NOT_INITIALIZED,
+                                  "quadrature state not initialized: evaluate the residual at the "
+                                  "linearization point first");
+  if (variant_ == 0 && fused_supported(p_, q_)) {
+    ++jacobian_applies_;
+    fused_jacobian_host(*this, xh, yh);
+    return;
+  }
+  if (!pipe_) pipe_ = std::make_unique<HostPipe>();
+  size_t n = (size_t)size();
+  if (pipe_->x.n != n) {
+    pipe_->x.alloc(n);
+    pipe_->y.alloc(n);
+  }
+  HXG_CUDA(cudaMemcpyAsync(pipe_->x.p, xh, n * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  apply_jacobian(pipe_->x.p, pipe_->y.p);
+  HXG_CUDA(cudaMemcpyAsync(yh, pipe_->y.p, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  HXG_CUDA(cudaStreamSynchronize(stream_));
+}
+
 int Operator::kernel_launches() const {
   return (variant_ == 0 && fused_supported(p_, q_)) ? fused_launches(p_, q_) : 2;
 }

@@ -52,6 +52,35 @@ struct Geometry {
   QLayout lay;
 };
 
+// Streams, events and device staging for the pipelined host-buffer apply
+// (H2D of z-chunks / compute / D2H overlapped).
+struct HostPipe {
+  static constexpr int kMaxChunks = 16;
+  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  cudaEvent_t in_ready[kMaxChunks], out_ready[kMaxChunks], done_evt = nullptr;
+  DevBuf<double> x, y;
+  HostPipe() {
+    HXG_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    HXG_CUDA(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
+    HXG_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < kMaxChunks; ++i) {
+      HXG_CUDA(cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming));
+      HXG_CUDA(cudaEventCreateWithFlags(&out_ready[i], cudaEventDisableTiming));
+    }
+    HXG_CUDA(cudaEventCreateWithFlags(&done_evt, cudaEventDisableTiming));
+  }
+  ~HostPipe() {
+    for (int i = 0; i < kMaxChunks; ++i) {
+      cudaEventDestroy(in_ready[i]);
+      cudaEventDestroy(out_ready[i]);
+    }
+    cudaEventDestroy(done_evt);
+    cudaStreamDestroy(h2d);
+    cudaStreamDestroy(comp);
+    cudaStreamDestroy(d2h);
+  }
+};
+
 class Operator {
  public:
   // desc fields as hxg_op_desc; geometry may come from desc (host arrays) or
@@ -105,7 +134,12 @@ class Operator {
   // Element matrices (e, 3N^3, 3N^3) of the assembled operator.
   void element_matrices(double* out);
 
+  // Host buffers in, host buffers out: pipelined over z-chunks when the fused
+  // path applies (H2D / compute / D2H overlap), else stage + apply + copy.
+  void apply_jacobian_host(const double* xh, double* yh);
+
   friend void fused_jacobian(Operator& op, const double* du, double* y);
+  friend void fused_jacobian_host(Operator& op, const double* xh, double* yh);
 
  private:
   void launch_element(int mode, const double* x, bool mask_input);
@@ -126,6 +160,7 @@ class Operator {
   DevBuf<double> load_;
   DevBuf<double> evec_;    // E-vector scratch for the two-pass path
   DevBuf<double> partial_; // brick-boundary partial sums for the fused path
+  std::unique_ptr<HostPipe> pipe_;
   DevBuf<unsigned long long> fail_;
   std::shared_ptr<State> state_;
   std::shared_ptr<Geometry> geometry_;
