@@ -148,6 +148,11 @@ int hxg_mg_level_op(hxg_mg_t mg, int level, hxg_op_t* op); /* borrowed */
 /* setup_numeric (multigrid.hpp:100-113): diagonals, Chebyshev lambda_max by
  * 10 Lanczos steps, coarse assembly (assembly.hpp:142-230) + Cholesky. */
 int hxg_mg_setup_numeric(hxg_mg_t mg);
+/* Coarse Cholesky backend: 0 automatic (dense below a few thousand DoFs,
+ * else nested-dissection multifrontal), 1 dense, 2 nested-dissection
+ * multifrontal, 3 cuSOLVER csrchol on the ND-permuted matrix.  Takes effect
+ * at the next setup_numeric. */
+int hxg_mg_set_coarse_mode(hxg_mg_t mg, int mode);
 int hxg_mg_lambda_max(hxg_mg_t mg, int level, double* out);
 /* prolong / restrict_to (multigrid.hpp:122-135). */
 int hxg_mg_prolong(hxg_mg_t mg, int coarse_level, const double* xc, double* xf);

@@ -113,6 +113,7 @@ SIGNATURES = {
     "hxg_mg_level_size": [_vp, _i, _P(_i64)],
     "hxg_mg_level_op": [_vp, _i, _vp],
     "hxg_mg_setup_numeric": [_vp],
+    "hxg_mg_set_coarse_mode": [_vp, _i],
     "hxg_mg_lambda_max": [_vp, _i, _P(_d)],
     "hxg_mg_prolong": [_vp, _i, _vp, _vp],
     "hxg_mg_restrict": [_vp, _i, _vp, _vp],

@@ -251,6 +251,13 @@ int hxg_mg_level_op(hxg_mg_t mg, int level, hxg_op_t* op) {
   });
 }
 int hxg_mg_setup_numeric(hxg_mg_t mg) { return guarded([&] { MG(mg).setup_numeric(); }); }
+int hxg_mg_set_coarse_mode(hxg_mg_t mg, int mode) {
+  return guarded([&] {
+    if (mode < 0 || mode > 3)
+      throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "coarse mode must be 0, 1, 2 or 3");
+    MG(mg).set_coarse_mode(mode);
+  });
+}
 int hxg_mg_lambda_max(hxg_mg_t mg, int level, double* out) {
   return guarded([&] { *out = MG(mg).level(level).smoother.lambda_max; });
 }

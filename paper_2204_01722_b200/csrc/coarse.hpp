@@ -36,18 +36,28 @@ class CoarseAssembly {
 };
 
 class CoarseSolverImpl;
+class SparseCholeskyImpl;
+
+// Coarse levels up to this many DoFs use the dense device factorization.
+constexpr int kDenseCoarseMax = 6000;
 
 class CoarseSolver {
  public:
   CoarseSolver();
   ~CoarseSolver();
   // analyzePattern (first call) + factorize; throws NOT_SPD on failure.
-  void factorize(const CsrMatrix& a, const int cells[3], cudaStream_t s);
+  // npd = nodes per dimension of the Q1 lattice (nested-dissection order).
+  void factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s);
   void solve(const double* b, double* x, cudaStream_t s);
   bool ready() const;
+  void set_mode(int m) { mode_ = m; }
 
  private:
+  int mode_ = 0;
+  int active_ = 0;  // backend used by the last factorize
   std::unique_ptr<CoarseSolverImpl> impl_;
+  std::unique_ptr<SparseCholeskyImpl> sparse_;
+  std::unique_ptr<class NdCholesky> nd_;
 };
 
 }  // namespace hxg

@@ -246,7 +246,8 @@ void Hierarchy::setup_numeric() {
   for (int k = 1; k < num_levels(); ++k) level(k).smoother.create(*level(k).op, degree_);
   if (!assembly_) assembly_ = std::make_unique<CoarseAssembly>(*level(0).op);
   assembly_->numeric(*level(0).op);
-  coarse_.factorize(assembly_->matrix(), level(0).op->cells(), stream());
+  coarse_.set_mode(coarse_mode_);
+  coarse_.factorize(assembly_->matrix(), level(0).op->box().npd, stream());
 }
 
 void Hierarchy::prolong(int coarse_level, const double* xc, double* xf) {

@@ -71,6 +71,8 @@ class Hierarchy {
   void v_cycle(const double* b, double* x, bool x_zero = false);
   void coarse_solve(const double* b, double* x);
   const CsrMatrix& coarse_matrix() const { return assembly_->matrix(); }
+  // 0 automatic (dense below kDenseCoarseMax DoFs), 1 dense, 2 sparse ND.
+  void set_coarse_mode(int m) { coarse_mode_ = m; }
   cudaStream_t stream() const { return levels_.back()->op->stream(); }
 
  private:
@@ -78,7 +80,7 @@ class Hierarchy {
   std::vector<std::unique_ptr<Level>> levels_;
   std::unique_ptr<CoarseAssembly> assembly_;
   CoarseSolver coarse_;
-  int pre_ = 1, post_ = 1, degree_ = 2;
+  int pre_ = 1, post_ = 1, degree_ = 2, coarse_mode_ = 0;
 };
 
 }  // namespace hxg

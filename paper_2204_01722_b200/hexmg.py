@@ -278,6 +278,11 @@ class MultigridHierarchy:
     def setup_numeric(self):
         check(lib().hxg_mg_setup_numeric(self.h))
 
+    def set_coarse_mode(self, mode):
+        """0 automatic, 1 dense, 2 nested-dissection multifrontal, 3 cuSOLVER csrchol."""
+        mode = {"auto": 0, "dense": 1, "sparse": 2, "nd": 2, "csrchol": 3}.get(mode, mode)
+        check(lib().hxg_mg_set_coarse_mode(self.h, int(mode)))
+
     def lambda_max(self, k):
         out = ctypes.c_double()
         check(lib().hxg_mg_lambda_max(self.h, k, ctypes.byref(out)))

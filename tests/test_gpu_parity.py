@@ -227,3 +227,30 @@ def test_host_pipelined_apply_matches_device(order, cells):
     assert np.array_equal(yh.numpy(), yd)
     yp = prob.op.apply_jacobian_host(x)  # pageable buffers
     assert np.array_equal(yp, yd)
+
+
+@pytest.mark.parametrize("order,cells", [(2, (6, 5, 7)), (3, (4, 4, 3)), (4, (3, 3, 4))])
+def test_coarse_cholesky_backends_agree(order, cells):
+    """The nested-dissection multifrontal coarse solver (and cuSOLVER csrchol)
+    solve the assembled coarse operator like the dense factorization
+    (coarse_solver.hpp:35-40 is an exact solve); p-MG PCG iteration counts
+    are unchanged."""
+    from paper_2204_01722_b200.hexmg import FemProblem, cg_solve
+    prob = FemProblem(extents=(1, 1, 1), cells=cells, order=order, fixed_faces=("-x",),
+                      traction_face="+x", traction=(0, 0, -0.02))
+    f = prob.op.apply_residual(torch.zeros(prob.size(), dtype=torch.float64, device="cuda"))
+    mg = prob.hierarchy
+    rp = np.random.RandomState(3).uniform(-1, 1, mg.level_size(0))
+    sols, its = {}, {}
+    for mode in ("dense", "nd", "csrchol"):
+        mg.set_coarse_mode(mode)
+        mg.setup_numeric()
+        sols[mode] = mg.coarse_solve(cuda(rp)).cpu().numpy()
+        its[mode] = cg_solve(prob.op, -f, rtol=1e-8, precond="mg", mg=mg)["iterations"]
+    rpc, cols, vals = mg.coarse_csr()
+    import scipy.sparse as sp
+    A = sp.csr_matrix((vals, cols, rpc))
+    for mode, x in sols.items():
+        assert np.linalg.norm(A @ x - rp) < 1e-10 * np.linalg.norm(rp), mode
+        assert rel(x, sols["dense"]) < 1e-10, mode
+    assert its["nd"] == its["dense"] and abs(its["csrchol"] - its["dense"]) <= 1
