@@ -280,6 +280,39 @@ def run_ours(args, rank, world, local_rank):
         e2e_s = t.item()
     e2e_value = ndof_job / e2e_s / 1e9
 
+    # p-MG Newton-Krylov step on the same problem (BASELINE.json configs[1]:
+    # "single Jacobian apply + Newton-Krylov step"): residual (state), p-MG
+    # numeric setup (diagonals, Chebyshev lambda_max, coarse assembly +
+    # nested-dissection Cholesky), PCG to the reference's linear_rtol = 1e-3
+    # (nonlinear.hpp:20), device-timed.
+    newton = None
+    if world == 1 and not args.no_newton:
+        from paper_2204_01722_b200.hexmg import cg_solve
+        ev0, ev1, ev2, ev3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+        prob_n = FemProblem(extents=(1.0, 1.0, 1.0), cells=(CELLS,) * 3, order=ORDER,
+                            fixed_faces=("-x",), traction_face="+x", traction=(0.0, 0.0, -0.02))
+        un = torch.zeros(prob_n.size(), dtype=torch.float64, device="cuda")
+        mg = prob_n.hierarchy
+        prob_n.op.apply_residual(un)
+        mg.setup_numeric()  # warm-up: symbolic analysis, allocations
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        fn = prob_n.op.apply_residual(un)
+        ev1.record(stream)
+        mg.setup_numeric()
+        ev2.record(stream)
+        rep = cg_solve(prob_n.op, -fn, rtol=1e-3, precond="mg", mg=mg)
+        un += rep["x"]
+        ev3.record(stream)
+        torch.cuda.synchronize()
+        newton = {"config": f"Q{ORDER} {CELLS}^3, fixed -x, traction (0,0,-0.02) on +x, u = 0",
+                  "step_ms": ev0.elapsed_time(ev3), "residual_ms": ev0.elapsed_time(ev1),
+                  "setup_numeric_ms": ev1.elapsed_time(ev2), "pcg_ms": ev2.elapsed_time(ev3),
+                  "cg_iterations": rep["iterations"], "linear_rtol": 1e-3,
+                  "condition": rep["eig_max"] / rep["eig_min"],
+                  "coarse_solver": "nested-dissection multifrontal Cholesky (device)"}
+        del prob_n, mg
+
     # CPU baseline: the reference on the host cores, rank 0, N = 1 only.
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -316,6 +349,7 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": args.steps * op.kernel_launches(),
             "clocks": sampler.summary(),
             "cpu_baseline": cpu,
+            "newton_krylov_step": newton,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -331,6 +365,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-applies", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-newton", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
