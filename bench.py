@@ -150,33 +150,11 @@ def run_reference_arm(args, rank, world):
 # our arm
 # --------------------------------------------------------------------------
 def exchange_faces(y, npd, rank, world, dist):
-    """Sum the shared x-interface planes with the neighbouring slabs (NCCL).
-    Both sides add lower-rank partial + upper-rank partial, so the shared
-    entries are bitwise identical on the two ranks."""
-    import torch
-    nx, ny, nz = npd
-    v = y.view(nz, ny, nx, 3)
-    ops, bufs = [], {}
-    if rank + 1 < world:
-        send_hi = v[:, :, nx - 1, :].contiguous()
-        recv_hi = torch.empty_like(send_hi)
-        ops += [dist.P2POp(dist.isend, send_hi, rank + 1), dist.P2POp(dist.irecv, recv_hi, rank + 1)]
-        bufs["hi"] = (send_hi, recv_hi)
-    if rank > 0:
-        send_lo = v[:, :, 0, :].contiguous()
-        recv_lo = torch.empty_like(send_lo)
-        ops += [dist.P2POp(dist.isend, send_lo, rank - 1), dist.P2POp(dist.irecv, recv_lo, rank - 1)]
-        bufs["lo"] = (send_lo, recv_lo)
-    if ops:
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
-    if "hi" in bufs:
-        s, r = bufs["hi"]
-        v[:, :, nx - 1, :] = s + r
-    if "lo" in bufs:
-        s, r = bufs["lo"]
-        v[:, :, 0, :] = r + s
-
+    """Interface-plane sum with the neighbouring slabs over NCCL
+    (paper_2204_01722_b200.partition.exchange_faces; gloo-tested in
+    tests/test_multirank_cpu.py)."""
+    from paper_2204_01722_b200.partition import exchange_faces as _xf
+    return _xf(y, npd, rank, world, dist)
 
 def run_ours(args, rank, world, local_rank):
     import numpy as np

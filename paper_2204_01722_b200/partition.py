@@ -1,0 +1,100 @@
+"""Slab partition of the box across ranks and the interface-plane exchange
+(SURVEY.md §8(e)).
+
+The reference is single-process; the paper's distributed version
+sums interface-node contributions with a PETSc star forest after every
+operator apply.  Here the box of ``cells_x`` elements
+is cut into contiguous slabs along x, one per rank; each rank owns the
+elements of its slab and holds every lattice node of the slab, so the only
+shared entries are the node planes between neighbouring slabs.  After a local
+apply, neighbours swap their partial sums on the shared plane and both add
+(lower-rank partial + upper-rank partial): the shared entries end up bitwise
+identical on both ranks.  Dot products count each shared node once (owned by
+the lower rank) and are summed with one all-reduce.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class Slab:
+    rank: int
+    world: int
+    cells: tuple  # local element counts (cx, cy, cz)
+    x0: int       # first global element index along x
+    order: int
+
+    @property
+    def npd(self):
+        p = self.order
+        return (p * self.cells[0] + 1, p * self.cells[1] + 1, p * self.cells[2] + 1)
+
+    @property
+    def node_x0(self):
+        """Global lattice x-index of this slab's first node plane."""
+        return self.order * self.x0
+
+
+def slab_partition(global_cells, world, rank, order):
+    """Split ``global_cells[0]`` elements along x as evenly as possible."""
+    cx = global_cells[0]
+    base, extra = divmod(cx, world)
+    sizes = [base + (1 if r < extra else 0) for r in range(world)]
+    if min(sizes) < 1:
+        raise ValueError("more ranks than element layers along x")
+    x0 = sum(sizes[:rank])
+    return Slab(rank, world, (sizes[rank], global_cells[1], global_cells[2]), x0, order)
+
+
+def exchange_faces(y, npd, rank, world, dist):
+    """Sum the shared x-interface planes of the L-vector ``y`` (torch tensor,
+    interleaved 3 per node, x fastest) with the neighbouring slabs."""
+    import torch
+
+    nx, ny, nz = npd
+    v = y.view(nz, ny, nx, 3)
+    ops, bufs = [], {}
+    if rank + 1 < world:
+        send_hi = v[:, :, nx - 1, :].contiguous()
+        recv_hi = torch.empty_like(send_hi)
+        ops += [dist.P2POp(dist.isend, send_hi, rank + 1), dist.P2POp(dist.irecv, recv_hi, rank + 1)]
+        bufs["hi"] = (send_hi, recv_hi)
+    if rank > 0:
+        send_lo = v[:, :, 0, :].contiguous()
+        recv_lo = torch.empty_like(send_lo)
+        ops += [dist.P2POp(dist.isend, send_lo, rank - 1), dist.P2POp(dist.irecv, recv_lo, rank - 1)]
+        bufs["lo"] = (send_lo, recv_lo)
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    if "hi" in bufs:
+        s, r = bufs["hi"]
+        v[:, :, nx - 1, :] = s + r  # this rank is the lower one
+    if "lo" in bufs:
+        s, r = bufs["lo"]
+        v[:, :, 0, :] = r + s  # the neighbour is the lower one
+    return y
+
+
+def owned_mask(npd, rank, world):
+    """Boolean mask over the local L-vector of the entries this rank owns
+    (shared planes belong to the lower rank)."""
+    import torch
+
+    nx, ny, nz = npd
+    m = torch.ones(nz, ny, nx, 3, dtype=torch.bool)
+    if rank > 0:
+        m[:, :, 0, :] = False
+    return m.reshape(-1)
+
+
+def global_dot(x, y, owned, dist):
+    """x . y over owned entries, all-reduced (one f64): the CG/Lanczos dots
+    of SURVEY.md §8(e)."""
+    import torch
+
+    local = torch.sum(x[owned] * y[owned]).reshape(1).to(torch.float64)
+    if dist is not None:
+        dist.all_reduce(local)
+    return float(local.item())
