@@ -40,10 +40,11 @@ template <int P, int Q>
 __device__ __forceinline__ ThreadPos<Q> thread_pos(const QLayout& lay, long long brick) {
   using D = Dims<P, Q>;
   ThreadPos<Q> tp;
+  // Thread t = (qy Q + qx) NE + le: elements fastest (QLayout).
   int t = threadIdx.x;
-  tp.le = t / D::Q2;
-  tp.qx = t % Q;
-  tp.qy = (t / Q) % Q;
+  tp.le = t % D::NE;
+  tp.qx = (t / D::NE) % Q;
+  tp.qy = t / (D::NE * Q);
   tp.brick = brick;
   long long bx = brick % lay.nb[0], by = (brick / lay.nb[0]) % lay.nb[1],
             bz = brick / ((long long)lay.nb[0] * lay.nb[1]);
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams
   double* S2 = S1 + D::Q3;
   load_tables<P, Q>(prm.tab, smem);
   gather_element<P, Q>(prm.box, tp.e, prm.x, MODE == kJacobian ? prm.mask : nullptr, U,
-                       threadIdx.x % D::Q2, D::Q2);
+                       tp.qy * Q + tp.qx, D::Q2);
   __syncthreads();
 
   double g[3][3][Q];  // [component][direction][qz]
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_energy_kernel(ElemParam
   double* S2 = S1 + D::Q3;
   double* red = smem + D::TAB + D::NE * D::ELEM_SMEM;  // T doubles
   load_tables<P, Q>(prm.tab, smem);
-  gather_element<P, Q>(prm.box, tp.e, prm.x, nullptr, U, threadIdx.x % D::Q2, D::Q2);
+  gather_element<P, Q>(prm.box, tp.e, prm.x, nullptr, U, tp.qy * Q + tp.qx, D::Q2);
   __syncthreads();
   double g[3][3][Q];
 #pragma unroll
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_energy_kernel(ElemParam
     __syncthreads();
     if (tp.qx == 0 && tp.qy == 0 && tp.e >= 0) {
       double s = qz == 0 ? 0.0 : prm.energy_part[tp.e];
-      for (int r = 0; r < D::Q2; ++r) s += red[threadIdx.x + r];
+      for (int r = 0; r < D::Q2; ++r) s += red[tp.le + r * D::NE];  // column r = qy Q + qx
       prm.energy_part[tp.e] = s;
     }
     __syncthreads();

@@ -41,15 +41,18 @@ constexpr int kGeoStride = 10;
 // Brick of elements processed by one CTA; depends only on Q so every level
 // of a hierarchy (which shares the fine quadrature, multigrid.hpp:229-249)
 // shares one quadrature-data layout.
-__host__ __device__ constexpr int brick_x(int q) { return q == 2 ? 4 : q == 3 ? 4 : q == 4 ? 4 : 2; }
-__host__ __device__ constexpr int brick_y(int q) { return q == 2 ? 4 : q == 3 ? 4 : q == 4 ? 2 : 2; }
-__host__ __device__ constexpr int brick_z(int q) { return q == 2 ? 4 : q == 3 ? 2 : q == 4 ? 2 : 2; }
+__host__ __device__ constexpr int brick_x(int q) { return q == 2 ? 4 : q == 3 ? 4 : 2; }
+__host__ __device__ constexpr int brick_y(int q) { return q == 2 ? 4 : q == 3 ? 4 : 2; }
+__host__ __device__ constexpr int brick_z(int q) { return q == 2 ? 4 : q == 3 ? 2 : q == 4 ? 2 : 1; }
 
 // Quadrature-data layout in HBM: brick-blocked structure-of-arrays so that
 // the thread owning column (element, qx, qy) reads one coalesced double per
 // (brick, qz, scalar) row:
 //   offset(brick, qz, s, t) = ((brick * Q + qz) * S + s) * T + t,
-//   t = local_element * Q^2 + qy * Q + qx,  T = BX*BY*BZ*Q^2.
+//   t = (qy * Q + qx) * NE + local_element,  NE = BX*BY*BZ,  T = NE*Q^2.
+// Elements are the fastest index so a warp holds one column position of
+// many elements: per-element shared slabs are then hit with a constant odd
+// stride (bank-conflict free) while the state loads stay coalesced.
 struct QLayout {
   int cells[3] = {1, 1, 1};
   int Q = 2;
@@ -86,7 +89,7 @@ struct QLayout {
     int le = lx + B[0] * (ly + B[1] * lz);
     int qx = qpt % Q, qy = (qpt / Q) % Q;
     qz = qpt / (Q * Q);
-    t = le * Q * Q + qy * Q + qx;
+    t = (qy * Q + qx) * (B[0] * B[1] * B[2]) + le;
   }
 };
 

@@ -32,7 +32,7 @@ __device__ __forceinline__ long long state_offset(const QLayout& lay, long long 
   int le = lx + lay.B[0] * (ly + lay.B[1] * lz);
   int Q = lay.Q;
   int qx = qpt % Q, qy = (qpt / Q) % Q, qz = qpt / (Q * Q);
-  int t = le * Q * Q + qy * Q + qx;
+  int t = (qy * Q + qx) * (lay.B[0] * lay.B[1] * lay.B[2]) + le;
   return ((brick * Q + qz) * kStateStride) * (long long)lay.T + t;
 }
 

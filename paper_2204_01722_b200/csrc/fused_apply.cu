@@ -46,13 +46,46 @@ struct FusedParams {
   const double* state;
   double mu, lambda, perturb;
   double* partial;
-  int brick0;  // first brick of this launch (pipelined host path)
+  int brick0;   // first brick of this launch (pipelined host path)
+  int nbricks;  // bricks in this launch
+  int face_bits;  // >= 0: constraints are these whole faces (analytic), -1: mask array
   int gz0;     // first node plane of this fix-up launch
   // Uniform copies of the 1D tables for the z-direction contractions
   // (constant-bank operands).
-  double B[kMaxQ * (kMaxP + 1)];
-  double Dc[kMaxQ * kMaxQ];
+  double B[kMaxQ * (kMaxP + 1)];   // interp (Q x N)
+  double Bd[kMaxQ * (kMaxP + 1)];  // deriv  (Q x N)
 };
+
+// Padding tables (P * 10 + Q) from the bank-conflict search.
+__host__ __device__ constexpr int elem_pad(int p, int q) {
+  return p * 10 + q == 34 || p * 10 + q == 14 || p * 10 + q == 15 ? 2
+         : p * 10 + q == 45 || p * 10 + q == 25 || p * 10 + q == 35 ? 0
+                                                                     : 1;
+}
+__host__ __device__ constexpr int pad_nbx(int p, int q) {
+  switch (p * 10 + q) {
+    case 12: return 12; case 23: return 10; case 34: return 7; case 45: return 10;
+    case 13: return 12; case 14: return 6; case 24: return 6; case 15: return 4;
+    case 25: return 12; case 35: return 10;
+  }
+  return 0;
+}
+__host__ __device__ constexpr int pad_nby(int p, int q) {
+  switch (p * 10 + q) {
+    case 12: return 5; case 23: return 9; case 34: return 7; case 45: return 9;
+    case 13: return 5; case 14: return 3; case 24: return 6; case 15: return 6;
+    case 25: return 5; case 35: return 10;
+  }
+  return 0;
+}
+__host__ __device__ constexpr int pad_plane(int p, int q) {
+  switch (p * 10 + q) {
+    case 12: return 300; case 23: return 450; case 34: return 343; case 45: return 451;
+    case 13: return 180; case 14: return 54; case 24: return 181; case 15: return 50;
+    case 25: return 181; case 35: return 400;
+  }
+  return 0;
+}
 
 template <int P, int Q>
 struct FDims : Dims<P, Q> {
@@ -60,24 +93,31 @@ struct FDims : Dims<P, Q> {
   static constexpr int N = P + 1;
   static constexpr int NBX = P * D::BX + 1, NBY = P * D::BY + 1, NBZ = P * D::BZ + 1;
   static constexpr int NB = NBX * NBY * NBZ;  // nodes per (full) brick block
-  static constexpr int A = 3 * D::Q3;         // per-element slab A / B (3 components)
+  static constexpr int S = 9 * N * D::Q2;     // per-element exchange slab [c][arr][k][b][a]
   static constexpr int EO = 3 * D::N3;        // element outputs [c][k][j][i]
-  // Element stride == Q^2 (mod 16 doubles): a thread's slab address is then
-  // == its thread index (mod 16) for the column-contiguous accesses, so every
-  // half-warp hits 16 distinct bank pairs (conflict-free 64-bit accesses).
-  static constexpr int ELEM0 = 2 * A + EO;
-  static constexpr int ELEM = ELEM0 + (((D::Q2 - ELEM0) % 16) + 16) % 16;
-  // Overlap-add rows (NBX doubles each) packed into the elements' A/B
+  // Element stride and node-block strides padded (exhaustive search over the
+  // half-warp access patterns of every phase) so 64-bit shared accesses are
+  // (nearly) bank-conflict free; lanes are (column or plane task, element)
+  // with elements fastest.
+  static constexpr int ELEM0 = S + EO;
+  static constexpr int ELEM = ELEM0 + elem_pad(P, Q);
+  static constexpr int NBXP = pad_nbx(P, Q), NBYP = pad_nby(P, Q), NBP = pad_plane(P, Q);
+  static_assert(NBXP >= NBX && NBYP >= NBY && NBP >= NBXP * NBYP * NBZ, "node block padding");
+  // Overlap-add rows (NBX doubles each) packed into the elements' exchange
   // slabs, which are free by then: RPS rows per slab.
   static constexpr int RX = D::BZ * D::BY * 3 * N * N;  // x-pass rows [lz][ly][c][k][j]
   static constexpr int RY = D::BZ * 3 * N * NBY;        // y-pass rows [lz][c][k][iy]
-  static constexpr int RPS = 2 * A / NBX;
+  static constexpr int RPS = S / NBX;
   static_assert(RX + RY <= D::NE * RPS, "overlap-add rows must fit the element slabs");
-  static constexpr int SMEM = D::TAB + 3 * NB + D::NE * ELEM;
+  static constexpr int SMEM = 2 * 3 * NBP + D::NE * ELEM;  // two node blocks + slabs
   // Register cap for two resident CTAs per SM.
   static constexpr int REGS0 = 65536 / (HXG_FUSED_MINB * ((D::T + 31) / 32 * 32)) / 8 * 8 - 8;
   static constexpr int REGS = REGS0 > 255 ? 255 : REGS0;
 };
+
+#if HXG_EXPERIMENT == 4
+__device__ unsigned long long g_phase_cycles[10];
+#endif
 
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -118,137 +158,196 @@ template <int P, int Q>
 __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
     fused_jacobian_kernel(const __grid_constant__ FusedParams prm) {
   using D = FDims<P, Q>;
-  constexpr int N = D::N, N3 = D::N3, Q3 = D::Q3, T = D::T;
+  constexpr int N = D::N, N3 = D::N3, T = D::T;
   constexpr int NBX = D::NBX, NBY = D::NBY, NB = D::NB;
   constexpr int BX = D::BX, BY = D::BY, BZ = D::BZ;
   extern __shared__ double smem[];
-  const double* sB = smem;          // Q x N
-  const double* sD = smem + Q * N;  // Q x Q
-  double* Xs = smem + D::TAB;       // node block [c][iz][iy][ix]
-  double* Ebase = Xs + 3 * NB;      // per-element slabs
+  double* Xs = smem;                // node block [c][iz][iy][ix] (padded strides)
+  double* Ebase = Xs + 2 * 3 * D::NBP;  // per-element slabs
   const int tid = threadIdx.x;
-  const int brick = blockIdx.x + prm.brick0;
   const QLayout& lay = prm.lay;
   const BoxDev& box = prm.box;
-  const int bx = brick % lay.nb[0], by = (brick / lay.nb[0]) % lay.nb[1],
-            bz = brick / (lay.nb[0] * lay.nb[1]);
-  // The brick's quadrature state is one contiguous run: start pulling it
-  // into L2 now so the q-function loads below hit L2.
-  const double* st_brick = prm.state + (size_t)lay.brick_points() * brick * kStateStride;
+  // Persistent CTAs walk bricks brick0 + blockIdx.x, + gridDim.x, ...; each
+  // brick's quadrature state is one contiguous run, pulled into L2 one brick
+  // ahead so the q-function loads hit L2.
+  auto prefetch_state = [&](int b) {
 #if HXG_EXPERIMENT != 1
-  if (tid == 0) {
     constexpr unsigned bytes = (unsigned)(sizeof(double) * Q * kStateStride * T);
     constexpr unsigned chunk = 32768;
+    const char* base = reinterpret_cast<const char*>(
+        prm.state + (size_t)lay.brick_points() * b * kStateStride);
 #pragma unroll
     for (unsigned off = 0; off < bytes; off += chunk)
-      prefetch_l2(reinterpret_cast<const char*>(st_brick) + off,
-                  off + chunk <= bytes ? chunk : bytes - off);
-  }
+      prefetch_l2(base + off, off + chunk <= bytes ? chunk : bytes - off);
 #endif
+  };
+  if (tid == 0 && (int)blockIdx.x < prm.nbricks) prefetch_state(prm.brick0 + blockIdx.x);
+#if HXG_EXPERIMENT == 4
+  long long t_last = clock64();
+  long long ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#define HXG_PHASE(i)                    \
+  if (tid == 0) {                       \
+    long long now_ = clock64();         \
+    ph[i] += now_ - t_last;             \
+    t_last = now_;                      \
+  }
+#else
+#define HXG_PHASE(i)
+#endif
+  // 1. node blocks of x: global rows of 3 nbx contiguous doubles, one warp per
+  // row (lane = interleaved (node, component) offset), copied asynchronously
+  // (cp.async) into one of two buffers one brick ahead, so the loads overlap
+  // the previous brick's compute.
+  constexpr int ROW3 = 3 * NBX;
+  static_assert(ROW3 <= 32, "a node row must fit one warp");
+  constexpr int WARPS = T / 32;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int lix = lane / 3, lc = lane - 3 * (lane / 3);
+  const int npx = box.npd[0], npy = box.npd[1];
+  auto issue_block = [&](int b, double* dst) {
+    const int bx = b % lay.nb[0], by = (b / lay.nb[0]) % lay.nb[1], bz = b / (lay.nb[0] * lay.nb[1]);
+    const int nbx = P * min(BX, box.cells[0] - bx * BX) + 1;
+    const int nby = P * min(BY, box.cells[1] - by * BY) + 1;
+    const int nbz = P * min(BZ, box.cells[2] - bz * BZ) + 1;
+    const int node0 = P * bx * BX + npx * (P * by * BY + npy * (P * bz * BZ));
+    if (warp < WARPS && lane < 3 * nbx) {
+      for (int row = warp; row < nby * nbz; row += WARPS) {
+        const int iz = row / nby, iy = row - iz * nby;
+        const double* src = prm.x + 3 * (node0 + npx * (iy + npy * iz)) + lane;
+        const unsigned d = (unsigned)__cvta_generic_to_shared(
+            dst + lc * D::NBP + (iz * D::NBYP + iy) * D::NBXP + lix);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if ((int)blockIdx.x < prm.nbricks) issue_block(prm.brick0 + blockIdx.x, Xs);
+  int cur = 0;
+#pragma unroll 1
+  for (int bi = blockIdx.x; bi < prm.nbricks; bi += gridDim.x, cur ^= 1) {
+  const int brick = prm.brick0 + bi;
+  if (tid == 0 && bi + (int)gridDim.x < prm.nbricks) prefetch_state(brick + gridDim.x);
+  const int bx = brick % lay.nb[0], by = (brick / lay.nb[0]) % lay.nb[1],
+            bz = brick / (lay.nb[0] * lay.nb[1]);
+  const double* st_brick = prm.state + (size_t)lay.brick_points() * brick * kStateStride;
   const int ecx = min(BX, box.cells[0] - bx * BX);
   const int ecy = min(BY, box.cells[1] - by * BY);
   const int ecz = min(BZ, box.cells[2] - bz * BZ);
   const int nbx = P * ecx + 1, nby = P * ecy + 1, nbz = P * ecz + 1;
-  const int npx = box.npd[0], npy = box.npd[1];
   const int node0 = P * bx * BX + npx * (P * by * BY + npy * (P * bz * BZ));
-
-  load_tables<P, Q>(prm.tab, smem);
-  // 1. node block of x: global rows of 3 nbx contiguous doubles, stored one
-  // plane per component.
-  constexpr int ROW3 = 3 * NBX;
-  for (int r = tid; r < NB * 3; r += T) {
-    const int c3 = r % ROW3, row = r / ROW3;
-    const int iy = row % NBY, iz = row / NBY;
-    const int ix = c3 / 3, c = c3 - 3 * ix;
-    if (ix < nbx && iy < nby && iz < nbz) {
-      const int dof = 3 * (node0 + npx * (iy + npy * iz)) + c3;
-      double v = prm.x[dof];
-      if (prm.mask && prm.mask[dof]) v = 0.0;
-      Xs[c * NB + (iz * NBY + iy) * NBX + ix] = v;
+  const int gx0 = P * bx * BX, gy0 = P * by * BY, gz0 = P * bz * BZ;
+  double* Xc = Xs + cur * (3 * D::NBP);
+  // Constrained test: analytic whole-face sets (build_constraints,
+  // operator.hpp:36-55) or the general mask array.
+  auto fixed = [&](int dof, int gx, int gy, int gz) -> bool {
+    if (prm.face_bits >= 0) {
+      const int b = prm.face_bits;
+      return ((b & 1) && gx == 0) || ((b & 2) && gx == npx - 1) || ((b & 4) && gy == 0) ||
+             ((b & 8) && gy == npy - 1) || ((b & 16) && gz == 0) ||
+             ((b & 32) && gz == box.npd[2] - 1);
+    }
+    return prm.mask && prm.mask[dof];
+  };
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  // Zero constrained inputs (operator.hpp:189-193) in the landed block.
+  if (prm.face_bits != 0 && warp < WARPS && lane < 3 * nbx) {
+    for (int row = warp; row < nby * nbz; row += WARPS) {
+      const int iz = row / nby, iy = row - iz * nby;
+      const int dof = 3 * (node0 + npx * (iy + npy * iz)) + lane;
+      if (fixed(dof, gx0 + lix, gy0 + iy, gz0 + iz))
+        Xc[lc * D::NBP + (iz * D::NBYP + iy) * D::NBXP + lix] = 0.0;
     }
   }
-  const int le = tid / D::Q2, qx = tid % Q, qy = (tid / Q) % Q;
+  // Next brick's block into the other buffer (free: its last readers, the
+  // previous brick's P1 pass, are behind the barrier above).
+  if (bi + (int)gridDim.x < prm.nbricks) issue_block(brick + gridDim.x, Xs + (cur ^ 1) * (3 * D::NBP));
+  // Lanes are (column te = qy Q + qx, element le) with elements fastest, so
+  // tid is also the state-layout index t (coalesced state loads).
+  const int le = tid % D::NE, te = tid / D::NE;
   const int lx = le % BX, ly = (le / BX) % BY, lz = le / (BX * BY);
   const bool valid = lx < ecx && ly < ecy && lz < ecz;
-  double* SA = Ebase + le * D::ELEM;  // 3 Q^3
-  double* SB = SA + D::A;             // 3 Q^3
-  double* EOe = SB + D::A;            // 3 N^3
-  __syncthreads();
+  // S[c][arr][k][b][a], arr 0 = interpolated, 1 = d/dx, 2 = d/dy (forward)
+  // or the z-adjoints (backward); EO[c][k][j][i] element outputs.
+  double* S = Ebase + le * D::ELEM;
+  double* EOe = S + D::S;
+  constexpr int Q2 = D::Q2;
+  __syncthreads(); HXG_PHASE(0);
 
-  // ---- forward: G = (D (x) B (x) B, ...) U, all components per phase ----
-  // F1: x-contraction T1[c][k][j][a] = sum_i B[a][i] U[c][k][j][i] (slab A).
-  if (qy < N) {
-    double bx_[N];
+  // ---- forward: G = (Bd (x) B (x) B, B (x) Bd (x) B, B (x) B (x) Bd) U -----
+  // The direct tensor-product gradient (deriv tabulated at the points,
+  // basis.hpp:144, = colloc_deriv * interp in exact arithmetic).  x and y
+  // passes run on (component, z-plane) owners in registers; the z pass on
+  // (qx, qy) column owners, so each value crosses shared memory once.
+  // P1: plane tasks (c, k), te < 3N.
+  // (3N plane tasks per element; Q^2 < 3N only for p = 1, q = 2.)
+#pragma unroll 1
+  for (int task = te; task < 3 * N; task += Q2) {
+    const int c = task / N, k = task - c * N;
+    const double* Xp = Xc + c * D::NBP + ((P * lz + k) * D::NBYP + P * ly) * D::NBXP + P * lx;
+    double u[N][N];
 #pragma unroll
-    for (int i = 0; i < N; ++i) bx_[i] = sB[qx * N + i];
-    const double* Xe = Xs + ((P * lz * NBY + P * ly + qy) * NBX + P * lx);
+    for (int j = 0; j < N; ++j)
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
+      for (int i = 0; i < N; ++i) u[j][i] = Xp[j * D::NBXP + i];
+    double ab[N][Q], ad[N][Q];
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        double s = 0.0;
+    for (int j = 0; j < N; ++j)
 #pragma unroll
-        for (int i = 0; i < N; ++i) s += bx_[i] * Xe[c * NB + k * NBY * NBX + i];
-        SA[((c * N + k) * N + qy) * Q + qx] = s;
-      }
-  }
-  __syncthreads();
-  // F2: y then z in registers; values V[c][qz][b][a] -> slab B; z-derivative.
-  double g[3][3][Q];
-  {
-    double by_[N];
+      for (int a = 0; a < Q; ++a) {
+        double sb = 0.0, sd = 0.0;
 #pragma unroll
-    for (int j = 0; j < N; ++j) by_[j] = sB[qy * N + j];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      double t2[N];
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        double s = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; ++j) s += by_[j] * SA[((c * N + k) * N + j) * Q + qx];
-        t2[k] = s;
-      }
-      double v[Q];
-#pragma unroll
-      for (int z = 0; z < Q; ++z) {
-        double s = 0.0;
-#pragma unroll
-        for (int k = 0; k < N; ++k) s += prm.B[z * N + k] * t2[k];
-        v[z] = s;
-        SB[((c * Q + z) * Q + qy) * Q + qx] = s;
-      }
-#pragma unroll
-      for (int z = 0; z < Q; ++z) {
-        double s = 0.0;
-#pragma unroll
-        for (int r = 0; r < Q; ++r) s += prm.Dc[z * Q + r] * v[r];
-        g[c][2][z] = s;
-      }
-    }
-  }
-  __syncthreads();
-  // F3: x and y collocated derivatives from slab B.
-  {
-    double dx_[Q], dy_[Q];
-#pragma unroll
-    for (int r = 0; r < Q; ++r) {
-      dx_[r] = sD[qx * Q + r];
-      dy_[r] = sD[qy * Q + r];
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int z = 0; z < Q; ++z) {
-        double sx = 0.0, sy = 0.0;
-#pragma unroll
-        for (int r = 0; r < Q; ++r) {
-          sx += dx_[r] * SB[((c * Q + z) * Q + qy) * Q + r];
-          sy += dy_[r] * SB[((c * Q + z) * Q + r) * Q + qx];
+        for (int i = 0; i < N; ++i) {
+          sb += prm.B[a * N + i] * u[j][i];
+          sd += prm.Bd[a * N + i] * u[j][i];
         }
-        g[c][0][z] = sx;
-        g[c][1][z] = sy;
+        ab[j][a] = sb;
+        ad[j][a] = sd;
       }
+    double* S0 = S + ((c * 3 + 0) * N + k) * Q2;
+    double* S1 = S + ((c * 3 + 1) * N + k) * Q2;
+    double* S2 = S + ((c * 3 + 2) * N + k) * Q2;
+#pragma unroll
+    for (int b = 0; b < Q; ++b)
+#pragma unroll
+      for (int a = 0; a < Q; ++a) {
+        double tb = 0.0, tdy = 0.0, tdx = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          tb += prm.B[b * N + j] * ab[j][a];
+          tdy += prm.Bd[b * N + j] * ab[j][a];
+          tdx += prm.B[b * N + j] * ad[j][a];
+        }
+        S0[b * Q + a] = tb;
+        S1[b * Q + a] = tdx;
+        S2[b * Q + a] = tdy;
+      }
+  }
+  __syncthreads(); HXG_PHASE(1);
+  // P2: column owners (qx, qy): z pass for the three arrays.
+  double g[3][3][Q];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double tb[N], tdx[N], tdy[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      tb[k] = S[((c * 3 + 0) * N + k) * Q2 + te];
+      tdx[k] = S[((c * 3 + 1) * N + k) * Q2 + te];
+      tdy[k] = S[((c * 3 + 2) * N + k) * Q2 + te];
+    }
+#pragma unroll
+    for (int z = 0; z < Q; ++z) {
+      double gx = 0.0, gy = 0.0, gz = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        gx += prm.B[z * N + k] * tdx[k];
+        gy += prm.B[z * N + k] * tdy[k];
+        gz += prm.Bd[z * N + k] * tb[k];
+      }
+      g[c][0][z] = gx;
+      g[c][1][z] = gy;
+      g[c][2][z] = gz;
+    }
   }
 
   // ---- q-function on the streamed state --------------------------------
@@ -273,7 +372,13 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int d = 0; d < 3; ++d) G[3 * c + d] = g[c][d][qz];
+#if HXG_EXPERIMENT == 2
+      // timing experiment: trivial q-function (state still loaded)
+#pragma unroll
+      for (int q9 = 0; q9 < 9; ++q9) H[q9] = G[q9] * st[q9] + st[q9 + 8];
+#else
       jacobian_qf(prm.mu, prm.lambda, G, st, H);
+#endif
       if (prm.perturb != 0.0) {
 #pragma unroll
         for (int k = 0; k < 9; ++k) H[k] += prm.perturb * st[0] * G[k];
@@ -287,90 +392,71 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
 #pragma unroll
       for (int d = 0; d < 3; ++d) g[c][d][qz] = H[3 * c + d];
   }
-  __syncthreads();  // slabs A/B free
+  __syncthreads(); HXG_PHASE(2);  // slabs free
 
-  // ---- backward: exact adjoint ------------------------------------------
-  // B1: Hx -> A, Hy -> B.
+  // ---- backward: exact adjoint of the forward passes ---------------------
+  // Q1: column owners: z adjoints R0 = Bd_z^T Hz, R1 = B_z^T Hx, R2 = B_z^T Hy.
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
-    for (int z = 0; z < Q; ++z) {
-      SA[((c * Q + z) * Q + qy) * Q + qx] = g[c][0][z];
-      SB[((c * Q + z) * Q + qy) * Q + qx] = g[c][1][z];
-    }
-  __syncthreads();
-  // B2: acc = Dx^T Hx + Dy^T Hy + Dz^T Hz (reference order), then z interp^T.
-  double w[3][N];
-  {
-    double dxt[Q], dyt[Q];
-#pragma unroll
-    for (int r = 0; r < Q; ++r) {
-      dxt[r] = sD[r * Q + qx];
-      dyt[r] = sD[r * Q + qy];
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      double acc[Q];
+    for (int k = 0; k < N; ++k) {
+      double r0 = 0.0, r1 = 0.0, r2 = 0.0;
 #pragma unroll
       for (int z = 0; z < Q; ++z) {
-        double sx = 0.0, sy = 0.0, sz = 0.0;
-#pragma unroll
-        for (int r = 0; r < Q; ++r) {
-          sx += dxt[r] * SA[((c * Q + z) * Q + qy) * Q + r];
-          sy += dyt[r] * SB[((c * Q + z) * Q + r) * Q + qx];
-          sz += prm.Dc[r * Q + z] * g[c][2][r];
-        }
-        acc[z] = (sx + sy) + sz;
+        r0 += prm.Bd[z * N + k] * g[c][2][z];
+        r1 += prm.B[z * N + k] * g[c][0][z];
+        r2 += prm.B[z * N + k] * g[c][1][z];
       }
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        double s = 0.0;
-#pragma unroll
-        for (int z = 0; z < Q; ++z) s += prm.B[z * N + k] * acc[z];
-        w[c][k] = s;
-      }
+      S[((c * 3 + 0) * N + k) * Q2 + te] = r0;
+      S[((c * 3 + 1) * N + k) * Q2 + te] = r1;
+      S[((c * 3 + 2) * N + k) * Q2 + te] = r2;
     }
-  }
-  __syncthreads();
-  // B3: W[c][k][b][a] -> A.
+  __syncthreads(); HXG_PHASE(3);
+  // Q2: plane tasks (c, k): y adjoints then x adjoints, in registers.
+#pragma unroll 1
+  for (int task = te; task < 3 * N; task += Q2) {
+    const int c = task / N, k = task - c * N;
+    const double* S0 = S + ((c * 3 + 0) * N + k) * Q2;
+    const double* S1 = S + ((c * 3 + 1) * N + k) * Q2;
+    const double* S2 = S + ((c * 3 + 2) * N + k) * Q2;
+    double ab[N][Q], ad[N][Q];
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
+    for (int j = 0; j < N; ++j)
 #pragma unroll
-    for (int k = 0; k < N; ++k) SA[((c * N + k) * Q + qy) * Q + qx] = w[c][k];
-  __syncthreads();
-  // B4: y interp^T: T[c][k][j][a] = sum_b B[b][j] W[c][k][b][a] -> B.
-  if (qy < N) {
-    double bcy[Q];
+      for (int a = 0; a < Q; ++a) {
+        ab[j][a] = 0.0;
+        ad[j][a] = 0.0;
+      }
 #pragma unroll
-    for (int b = 0; b < Q; ++b) bcy[b] = sB[b * N + qy];
+    for (int b = 0; b < Q; ++b)
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
+      for (int a = 0; a < Q; ++a) {
+        const double r0 = S0[b * Q + a], r1 = S1[b * Q + a], r2 = S2[b * Q + a];
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
+        for (int j = 0; j < N; ++j) {
+          ab[j][a] += prm.B[b * N + j] * r0 + prm.Bd[b * N + j] * r2;
+          ad[j][a] += prm.B[b * N + j] * r1;
+        }
+      }
+    double* Oc = EOe + (c * N + k) * N * N;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
         double s = 0.0;
 #pragma unroll
-        for (int b = 0; b < Q; ++b) s += bcy[b] * SA[((c * N + k) * Q + b) * Q + qx];
-        SB[((c * N + k) * N + qy) * Q + qx] = s;
+        for (int a = 0; a < Q; ++a) s += prm.B[a * N + i] * ab[j][a] + prm.Bd[a * N + i] * ad[j][a];
+        Oc[j * N + i] = valid ? s : 0.0;  // padding elements add exact zeros
       }
   }
-  __syncthreads();
-  // B5: x interp^T: EO[c][k][j][i] = sum_a B[a][i] T[c][k][j][a].
-  if (qx < N && qy < N) {
-    double bcx[Q];
-#pragma unroll
-    for (int a = 0; a < Q; ++a) bcx[a] = sB[a * N + qx];
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        double s = 0.0;
-#pragma unroll
-        for (int a = 0; a < Q; ++a) s += bcx[a] * SB[((c * N + k) * N + qy) * Q + a];
-        EOe[(c * N + k) * N * N + qy * N + qx] = valid ? s : 0.0;  // padding elements add 0
-      }
-  }
-  __syncthreads();
+  __syncthreads(); HXG_PHASE(4);
 
+#if HXG_EXPERIMENT == 3
+  // timing experiment: no overlap-add / stores of y
+  if (tid == 0 && brick < 0) prm.y[0] = Ebase[0];
+  __syncthreads(); HXG_PHASE(5);
+  continue;
+#endif
   // ---- overlap-add onto the node block: x, then y, then z ---------------
   // A shared node takes (lower element + upper element) in each direction.
   // AX [lz][ly][c][k][j][ix] and AY [lz][c][k][iy][ix] live in the elements'
@@ -382,7 +468,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
   for (int row = tid; row < RX; row += T) {
     const int kj = row % (N * N), lzlyc = row / (N * N);
     const int c = lzlyc % 3, lzly = lzlyc / 3;
-    const double* e = Ebase + lzly * BX * D::ELEM + 2 * D::A + c * N3 + kj * N;
+    const double* e = Ebase + lzly * BX * D::ELEM + D::S + c * N3 + kj * N;
     double* out = rowp(row);
 #pragma unroll
     for (int ix = 0; ix < NBX; ++ix) {
@@ -393,7 +479,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
       out[ix] = v;
     }
   }
-  __syncthreads();
+  __syncthreads(); HXG_PHASE(6);
   // y pass: one thread per (lz, c, k, iy) row.
   constexpr int RY = D::RY;
   for (int row = tid; row < RY; row += T) {
@@ -410,28 +496,37 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
 #pragma unroll
     for (int ix = 0; ix < NBX; ++ix) out[ix] = two ? b[ix] + a[ix] : a[ix];
   }
-  __syncthreads();
+  __syncthreads(); HXG_PHASE(7);
   // z pass fused with the stores: consecutive threads walk the global node
   // rows (3 nbx interleaved doubles, contiguous) for coalesced stores.
   double* part = prm.partial + (size_t)brick * (D::NB * 3);
   const unsigned long long pol_keep = policy_evict_last();
-  for (int w = tid; w < NB * 3; w += T) {
-    const int c3 = w % ROW3, row = w / ROW3;
-    const int iy = row % NBY, iz = row / NBY;
-    const int ix = c3 / 3, c = c3 - 3 * ix;
-    if (ix >= nbx || iy >= nby || iz >= nbz) continue;
-    const int lzh = iz / P < BZ ? iz / P : BZ - 1;
-    const int k = iz - P * lzh;
-    const int ra = RX + ((lzh * 3 + c) * N + k) * NBY + iy;
-    double s = rowp(ra)[ix];
-    if (k == 0 && lzh > 0) s = rowp(ra + (P - 3 * N) * NBY)[ix] + s;  // lz - 1, k = P
-    if (ix == 0 || iy == 0 || iz == 0 || ix == nbx - 1 || iy == nby - 1 || iz == nbz - 1) {
-      st_keep(part + w, s, pol_keep);
-    } else {
-      const int dof = 3 * (node0 + npx * (iy + npy * iz)) + c3;
-      prm.y[dof] = (prm.mask && prm.mask[dof]) ? prm.x[dof] : s;
+  if (warp < WARPS && lane < 3 * nbx) {
+    const int ix = lix, c = lc;
+#pragma unroll 2
+    for (int row = warp; row < nby * nbz; row += WARPS) {
+      const int iz = row / nby, iy = row - iz * nby;
+      const int lzh = iz / P < BZ ? iz / P : BZ - 1;
+      const int k = iz - P * lzh;
+      const int ra = RX + ((lzh * 3 + c) * N + k) * NBY + iy;
+      double s = rowp(ra)[ix];
+      if (k == 0 && lzh > 0) s = rowp(ra + (P - 3 * N) * NBY)[ix] + s;  // lz - 1, k = P
+      if (ix == 0 || iy == 0 || iz == 0 || ix == nbx - 1 || iy == nby - 1 || iz == nbz - 1) {
+        st_keep(part + (iz * NBY + iy) * ROW3 + lane, s, pol_keep);
+      } else {
+        const int dof = 3 * (node0 + npx * (iy + npy * iz)) + lane;
+        prm.y[dof] = fixed(dof, gx0 + ix, gy0 + iy, gz0 + iz) ? prm.x[dof] : s;
+      }
     }
   }
+  // (the next iteration's first barrier orders these slab reads before the
+  // slabs are rewritten)
+  HXG_PHASE(8);
+  }  // brick loop
+#if HXG_EXPERIMENT == 4
+  if (tid == 0)
+    for (int i = 0; i < 10; ++i) atomicAdd(&g_phase_cycles[i], (unsigned long long)ph[i]);
+#endif
 }
 
 // Sums brick-boundary partials: nodes on planes g_d = k P B_d (or the domain's
@@ -485,7 +580,31 @@ __global__ void fused_fixup_kernel(const __grid_constant__ FusedParams prm) {
   }
 }
 
+// Persistent grid: every resident CTA slot of the device, capped by the work.
+template <class K>
+unsigned persistent_grid(K kernel, int threads, size_t smem, int work) {
+  static int sms = 0;
+  if (!sms) HXG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  int per_sm = 0;
+  HXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  long long g = (long long)(per_sm > 0 ? per_sm : 1) * sms;
+  if (g > work) g = work;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
 }  // namespace
+
+#if HXG_EXPERIMENT == 4
+extern "C" int hxg_debug_phase_cycles(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 10);
+  if (reset) {
+    unsigned long long z[10] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 bool fused_supported(int p, int q) {
   bool ok = false;
@@ -506,13 +625,14 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
   prm.x = du;
   prm.y = y;
   prm.mask = op.mask();
+  prm.face_bits = op.face_bits();
   prm.tab = op.tab_.p;
   prm.state = op.state_->data.p;
   prm.mu = op.mu_;
   prm.lambda = op.lambda_;
   prm.perturb = op.perturb_;
   for (size_t i = 0; i < op.interp_.size(); ++i) prm.B[i] = op.interp_[i];
-  for (size_t i = 0; i < op.colloc_.size(); ++i) prm.Dc[i] = op.colloc_[i];
+  for (size_t i = 0; i < op.deriv_.size(); ++i) prm.Bd[i] = op.deriv_[i];
   dispatch_pq(op.p_, op.q_, [&](auto Pc, auto Qc) {
     constexpr int P = decltype(Pc)::value, Q = decltype(Qc)::value;
     using D = FDims<P, Q>;
@@ -524,7 +644,9 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
     HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));
-    k<<<(unsigned)op.lay_.num_bricks(), D::T, smem, op.stream_>>>(prm);
+    prm.brick0 = 0;
+    prm.nbricks = (int)op.lay_.num_bricks();
+    k<<<persistent_grid(k, D::T, smem, prm.nbricks), D::T, smem, op.stream_>>>(prm);
     HXG_CUDA(cudaGetLastError());
     dim3 fb(32, 4), fg((op.box_.npd[1] + 3) / 4, op.box_.npd[2]);
     fused_fixup_kernel<P, Q><<<fg, fb, 0, op.stream_>>>(prm);
@@ -551,13 +673,14 @@ void fused_jacobian_host(Operator& op, const double* xh, double* yh) {
   prm.x = pp.x.p;
   prm.y = pp.y.p;
   prm.mask = op.mask();
+  prm.face_bits = op.face_bits();
   prm.tab = op.tab_.p;
   prm.state = op.state_->data.p;
   prm.mu = op.mu_;
   prm.lambda = op.lambda_;
   prm.perturb = op.perturb_;
   for (size_t i = 0; i < op.interp_.size(); ++i) prm.B[i] = op.interp_[i];
-  for (size_t i = 0; i < op.colloc_.size(); ++i) prm.Dc[i] = op.colloc_[i];
+  for (size_t i = 0; i < op.deriv_.size(); ++i) prm.Bd[i] = op.deriv_[i];
   dispatch_pq(op.p_, op.q_, [&](auto Pc, auto Qc) {
     constexpr int P = decltype(Pc)::value, Q = decltype(Qc)::value;
     using D = FDims<P, Q>;
@@ -592,7 +715,8 @@ void fused_jacobian_host(Operator& op, const double* xh, double* yh) {
       HXG_CUDA(cudaStreamWaitEvent(pp.comp, pp.in_ready[i], 0));
       FusedParams pc = prm;
       pc.brick0 = lb * layer;
-      k<<<(unsigned)((le - lb) * layer), D::T, smem, pp.comp>>>(pc);
+      pc.nbricks = (le - lb) * layer;
+      k<<<persistent_grid(k, D::T, smem, pc.nbricks), D::T, smem, pp.comp>>>(pc);
       HXG_CUDA(cudaGetLastError());
       const int zs = i == 0 ? 0 : pb2 * lb;
       const int ze = i == C - 1 ? npz : pb2 * le;

@@ -69,6 +69,20 @@ Operator::Operator(int p, int q, const int cells[3], const std::vector<double>& 
   if (mask_host) {
     mask_host_.assign(mask_host, mask_host + size());
     mask_.upload(mask_host_);
+    // Whole-face detection: faces whose every DoF is constrained; the mask
+    // is analytic when it equals the union of those faces.
+    int bits = 0;
+    for (int f = 0; f < 6; ++f) {
+      std::vector<uint8_t> fm;
+      face_mask(cells, p, 1 << f, fm);
+      bool all = true;
+      for (size_t i = 0; i < fm.size() && all; ++i)
+        if (fm[i] && !mask_host_[i]) all = false;
+      if (all) bits |= 1 << f;
+    }
+    std::vector<uint8_t> gen;
+    face_mask(cells, p, bits, gen);
+    face_bits_ = gen == mask_host_ ? bits : -1;
   }
   if (!state_) state_ = std::make_shared<State>();
   size_t need = (size_t)lay_.total_points() * kStateStride;

@@ -102,6 +102,10 @@ class Operator {
   const QLayout& layout() const { return lay_; }
   const int* cells() const { return cells_; }
   const uint8_t* mask() const { return mask_.n ? mask_.p : nullptr; }
+  // >= 0 when the constraint mask is exactly a union of whole faces (all
+  // components) — bit f = Face f — so kernels can test it analytically;
+  // -1 for general masks.
+  int face_bits() const { return face_bits_; }
   const std::vector<uint8_t>& mask_host() const { return mask_host_; }
   const std::shared_ptr<State>& state() const { return state_; }
   const std::shared_ptr<Geometry>& geometry() const { return geometry_; }
@@ -152,6 +156,7 @@ class Operator {
   double mu_, lambda_;
   double load_scale_ = 1.0, perturb_ = 0.0;
   int variant_ = 0;
+  int face_bits_ = 0;
   std::vector<double> interp_, deriv_, colloc_;
   std::vector<uint8_t> mask_host_;
   DevBuf<double> tab_;     // B (Q x N) then Dc (Q x Q)
