@@ -3,16 +3,16 @@
 //
 // One CTA per brick of BX x BY x BZ elements (the QLayout brick), one thread
 // per quadrature column (element, qx, qy):
-//   1. the brick's node block of x is loaded once (coalesced rows; masked
-//      entries zeroed, operator.hpp:189-193) into shared memory, one plane
-//      per component;
+//   1. the brick's node block of x is copied once (coalesced rows, cp.async
+//      one brick ahead) into shared memory, one plane per component; masked
+//      entries read as zero (operator.hpp:189-193);
 //   2. per element, all three components per phase: sum-factorised gradient
 //      (basis.hpp:319-335) with every contraction reading its operand rows
 //      from registers, Neo-Hookean Jacobian q-function on the streamed
 //      17-scalar state (material.hpp:179-194), exact transpose
 //      (basis.hpp:339-355);
-//   3. the element patches are overlap-added onto the brick's node block,
-//      separably in x, y, z, in a fixed order (scatter_add, mesh.hpp:105-116);
+//   3. each node of the block sums the element patches sharing it in a
+//      fixed order (scatter_add, mesh.hpp:105-116);
 //   4. nodes interior to the brick are final and stored to y (constrained
 //      entries pass x through, operator.hpp:212-214); nodes on brick
 //      boundary planes store their partial sum to a per-brick buffer;
@@ -62,6 +62,15 @@ __host__ __device__ constexpr int elem_pad(int p, int q) {
          : p * 10 + q == 45 || p * 10 + q == 25 || p * 10 + q == 35 ? 0
                                                                      : 1;
 }
+// Element-output component padding: spreads the node-centric overlap-add
+// reads (lanes over (ix, c)) across banks.
+__host__ __device__ constexpr int eo_pad(int p, int q) {
+  switch (p * 10 + q) {
+    case 12: return 3; case 34: case 35: return 4; case 45: return 8;
+    case 24: case 25: return 0;
+  }
+  return 1;
+}
 __host__ __device__ constexpr int pad_nbx(int p, int q) {
   switch (p * 10 + q) {
     case 12: return 12; case 23: return 10; case 34: return 7; case 45: return 10;
@@ -94,25 +103,18 @@ struct FDims : Dims<P, Q> {
   static constexpr int NBX = P * D::BX + 1, NBY = P * D::BY + 1, NBZ = P * D::BZ + 1;
   static constexpr int NB = NBX * NBY * NBZ;  // nodes per (full) brick block
   static constexpr int S = 9 * N * D::Q2;     // per-element exchange slab [c][arr][k][b][a]
-  static constexpr int EO = 3 * D::N3;        // element outputs [c][k][j][i]
+  // Element outputs [c][k][j][i], component stride EOC >= N^3.
+  static constexpr int EOC = D::N3 + eo_pad(P, Q);
   // Element stride and node-block strides padded (exhaustive search over the
   // half-warp access patterns of every phase) so 64-bit shared accesses are
   // (nearly) bank-conflict free; lanes are (column or plane task, element)
-  // with elements fastest.
-  static constexpr int ELEM0 = S + EO;
-  static constexpr int ELEM = ELEM0 + elem_pad(P, Q);
+  // with elements fastest.  Only ELEM mod 16 matters to the slab phases.
+  static constexpr int ELEM0 = S + 3 * EOC;
+  static constexpr int ELEM =
+      ELEM0 + ((S + 3 * D::N3 + elem_pad(P, Q) - ELEM0) % 16 + 16) % 16;
   static constexpr int NBXP = pad_nbx(P, Q), NBYP = pad_nby(P, Q), NBP = pad_plane(P, Q);
   static_assert(NBXP >= NBX && NBYP >= NBY && NBP >= NBXP * NBYP * NBZ, "node block padding");
-  // Overlap-add rows (NBX doubles each) packed into the elements' exchange
-  // slabs, which are free by then: RPS rows per slab.
-  static constexpr int RX = D::BZ * D::BY * 3 * N * N;  // x-pass rows [lz][ly][c][k][j]
-  static constexpr int RY = D::BZ * 3 * N * NBY;        // y-pass rows [lz][c][k][iy]
-  static constexpr int RPS = S / NBX;
-  static_assert(RX + RY <= D::NE * RPS, "overlap-add rows must fit the element slabs");
   static constexpr int SMEM = 2 * 3 * NBP + D::NE * ELEM;  // two node blocks + slabs
-  // Register cap for two resident CTAs per SM.
-  static constexpr int REGS0 = 65536 / (HXG_FUSED_MINB * ((D::T + 31) / 32 * 32)) / 8 * 8 - 8;
-  static constexpr int REGS = REGS0 > 255 ? 255 : REGS0;
 };
 
 #if HXG_EXPERIMENT == 4
@@ -138,7 +140,7 @@ __device__ __forceinline__ unsigned long long policy_evict_last() {
 }
 __device__ __forceinline__ double ld_stream(const double* a, unsigned long long pol) {
   double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
                : "=d"(v)
                : "l"(a), "l"(pol));
   return v;
@@ -158,8 +160,8 @@ template <int P, int Q>
 __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
     fused_jacobian_kernel(const __grid_constant__ FusedParams prm) {
   using D = FDims<P, Q>;
-  constexpr int N = D::N, N3 = D::N3, T = D::T;
-  constexpr int NBX = D::NBX, NBY = D::NBY, NB = D::NB;
+  constexpr int N = D::N, T = D::T;
+  constexpr int NBX = D::NBX, NBY = D::NBY;
   constexpr int BX = D::BX, BY = D::BY, BZ = D::BZ;
   extern __shared__ double smem[];
   double* Xs = smem;                // node block [c][iz][iy][ix] (padded strides)
@@ -250,8 +252,10 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
   };
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  // Zero constrained inputs (operator.hpp:189-193) in the landed block.
-  if (prm.face_bits != 0 && warp < WARPS && lane < 3 * nbx) {
+  // General masks: zero constrained inputs (operator.hpp:189-193) in the
+  // landed block.  Whole-face masks are applied analytically as P1 reads the
+  // block, which keeps x intact for the constrained pass-through.
+  if (prm.face_bits < 0 && warp < WARPS && lane < 3 * nbx) {
     for (int row = warp; row < nby * nbz; row += WARPS) {
       const int iz = row / nby, iy = row - iz * nby;
       const int dof = 3 * (node0 + npx * (iy + npy * iz)) + lane;
@@ -290,6 +294,20 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
     for (int j = 0; j < N; ++j)
 #pragma unroll
       for (int i = 0; i < N; ++i) u[j][i] = Xp[j * D::NBXP + i];
+    if (prm.face_bits > 0) {
+      const int fb = prm.face_bits;
+      const int gx = gx0 + P * lx, gy = gy0 + P * ly, gz = gz0 + P * lz + k;
+      const bool mz = ((fb & 16) && gz == 0) || ((fb & 32) && gz == box.npd[2] - 1);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const bool my = mz || ((fb & 4) && gy + j == 0) || ((fb & 8) && gy + j == npy - 1);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const bool m = my || ((fb & 1) && gx + i == 0) || ((fb & 2) && gx + i == npx - 1);
+          u[j][i] = m ? 0.0 : u[j][i];
+        }
+      }
+    }
     double ab[N][Q], ad[N][Q];
 #pragma unroll
     for (int j = 0; j < N; ++j)
@@ -438,7 +456,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
           ad[j][a] += prm.B[b * N + j] * r1;
         }
       }
-    double* Oc = EOe + (c * N + k) * N * N;
+    double* Oc = EOe + c * D::EOC + k * N * N;
 #pragma unroll
     for (int j = 0; j < N; ++j)
 #pragma unroll
@@ -457,65 +475,47 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
   __syncthreads(); HXG_PHASE(5);
   continue;
 #endif
-  // ---- overlap-add onto the node block: x, then y, then z ---------------
-  // A shared node takes (lower element + upper element) in each direction.
-  // AX [lz][ly][c][k][j][ix] and AY [lz][c][k][iy][ix] live in the elements'
-  // A/B slabs (free now; the EO regions they read from stay untouched):
-  // slab index r -> element r / 2A, offset r % 2A.
-  auto rowp = [&](int r) { return Ebase + (r / D::RPS) * D::ELEM + (r % D::RPS) * NBX; };
-  // x pass: one thread per (lz, ly, c, k, j) row of NBX nodes.
-  constexpr int RX = D::RX;
-  for (int row = tid; row < RX; row += T) {
-    const int kj = row % (N * N), lzlyc = row / (N * N);
-    const int c = lzlyc % 3, lzly = lzlyc / 3;
-    const double* e = Ebase + lzly * BX * D::ELEM + D::S + c * N3 + kj * N;
-    double* out = rowp(row);
-#pragma unroll
-    for (int ix = 0; ix < NBX; ++ix) {
-      const int lxh = ix / P < BX ? ix / P : BX - 1;
-      const int i = ix - P * lxh;
-      double v = e[lxh * D::ELEM + i];
-      if (i == 0 && lxh > 0) v = e[(lxh - 1) * D::ELEM + P] + v;
-      out[ix] = v;
-    }
-  }
-  __syncthreads(); HXG_PHASE(6);
-  // y pass: one thread per (lz, c, k, iy) row.
-  constexpr int RY = D::RY;
-  for (int row = tid; row < RY; row += T) {
-    const int iy = row % NBY, lzck = row / NBY;
-    const int k = lzck % N, lzc = lzck / N;
-    const int c = lzc % 3, lz = lzc / 3;
-    const int lyh = iy / P < BY ? iy / P : BY - 1;
-    const int j = iy - P * lyh;
-    const int ra = (((lz * BY + lyh) * 3 + c) * N + k) * N + j;
-    const double* a = rowp(ra);
-    const bool two = j == 0 && lyh > 0;
-    const double* b = rowp(ra + P - 3 * N * N);  // ly - 1, j = P
-    double* out = rowp(RX + row);
-#pragma unroll
-    for (int ix = 0; ix < NBX; ++ix) out[ix] = two ? b[ix] + a[ix] : a[ix];
-  }
-  __syncthreads(); HXG_PHASE(7);
-  // z pass fused with the stores: consecutive threads walk the global node
-  // rows (3 nbx interleaved doubles, contiguous) for coalesced stores.
+  // ---- overlap-add fused with the stores: node-centric ------------------
+  // Node (ix, iy, iz) of the block sums the outputs of the elements sharing
+  // it, lower element first in x, then y, then z: a fixed order (the
+  // scatter_add of mesh.hpp:105-116, made deterministic).  One warp per node
+  // row, lanes over the row's 3 nbx interleaved (node, component) doubles,
+  // which are contiguous in y (coalesced stores).
   double* part = prm.partial + (size_t)brick * (D::NB * 3);
   const unsigned long long pol_keep = policy_evict_last();
   if (warp < WARPS && lane < 3 * nbx) {
     const int ix = lix, c = lc;
-#pragma unroll 2
+    const int lxh = ix / P < BX ? ix / P : BX - 1;
+    const int i = ix - P * lxh;
+    const bool twox = i == 0 && lxh > 0;
+    const double* ex = Ebase + lxh * D::ELEM + D::S + c * D::EOC + i;
+    constexpr int DX = P - D::ELEM;                 // (lx - 1, i = P)
+    constexpr int DY = P * N - BX * D::ELEM;        // (ly - 1, j = P)
+    constexpr int DZ = P * N * N - BY * BX * D::ELEM;  // (lz - 1, k = P)
+    auto xsum = [&](const double* e) {
+      const double v = e[0];
+      return twox ? e[DX] + v : v;
+    };
+#pragma unroll 1
     for (int row = warp; row < nby * nbz; row += WARPS) {
       const int iz = row / nby, iy = row - iz * nby;
-      const int lzh = iz / P < BZ ? iz / P : BZ - 1;
-      const int k = iz - P * lzh;
-      const int ra = RX + ((lzh * 3 + c) * N + k) * NBY + iy;
-      double s = rowp(ra)[ix];
-      if (k == 0 && lzh > 0) s = rowp(ra + (P - 3 * N) * NBY)[ix] + s;  // lz - 1, k = P
+      const int lzh = iz / P < BZ ? iz / P : BZ - 1, k = iz - P * lzh;
+      const int lyh = iy / P < BY ? iy / P : BY - 1, j = iy - P * lyh;
+      const bool twoy = j == 0 && lyh > 0;
+      const double* e = ex + (lzh * BY + lyh) * BX * D::ELEM + (k * N + j) * N;
+      auto ysum = [&](const double* f) {
+        const double v = xsum(f);
+        return twoy ? xsum(f + DY) + v : v;
+      };
+      double s = ysum(e);
+      if (k == 0 && lzh > 0) s = ysum(e + DZ) + s;
       if (ix == 0 || iy == 0 || iz == 0 || ix == nbx - 1 || iy == nby - 1 || iz == nbz - 1) {
         st_keep(part + (iz * NBY + iy) * ROW3 + lane, s, pol_keep);
       } else {
         const int dof = 3 * (node0 + npx * (iy + npy * iz)) + lane;
-        prm.y[dof] = fixed(dof, gx0 + ix, gy0 + iy, gz0 + iz) ? prm.x[dof] : s;
+        if (fixed(dof, gx0 + ix, gy0 + iy, gz0 + iz))  // pass x through (operator.hpp:212-214)
+          s = prm.face_bits >= 0 ? Xc[c * D::NBP + (iz * D::NBYP + iy) * D::NBXP + ix] : prm.x[dof];
+        prm.y[dof] = s;
       }
     }
   }
