@@ -28,8 +28,11 @@
 #ifndef HXG_EXPERIMENT
 #define HXG_EXPERIMENT 0
 #endif
-#ifndef HXG_FUSED_MINB
-#define HXG_FUSED_MINB 2
+#ifndef HXG_MINB_HIGHP
+#define HXG_MINB_HIGHP 3
+#endif
+#ifndef HXG_SLOTS_HIGHP
+#define HXG_SLOTS_HIGHP 0
 #endif
 
 namespace hxg {
@@ -96,6 +99,17 @@ __host__ __device__ constexpr int pad_plane(int p, int q) {
   return 0;
 }
 
+// Resident CTAs per SM the register allocation targets: two for the 9-warp
+// bricks; three for the 4-warp (3, 4) brick (shared memory allows it).
+__host__ __device__ constexpr int fused_min_blocks(int p, int q) {
+  return p * 10 + q == 34 ? HXG_MINB_HIGHP : 2;
+}
+// Column-private shared slots for the gradients (see P2).
+__host__ __device__ constexpr bool fused_slots(int p, int q) {
+  return p * 10 + q == 12 || p * 10 + q == 13 || p * 10 + q == 23 ||
+         (HXG_SLOTS_HIGHP && (p * 10 + q == 34 || p * 10 + q == 45));
+}
+
 template <int P, int Q>
 struct FDims : Dims<P, Q> {
   using D = Dims<P, Q>;
@@ -157,7 +171,7 @@ __device__ __forceinline__ double ld_once(const double* a, unsigned long long po
 }
 
 template <int P, int Q>
-__global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
+__global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
     fused_jacobian_kernel(const __grid_constant__ FusedParams prm) {
   using D = FDims<P, Q>;
   constexpr int N = D::N, T = D::T;
@@ -206,31 +220,60 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
   const int lane = tid & 31, warp = tid >> 5;
   const int lix = lane / 3, lc = lane - 3 * (lane / 3);
   const int npx = box.npd[0], npy = box.npd[1];
-  auto issue_block = [&](int b, double* dst) {
-    const int bx = b % lay.nb[0], by = (b / lay.nb[0]) % lay.nb[1], bz = b / (lay.nb[0] * lay.nb[1]);
-    const int nbx = P * min(BX, box.cells[0] - bx * BX) + 1;
-    const int nby = P * min(BY, box.cells[1] - by * BY) + 1;
-    const int nbz = P * min(BZ, box.cells[2] - bz * BZ) + 1;
-    const int node0 = P * bx * BX + npx * (P * by * BY + npy * (P * bz * BZ));
+  // Node rows (iy, iz) of a block, strided over the warps, without divisions.
+  auto for_rows = [&](int nby_, int nbz_, auto&& f) {
+    int iy = warp, iz = 0;
+    while (iy >= nby_) iy -= nby_, ++iz;
+    while (iz < nbz_) {
+      f(iy, iz);
+      iy += WARPS;
+      while (iy >= nby_) iy -= nby_, ++iz;
+    }
+  };
+  // Brick coordinates, advanced by the grid stride with carries.
+  struct BrickXYZ {
+    int x, y, z;
+  };
+  auto decompose = [&](int b) {
+    BrickXYZ c;
+    c.x = b % lay.nb[0];
+    c.y = (b / lay.nb[0]) % lay.nb[1];
+    c.z = b / (lay.nb[0] * lay.nb[1]);
+    return c;
+  };
+  const BrickXYZ step = decompose(gridDim.x);
+  auto advance = [&](BrickXYZ c) {
+    c.x += step.x;
+    c.y += step.y;
+    c.z += step.z;
+    if (c.x >= lay.nb[0]) c.x -= lay.nb[0], ++c.y;
+    if (c.y >= lay.nb[1]) c.y -= lay.nb[1], ++c.z;
+    return c;
+  };
+  auto issue_block = [&](BrickXYZ c, double* dst) {
+    const int nbx = P * min(BX, box.cells[0] - c.x * BX) + 1;
+    const int nby = P * min(BY, box.cells[1] - c.y * BY) + 1;
+    const int nbz = P * min(BZ, box.cells[2] - c.z * BZ) + 1;
+    const int node0 = P * c.x * BX + npx * (P * c.y * BY + npy * (P * c.z * BZ));
     if (warp < WARPS && lane < 3 * nbx) {
-      for (int row = warp; row < nby * nbz; row += WARPS) {
-        const int iz = row / nby, iy = row - iz * nby;
+      for_rows(nby, nbz, [&](int iy, int iz) {
         const double* src = prm.x + 3 * (node0 + npx * (iy + npy * iz)) + lane;
         const unsigned d = (unsigned)__cvta_generic_to_shared(
             dst + lc * D::NBP + (iz * D::NBYP + iy) * D::NBXP + lix);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-      }
+      });
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  if ((int)blockIdx.x < prm.nbricks) issue_block(prm.brick0 + blockIdx.x, Xs);
+  BrickXYZ bc = decompose(prm.brick0 + blockIdx.x);
+  if ((int)blockIdx.x < prm.nbricks) issue_block(bc, Xs);
   int cur = 0;
 #pragma unroll 1
   for (int bi = blockIdx.x; bi < prm.nbricks; bi += gridDim.x, cur ^= 1) {
   const int brick = prm.brick0 + bi;
   if (tid == 0 && bi + (int)gridDim.x < prm.nbricks) prefetch_state(brick + gridDim.x);
-  const int bx = brick % lay.nb[0], by = (brick / lay.nb[0]) % lay.nb[1],
-            bz = brick / (lay.nb[0] * lay.nb[1]);
+  const int bx = bc.x, by = bc.y, bz = bc.z;
+  const BrickXYZ bnext = advance(bc);
   const double* st_brick = prm.state + (size_t)lay.brick_points() * brick * kStateStride;
   const int ecx = min(BX, box.cells[0] - bx * BX);
   const int ecy = min(BY, box.cells[1] - by * BY);
@@ -239,6 +282,12 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
   const int node0 = P * bx * BX + npx * (P * by * BY + npy * (P * bz * BZ));
   const int gx0 = P * bx * BX, gy0 = P * by * BY, gz0 = P * bz * BZ;
   double* Xc = Xs + cur * (3 * D::NBP);
+  // Does the brick touch a constrained face (or is the mask general)?
+  const int fb = prm.face_bits;
+  const bool bmask =
+      fb < 0 || (fb > 0 && (((fb & 1) && gx0 == 0) || ((fb & 2) && gx0 + nbx == npx) ||
+                            ((fb & 4) && gy0 == 0) || ((fb & 8) && gy0 + nby == npy) ||
+                            ((fb & 16) && gz0 == 0) || ((fb & 32) && gz0 + nbz == box.npd[2])));
   // Constrained test: analytic whole-face sets (build_constraints,
   // operator.hpp:36-55) or the general mask array.
   auto fixed = [&](int dof, int gx, int gy, int gz) -> bool {
@@ -255,17 +304,17 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
   // General masks: zero constrained inputs (operator.hpp:189-193) in the
   // landed block.  Whole-face masks are applied analytically as P1 reads the
   // block, which keeps x intact for the constrained pass-through.
-  if (prm.face_bits < 0 && warp < WARPS && lane < 3 * nbx) {
-    for (int row = warp; row < nby * nbz; row += WARPS) {
-      const int iz = row / nby, iy = row - iz * nby;
+  if (fb < 0 && warp < WARPS && lane < 3 * nbx) {
+    for_rows(nby, nbz, [&](int iy, int iz) {
       const int dof = 3 * (node0 + npx * (iy + npy * iz)) + lane;
       if (fixed(dof, gx0 + lix, gy0 + iy, gz0 + iz))
         Xc[lc * D::NBP + (iz * D::NBYP + iy) * D::NBXP + lix] = 0.0;
-    }
+    });
   }
   // Next brick's block into the other buffer (free: its last readers, the
   // previous brick's P1 pass, are behind the barrier above).
-  if (bi + (int)gridDim.x < prm.nbricks) issue_block(brick + gridDim.x, Xs + (cur ^ 1) * (3 * D::NBP));
+  if (bi + (int)gridDim.x < prm.nbricks) issue_block(bnext, Xs + (cur ^ 1) * (3 * D::NBP));
+  bc = bnext;
   // Lanes are (column te = qy Q + qx, element le) with elements fastest, so
   // tid is also the state-layout index t (coalesced state loads).
   const int le = tid % D::NE, te = tid / D::NE;
@@ -294,8 +343,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
     for (int j = 0; j < N; ++j)
 #pragma unroll
       for (int i = 0; i < N; ++i) u[j][i] = Xp[j * D::NBXP + i];
-    if (prm.face_bits > 0) {
-      const int fb = prm.face_bits;
+    if (fb > 0 && bmask) {
       const int gx = gx0 + P * lx, gy = gy0 + P * ly, gz = gz0 + P * lz + k;
       const bool mz = ((fb & 16) && gz == 0) || ((fb & 32) && gz == box.npd[2] - 1);
 #pragma unroll
@@ -343,7 +391,18 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
   }
   __syncthreads(); HXG_PHASE(1);
   // P2: column owners (qx, qy): z pass for the three arrays.
-  double g[3][3][Q];
+  // Between the P1 and Q2 barriers the slab entries S[idx Q^2 + te] (idx <
+  // 9N) belong to this thread alone (its column).  For (p, q) = (1, 2),
+  // (1, 3), (2, 3) they hold the gradients and q-function outputs of the
+  // column's first N points (shared memory instead of registers: no spills at
+  // the two-CTA register cap), registers the remaining Q - N; elsewhere all Q
+  // stay in registers (no spills there, and fewer shared accesses).  The slots are volatile so the compiler
+  // does not forward them back into registers.
+  constexpr int NS = fused_slots(P, Q) ? N : 0;
+  constexpr int QR = Q - NS;
+  volatile double* slot = S + te;
+  double g[3][3][QR > 0 ? QR : 1];
+  auto gslot = [&](int c, int d, int z) { return ((c * 3 + d) * N + z) * Q2; };
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     double tb[N], tdx[N], tdy[N];
@@ -362,9 +421,15 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
         gy += prm.B[z * N + k] * tdy[k];
         gz += prm.Bd[z * N + k] * tb[k];
       }
-      g[c][0][z] = gx;
-      g[c][1][z] = gy;
-      g[c][2][z] = gz;
+      if (z < NS) {
+        slot[gslot(c, 0, z)] = gx;
+        slot[gslot(c, 1, z)] = gy;
+        slot[gslot(c, 2, z)] = gz;
+      } else {
+        g[c][0][z - NS] = gx;
+        g[c][1][z - NS] = gy;
+        g[c][2][z - NS] = gz;
+      }
     }
   }
 
@@ -389,7 +454,8 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) G[3 * c + d] = g[c][d][qz];
+        for (int d = 0; d < 3; ++d)
+          G[3 * c + d] = qz < NS ? slot[gslot(c, d, qz)] : g[c][d][qz - NS];
 #if HXG_EXPERIMENT == 2
       // timing experiment: trivial q-function (state still loaded)
 #pragma unroll
@@ -408,27 +474,39 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int d = 0; d < 3; ++d) g[c][d][qz] = H[3 * c + d];
+      for (int d = 0; d < 3; ++d) {
+        if (qz < NS)
+          slot[gslot(c, d, qz)] = H[3 * c + d];
+        else
+          g[c][d][qz - NS] = H[3 * c + d];
+      }
   }
-  __syncthreads(); HXG_PHASE(2);  // slabs free
+  HXG_PHASE(2);
 
   // ---- backward: exact adjoint of the forward passes ---------------------
-  // Q1: column owners: z adjoints R0 = Bd_z^T Hz, R1 = B_z^T Hx, R2 = B_z^T Hy.
+  // Q1: column owners: z adjoints R0 = Bd_z^T Hz, R1 = B_z^T Hx, R2 = B_z^T Hy
+  // (into this column's own slab entries: no barrier needed before it).
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
+  for (int c = 0; c < 3; ++c) {
+    double h[3][Q];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int z = 0; z < Q; ++z) h[d][z] = z < NS ? slot[gslot(c, d, z)] : g[c][d][z - NS];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       double r0 = 0.0, r1 = 0.0, r2 = 0.0;
 #pragma unroll
       for (int z = 0; z < Q; ++z) {
-        r0 += prm.Bd[z * N + k] * g[c][2][z];
-        r1 += prm.B[z * N + k] * g[c][0][z];
-        r2 += prm.B[z * N + k] * g[c][1][z];
+        r0 += prm.Bd[z * N + k] * h[2][z];
+        r1 += prm.B[z * N + k] * h[0][z];
+        r2 += prm.B[z * N + k] * h[1][z];
       }
-      S[((c * 3 + 0) * N + k) * Q2 + te] = r0;
-      S[((c * 3 + 1) * N + k) * Q2 + te] = r1;
-      S[((c * 3 + 2) * N + k) * Q2 + te] = r2;
+      slot[((c * 3 + 0) * N + k) * Q2] = r0;
+      slot[((c * 3 + 1) * N + k) * Q2] = r1;
+      slot[((c * 3 + 2) * N + k) * Q2] = r2;
     }
+  }
   __syncthreads(); HXG_PHASE(3);
   // Q2: plane tasks (c, k): y adjoints then x adjoints, in registers.
 #pragma unroll 1
@@ -496,9 +574,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
       const double v = e[0];
       return twox ? e[DX] + v : v;
     };
-#pragma unroll 1
-    for (int row = warp; row < nby * nbz; row += WARPS) {
-      const int iz = row / nby, iy = row - iz * nby;
+    for_rows(nby, nbz, [&](int iy, int iz) {
       const int lzh = iz / P < BZ ? iz / P : BZ - 1, k = iz - P * lzh;
       const int lyh = iy / P < BY ? iy / P : BY - 1, j = iy - P * lyh;
       const bool twoy = j == 0 && lyh > 0;
@@ -513,11 +589,11 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, HXG_FUSED_MINB)
         st_keep(part + (iz * NBY + iy) * ROW3 + lane, s, pol_keep);
       } else {
         const int dof = 3 * (node0 + npx * (iy + npy * iz)) + lane;
-        if (fixed(dof, gx0 + ix, gy0 + iy, gz0 + iz))  // pass x through (operator.hpp:212-214)
-          s = prm.face_bits >= 0 ? Xc[c * D::NBP + (iz * D::NBYP + iy) * D::NBXP + ix] : prm.x[dof];
+        if (bmask && fixed(dof, gx0 + ix, gy0 + iy, gz0 + iz))  // pass x through (operator.hpp:212-214)
+          s = fb >= 0 ? Xc[c * D::NBP + (iz * D::NBYP + iy) * D::NBXP + ix] : prm.x[dof];
         prm.y[dof] = s;
       }
-    }
+    });
   }
   // (the next iteration's first barrier orders these slab reads before the
   // slabs are rewritten)
