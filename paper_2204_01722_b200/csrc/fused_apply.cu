@@ -31,6 +31,12 @@
 #ifndef HXG_MINB_HIGHP
 #define HXG_MINB_HIGHP 3
 #endif
+#ifndef HXG_MINB_Q2
+#define HXG_MINB_Q2 2
+#endif
+#ifndef HXG_SLOTS_Q2
+#define HXG_SLOTS_Q2 1
+#endif
 #ifndef HXG_SLOTS_HIGHP
 #define HXG_SLOTS_HIGHP 0
 #endif
@@ -102,11 +108,11 @@ __host__ __device__ constexpr int pad_plane(int p, int q) {
 // Resident CTAs per SM the register allocation targets: two for the 9-warp
 // bricks; three for the 4-warp (3, 4) brick (shared memory allows it).
 __host__ __device__ constexpr int fused_min_blocks(int p, int q) {
-  return p * 10 + q == 34 ? HXG_MINB_HIGHP : 2;
+  return p * 10 + q == 34 ? HXG_MINB_HIGHP : p * 10 + q == 23 ? HXG_MINB_Q2 : 2;
 }
 // Column-private shared slots for the gradients (see P2).
 __host__ __device__ constexpr bool fused_slots(int p, int q) {
-  return p * 10 + q == 12 || p * 10 + q == 13 || p * 10 + q == 23 ||
+  return p * 10 + q == 12 || p * 10 + q == 13 || (HXG_SLOTS_Q2 && p * 10 + q == 23) ||
          (HXG_SLOTS_HIGHP && (p * 10 + q == 34 || p * 10 + q == 45));
 }
 

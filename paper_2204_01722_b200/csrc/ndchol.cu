@@ -8,10 +8,14 @@
 // region, all of which are ancestor pivots.  Numeric phase (device, per
 // setup): postorder over fronts, assemble original entries + children's
 // update matrices (extend-add, fixed order), potrf / trsm / syrk on the
-// dense front, keep the (np + ns) x np panel.  Solve (per V-cycle): forward
-// sweep leaves -> root passing update vectors up the tree, backward sweep
-// root -> leaves reading ancestor values; fronts of one tree level run in
-// one launch (one CTA per small front), large fronts use cuBLAS.
+// dense front, then keep the (np + ns) x np panel in inverse form
+// M = [L11^-1; L21 L11^-1] (two cuBLAS trsm).  Solve (per V-cycle): forward
+// sweep leaves -> root, z1 = L11^-1 y1 and u = y2 - L21 L11^-1 y1 in ONE
+// GEMV with M, update vectors passed up the tree; backward sweep root ->
+// leaves, x1 = M^T [z1; -x2] in one transposed GEMV.  Every front of a tree
+// level runs in the same launches: the GEMVs are cut into fixed tiles
+// (row block x column chunk) whose partial sums are reduced in a fixed
+// order, so the solve is bandwidth-bound and deterministic.
 #include "ndchol.hpp"
 
 #include <algorithm>
@@ -24,8 +28,6 @@ namespace hxg {
 namespace {
 
 constexpr int kLeafNodes = 128;
-constexpr int kSmallM = 2048;   // small fronts: one CTA, front vector in smem
-constexpr int kSolveThreads = 256;
 
 __global__ void assemble_kernel(const long long* __restrict__ dst, const int* __restrict__ src,
                                 long long n, const double* __restrict__ vals, double* front) {
@@ -58,133 +60,156 @@ __global__ void permute_scatter(const double* __restrict__ w, const int* __restr
     x[perm[i]] = w[i];
 }
 
-struct SolveArgs {
-  const int* fronts;  // front ids of this level
-  const int* piv0;
-  const int* np;
-  const int* ns;
-  const long long* loff;
-  const long long* rows_off;
-  const int* child0;
-  const int* child1;
-  const long long* map0;  // child-update map offsets
-  const long long* map1;
-  const int* maps;
-  const int* shell;
-  const long long* uoff;  // update-vector offsets
-  const double* L;
-  double* w;
-  double* ubuf;
+constexpr int kFR = 256;    // forward GEMV tile: rows (threads)
+constexpr int kFC = 1024;   //                    columns (y1 chunk in smem)
+constexpr int kBC = 64;     // backward GEMV tile: columns (8 warps x 8)
+constexpr int kBR = 2048;   //                     rows (v chunk in smem)
+
+struct NdSolve {
+  const int *piv0, *np, *ns, *child0, *child1, *ftile0, *btile0;
+  const long long *loff, *rows_off, *yoff, *uoff;
+  const int *src0, *src1, *shell;
+  const int *ftile_front, *btile_front, *rtile_front, *rtile_rb, *ctile_front, *ctile_cb;
+  const double* M;
+  double *w, *u, *y, *part_f, *part_b;
 };
 
-// y = [w(piv); 0] + extend(u_c0) + extend(u_c1)  (front vector, size m)
-__device__ void build_front_vector(const SolveArgs& a, int t, int np, int m, double* y) {
-  for (int k = threadIdx.x; k < m; k += blockDim.x) y[k] = k < np ? a.w[a.piv0[t] + k] : 0.0;
+__device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Forward front vector y = [w(piv); 0] + extend(u_child0) + extend(u_child1)
+// (the children's update rows gathered through the inverse extend maps).
+__global__ void __launch_bounds__(kFR) nd_fwd_assemble(NdSolve a, int rt0) {
+  const int rt = rt0 + blockIdx.x, t = a.rtile_front[rt];
+  const int np = a.np[t], m = np + a.ns[t];
+  const int r = a.rtile_rb[rt] * kFR + threadIdx.x;
+  if (r >= m) return;
+  const long long yo = a.yoff[t];
+  double v = r < np ? a.w[a.piv0[t] + r] : 0.0;
+  const int s0 = a.src0[yo + r], s1 = a.src1[yo + r];
+  if (s0 >= 0) v += a.u[a.uoff[a.child0[t]] + s0];
+  if (s1 >= 0) v += a.u[a.uoff[a.child1[t]] + s1];
+  a.y[yo + r] = v;
+}
+
+// Tile (row block rb, column chunk cc) of M y1: one row per thread.
+__global__ void __launch_bounds__(kFR) nd_fwd_gemv(NdSolve a, int ft0) {
+  __shared__ double ys[kFC];
+  const int tile = ft0 + blockIdx.x, t = a.ftile_front[tile];
+  const int np = a.np[t], m = np + a.ns[t];
+  const int ncc = ceil_div(np, kFC), local = tile - a.ftile0[t];
+  const int rb = local / ncc, cc = local - rb * ncc;
+  const int row0 = rb * kFR, col0 = cc * kFC, ncols = min(kFC, np - col0);
+  const int rend = min(row0 + kFR, m);
+  double* out = a.part_f + (size_t)tile * kFR;
+  if (rend <= np && rend - 1 < col0) {  // strictly above the diagonal of L11^-1: zeros
+    out[threadIdx.x] = 0.0;
+    return;
+  }
+  const long long yo = a.yoff[t];
+  for (int k = threadIdx.x; k < ncols; k += kFR) ys[k] = a.y[yo + col0 + k];
   __syncthreads();
-  const int ch[2] = {a.child0[t], a.child1[t]};
-  const long long mo[2] = {a.map0[t], a.map1[t]};
-  for (int q = 0; q < 2; ++q) {
-    const int c = ch[q];
-    if (c < 0) continue;
-    const int nsc = a.ns[c];
-    const double* u = a.ubuf + a.uoff[c];
-    const int* mp = a.maps + mo[q];
-    for (int k = threadIdx.x; k < nsc; k += blockDim.x) y[mp[k]] += u[k];
-    __syncthreads();
-  }
-}
-
-// Forward sweep on small fronts: one CTA per front, column-oriented
-// substitution through the whole (np + ns) x np panel.
-__global__ void __launch_bounds__(kSolveThreads) fwd_small_kernel(SolveArgs a) {
-  __shared__ double y[kSmallM];
-  __shared__ double zj;
-  const int t = a.fronts[blockIdx.x];
-  const int np = a.np[t], ns = a.ns[t], m = np + ns;
-  build_front_vector(a, t, np, m, y);
-  const double* L = a.L + a.loff[t];
-  for (int j = 0; j < np; ++j) {
-    if (threadIdx.x == 0) {
-      zj = y[j] / L[j + (long long)j * m];
-      y[j] = zj;
+  const int r = row0 + threadIdx.x;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (r < m) {
+    const double* col = a.M + a.loff[t] + (size_t)col0 * m + r;
+    int k = 0;
+    for (; k + 8 <= ncols; k += 8) {
+      double mv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) mv[q] = __ldg(col + (size_t)(k + q) * m);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q & 3] = fma(mv[q], ys[k + q], acc[q & 3]);
     }
-    __syncthreads();
-    const double z = zj;
-    const double* col = L + (long long)j * m;
-    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) y[i] -= col[i] * z;
-    __syncthreads();
+    for (; k < ncols; ++k) acc[k & 3] = fma(__ldg(col + (size_t)k * m), ys[k], acc[k & 3]);
   }
-  for (int k = threadIdx.x; k < m; k += blockDim.x) {
-    if (k < np)
-      a.w[a.piv0[t] + k] = y[k];
-    else
-      a.ubuf[a.uoff[t] + (k - np)] = y[k];
-  }
+  out[threadIdx.x] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
-// Backward sweep on small fronts: x_j = (x_j - sum_{i > j} L_ij x_i) / L_jj.
-__global__ void __launch_bounds__(kSolveThreads) bwd_small_kernel(SolveArgs a) {
-  __shared__ double x[kSmallM];
-  __shared__ double red[kSolveThreads / 32];
-  const int t = a.fronts[blockIdx.x];
-  const int np = a.np[t], ns = a.ns[t], m = np + ns;
-  const int* sh = a.shell + a.rows_off[t];
-  for (int k = threadIdx.x; k < m; k += blockDim.x)
-    x[k] = k < np ? a.w[a.piv0[t] + k] : a.w[sh[k - np]];
+// z1 = (M y1)_top -> w(piv);  u = y2 - (M y1)_bottom -> update vector.
+__global__ void __launch_bounds__(kFR) nd_fwd_finish(NdSolve a, int rt0) {
+  const int rt = rt0 + blockIdx.x, t = a.rtile_front[rt];
+  const int np = a.np[t], m = np + a.ns[t];
+  const int rb = a.rtile_rb[rt], r = rb * kFR + threadIdx.x;
+  if (r >= m) return;
+  const int ncc = ceil_div(np, kFC);
+  const double* p = a.part_f + ((size_t)a.ftile0[t] + (size_t)rb * ncc) * kFR + threadIdx.x;
+  double s = 0.0;
+  for (int cc = 0; cc < ncc; ++cc) s += p[(size_t)cc * kFR];
+  if (r < np)
+    a.w[a.piv0[t] + r] = s;
+  else
+    a.u[a.uoff[t] + (r - np)] = a.y[a.yoff[t] + r] - s;
+}
+
+// Backward front vector v = [z1; -x2] (x2 = ancestor solution values).
+__global__ void __launch_bounds__(kFR) nd_bwd_assemble(NdSolve a, int rt0) {
+  const int rt = rt0 + blockIdx.x, t = a.rtile_front[rt];
+  const int np = a.np[t], m = np + a.ns[t];
+  const int r = a.rtile_rb[rt] * kFR + threadIdx.x;
+  if (r >= m) return;
+  a.y[a.yoff[t] + r] = r < np ? a.w[a.piv0[t] + r] : -a.w[a.shell[a.rows_off[t] + (r - np)]];
+}
+
+// Tile (column block cb, row chunk rc) of M^T v: 8 warps x 8 columns, lanes
+// stride the (contiguous) column, fixed-order warp reduction.
+__global__ void __launch_bounds__(256) nd_bwd_gemv(NdSolve a, int bt0) {
+  __shared__ double vs[kBR];
+  const int tile = bt0 + blockIdx.x, t = a.btile_front[tile];
+  const int np = a.np[t], m = np + a.ns[t];
+  const int nrc = ceil_div(m, kBR), local = tile - a.btile0[t];
+  const int cb = local / nrc, rc = local - cb * nrc;
+  const int col0 = cb * kBC, row0 = rc * kBR, nrows = min(kBR, m - row0);
+  double* out = a.part_b + (size_t)tile * kBC;
+  if (row0 + nrows <= col0) {  // rows above the diagonal block of every column: zeros
+    if (threadIdx.x < kBC) out[threadIdx.x] = 0.0;
+    return;
+  }
+  const long long yo = a.yoff[t];
+  for (int k = threadIdx.x; k < nrows; k += 256) vs[k] = a.y[yo + row0 + k];
   __syncthreads();
-  const double* L = a.L + a.loff[t];
-  for (int j = np - 1; j >= 0; --j) {
-    const double* col = L + (long long)j * m;
-    double s = 0.0;
-    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) s += col[i] * x[i];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double tot = 0.0;
-      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += red[q];
-      x[j] = (x[j] - tot) / col[j];
-    }
-    __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* base = a.M + a.loff[t] + row0;
+  double acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  const int j0 = col0 + warp * 8;
+  for (int k = lane; k < nrows; k += 32) {
+    const double vk = vs[k];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (j0 + q < np) acc[q] = fma(__ldg(base + (size_t)(j0 + q) * m + k), vk, acc[q]);
   }
-  for (int k = threadIdx.x; k < np; k += blockDim.x) a.w[a.piv0[t] + k] = x[k];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+  }
+  if (lane < 8) {
+    double v = acc[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) v = lane == q ? acc[q] : v;
+    out[warp * 8 + lane] = v;
+  }
 }
 
-// Large fronts: the front vector lives in global scratch (ybuf), cuBLAS does
-// the dense triangular solve and the panel product.
-__global__ void big_build_kernel(SolveArgs a, int t, double* ybuf) {
-  const int np = a.np[t], ns = a.ns[t], m = np + ns;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x)
-    ybuf[k] = k < np ? a.w[a.piv0[t] + k] : 0.0;
+// x1 = sum over row chunks -> w(piv).
+__global__ void __launch_bounds__(kBC) nd_bwd_finish(NdSolve a, int ct0) {
+  const int ct = ct0 + blockIdx.x, t = a.ctile_front[ct];
+  const int np = a.np[t], m = np + a.ns[t];
+  const int cb = a.ctile_cb[ct], j = cb * kBC + threadIdx.x;
+  if (j >= np) return;
+  const int nrc = ceil_div(m, kBR);
+  const double* p = a.part_b + ((size_t)a.btile0[t] + (size_t)cb * nrc) * kBC + threadIdx.x;
+  double s = 0.0;
+  for (int rc = 0; rc < nrc; ++rc) s += p[(size_t)rc * kBC];
+  a.w[a.piv0[t] + j] = s;
 }
-__global__ void big_extend_kernel(SolveArgs a, int t, int q, double* ybuf) {
-  const int c = q == 0 ? a.child0[t] : a.child1[t];
-  if (c < 0) return;
-  const int nsc = a.ns[c];
-  const double* u = a.ubuf + a.uoff[c];
-  const int* mp = a.maps + (q == 0 ? a.map0[t] : a.map1[t]);
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nsc; k += gridDim.x * blockDim.x)
-    ybuf[mp[k]] += u[k];
-}
-__global__ void big_fwd_store_kernel(SolveArgs a, int t, const double* ybuf) {
-  const int np = a.np[t], ns = a.ns[t], m = np + ns;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
-    if (k < np)
-      a.w[a.piv0[t] + k] = ybuf[k];
-    else
-      a.ubuf[a.uoff[t] + (k - np)] = ybuf[k];
-  }
-}
-__global__ void big_bwd_load_kernel(SolveArgs a, int t, double* ybuf) {
-  const int np = a.np[t], ns = a.ns[t], m = np + ns;
-  const int* sh = a.shell + a.rows_off[t];
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x)
-    ybuf[k] = k < np ? a.w[a.piv0[t] + k] : a.w[sh[k - np]];
-}
-__global__ void big_bwd_store_kernel(SolveArgs a, int t, const double* ybuf) {
-  const int np = a.np[t];
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < np; k += gridDim.x * blockDim.x)
-    a.w[a.piv0[t] + k] = ybuf[k];
+
+__global__ void identity_kernel(double* a, int n) {
+  const long long total = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x)
+    a[e] = (e % (n + 1)) == 0 ? 1.0 : 0.0;
 }
 
 void cublas_check(cublasStatus_t s, const char* what) {
@@ -357,38 +382,38 @@ void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
   }
   asm_begin_[(size_t)nf] = adst.size();
 
-  // Levels for the batched solves: small fronts (one CTA each) and large
-  // fronts (cuBLAS) per tree depth.
+  // Levels for the batched solves and their GEMV tile lists.
   int maxlev = 0;
   for (const auto& f : fronts_) maxlev = std::max(maxlev, f.level);
   levels_.assign((size_t)maxlev + 1, {});
   for (int t = 0; t < nf; ++t) levels_[(size_t)fronts_[(size_t)t].level].push_back(t);
-  std::vector<int> sl;
-  small_off_.assign(levels_.size() + 1, 0);
-  big_.assign(levels_.size(), {});
+  auto cdiv = [](long long x, long long y) { return (int)((x + y - 1) / y); };
+  std::vector<int> piv0(nf), np(nf), ns(nf), c0(nf), c1(nf), ft0(nf), bt0(nf);
+  std::vector<long long> loff(nf), roff(nf), yoff(nf), uoff(nf);
+  std::vector<int> ftf, btf, rtf, rtb, ctf, ctb;
+  lev_ft_.assign(levels_.size() + 1, 0);
+  lev_bt_ = lev_rt_ = lev_ct_ = lev_ft_;
+  long long ucount = 0, ycount = 0;
   for (size_t l = 0; l < levels_.size(); ++l) {
-    small_off_[l] = sl.size();
+    lev_ft_[l] = (int)ftf.size();
+    lev_bt_[l] = (int)btf.size();
+    lev_rt_[l] = (int)rtf.size();
+    lev_ct_[l] = (int)ctf.size();
     for (int t : levels_[l]) {
       const Front& f = fronts_[(size_t)t];
-      if (f.np + f.ns <= kSmallM)
-        sl.push_back(t);
-      else
-        big_[l].push_back(t);
+      const int m = f.np + f.ns;
+      ft0[t] = (int)ftf.size();
+      for (int k = 0, n = cdiv(m, kFR) * cdiv(f.np, kFC); k < n; ++k) ftf.push_back(t);
+      bt0[t] = (int)btf.size();
+      for (int k = 0, n = cdiv(f.np, kBC) * cdiv(m, kBR); k < n; ++k) btf.push_back(t);
+      for (int rb = 0; rb < cdiv(m, kFR); ++rb) rtf.push_back(t), rtb.push_back(rb);
+      for (int cb = 0; cb < cdiv(f.np, kBC); ++cb) ctf.push_back(t), ctb.push_back(cb);
     }
   }
-  small_off_[levels_.size()] = sl.size();
-
-  // Device copies.
-  perm_.upload(perm);
-  shell_rows_.upload(shell_rows.empty() ? std::vector<int>{0} : shell_rows);
-  child_map_.upload(maps.empty() ? std::vector<int>{0} : maps);
-  asm_dst_.upload(adst);
-  asm_src_.upload(asrc);
-  small_lists_.upload(sl.empty() ? std::vector<int>{0} : sl);
-  (void)afront;
-  std::vector<int> piv0(nf), np(nf), ns(nf), c0(nf), c1(nf);
-  std::vector<long long> loff(nf), roff(nf), m0(nf), m1(nf), uoff(nf);
-  long long ucount = 0;
+  lev_ft_[levels_.size()] = (int)ftf.size();
+  lev_bt_[levels_.size()] = (int)btf.size();
+  lev_rt_[levels_.size()] = (int)rtf.size();
+  lev_ct_[levels_.size()] = (int)ctf.size();
   for (int t = 0; t < nf; ++t) {
     const Front& f = fronts_[(size_t)t];
     piv0[t] = f.piv0;
@@ -398,29 +423,64 @@ void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
     c1[t] = f.child[1];
     loff[t] = (long long)f.loff;
     roff[t] = (long long)f.rows_off;
-    m0[t] = (long long)f.map_off[0];
-    m1[t] = (long long)f.map_off[1];
     uoff[t] = ucount;
     ucount += f.ns;
+    yoff[t] = ycount;
+    ycount += f.np + f.ns;
   }
-  dfront_piv0_.upload(piv0);
-  dfront_np_.upload(np);
-  dfront_ns_.upload(ns);
+  // Inverse extend maps: front position -> index in child q's update vector.
+  std::vector<int> src0((size_t)ycount, -1), src1((size_t)ycount, -1);
+  for (int t = 0; t < nf; ++t) {
+    const Front& f = fronts_[(size_t)t];
+    for (int q = 0; q < 2; ++q) {
+      const int c = f.child[q];
+      if (c < 0) continue;
+      auto& src = q == 0 ? src0 : src1;
+      const int nsc = fronts_[(size_t)c].ns;
+      for (int k = 0; k < nsc; ++k) src[(size_t)yoff[t] + maps[f.map_off[q] + (size_t)k]] = k;
+    }
+  }
+
+  // Device copies.
+  auto up = [](DevBuf<int>& d, const std::vector<int>& v) {
+    d.upload(v.empty() ? std::vector<int>{0} : v);
+  };
+  perm_.upload(perm);
+  up(shell_rows_, shell_rows);
+  up(child_map_, maps);
+  asm_dst_.upload(adst);
+  asm_src_.upload(asrc);
+  (void)afront;
+  up(dfront_piv0_, piv0);
+  up(dfront_np_, np);
+  up(dfront_ns_, ns);
+  up(c0_, c0);
+  up(c1_, c1);
+  up(ftile0_, ft0);
+  up(btile0_, bt0);
   dfront_loff_.upload(loff);
   dfront_rows_off_.upload(roff);
-  c0_.upload(c0);
-  c1_.upload(c1);
-  map0_.upload(m0);
-  map1_.upload(m1);
+  yoff_.upload(yoff);
   uoff_.upload(uoff);
+  up(src0_, src0);
+  up(src1_, src1);
+  up(ftile_front_, ftf);
+  up(btile_front_, btf);
+  up(rtile_front_, rtf);
+  up(rtile_rb_, rtb);
+  up(ctile_front_, ctf);
+  up(ctile_cb_, ctb);
   ubuf_.alloc((size_t)std::max<long long>(ucount, 1));
+  yvec_.alloc((size_t)std::max<long long>(ycount, 1));
+  part_f_.alloc(std::max<size_t>(ftf.size(), 1) * kFR);
+  part_b_.alloc(std::max<size_t>(btf.size(), 1) * kBC);
   L_.alloc(lsize_);
   work_.alloc(max_front_);
+  size_t maxnp = 1;
+  for (const auto& f : fronts_) maxnp = std::max(maxnp, (size_t)f.np);
+  inv_.alloc(maxnp * maxnp);
   stack_.alloc(std::max<size_t>(max_update_, 1));
   wvec_.alloc((size_t)n_);
-  size_t maxm = 0;
-  for (const auto& f : fronts_) maxm = std::max(maxm, (size_t)(f.np + f.ns));
-  ybuf_.alloc(maxm);
   info_.alloc((size_t)nf);
   analyzed_ = true;
 }
@@ -480,6 +540,19 @@ void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s)
                                &minus_one, W + f.np, m, &one, W + f.np + (size_t)f.np * m, m),
                    "syrk");
     }
+    // Inverse form of the panel: M_bot = L21 L11^-1 (in place, after syrk has
+    // consumed L21), M_top = L11^-1 (trsm against the identity: exact zeros
+    // above the diagonal).
+    if (f.ns > 0)
+      cublas_check(cublasDtrsm(cublas_, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
+                               CUBLAS_DIAG_NON_UNIT, f.ns, f.np, &one, W, m, W + f.np, m),
+                   "trsm (inverse panel)");
+    identity_kernel<<<grid_for((long long)f.np * f.np, 256), 256, 0, s>>>(inv_.p, f.np);
+    cublas_check(cublasDtrsm(cublas_, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
+                             CUBLAS_DIAG_NON_UNIT, f.np, f.np, &one, W, m, inv_.p, f.np),
+                 "trsm (L11 inverse)");
+    HXG_CUDA(cudaMemcpy2DAsync(W, sizeof(double) * m, inv_.p, sizeof(double) * f.np,
+                               sizeof(double) * f.np, f.np, cudaMemcpyDeviceToDevice, s));
     HXG_CUDA(cudaMemcpyAsync(L_.p + f.loff, W, sizeof(double) * (size_t)m * f.np,
                              cudaMemcpyDeviceToDevice, s));
     if (f.ns > 0) {
@@ -503,72 +576,52 @@ void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s)
 
 void NdCholesky::solve(const double* b, double* x, cudaStream_t s) {
   if (!ready_) throw Error(HXG_ERR_GENERIC, "coarse solver not factorized");
-  cublasSetStream(cublas_, s);
-  SolveArgs a;
+  NdSolve a;
   a.piv0 = dfront_piv0_.p;
   a.np = dfront_np_.p;
   a.ns = dfront_ns_.p;
-  a.loff = dfront_loff_.p;
-  a.rows_off = dfront_rows_off_.p;
   a.child0 = c0_.p;
   a.child1 = c1_.p;
-  a.map0 = map0_.p;
-  a.map1 = map1_.p;
-  a.maps = child_map_.p;
-  a.shell = shell_rows_.p;
+  a.ftile0 = ftile0_.p;
+  a.btile0 = btile0_.p;
+  a.loff = dfront_loff_.p;
+  a.rows_off = dfront_rows_off_.p;
+  a.yoff = yoff_.p;
   a.uoff = uoff_.p;
-  a.L = L_.p;
+  a.src0 = src0_.p;
+  a.src1 = src1_.p;
+  a.shell = shell_rows_.p;
+  a.ftile_front = ftile_front_.p;
+  a.btile_front = btile_front_.p;
+  a.rtile_front = rtile_front_.p;
+  a.rtile_rb = rtile_rb_.p;
+  a.ctile_front = ctile_front_.p;
+  a.ctile_cb = ctile_cb_.p;
+  a.M = L_.p;
   a.w = wvec_.p;
-  a.ubuf = ubuf_.p;
+  a.u = ubuf_.p;
+  a.y = yvec_.p;
+  a.part_f = part_f_.p;
+  a.part_b = part_b_.p;
   permute_gather<<<grid_for(n_, 256), 256, 0, s>>>(b, perm_.p, n_, wvec_.p);
-  const double one = 1.0, minus_one = -1.0;
   // Forward: deepest level first.
   for (int l = (int)levels_.size() - 1; l >= 0; --l) {
-    const size_t ns0 = small_off_[(size_t)l], ns1 = small_off_[(size_t)l + 1];
-    if (ns1 > ns0) {
-      a.fronts = small_lists_.p + ns0;
-      fwd_small_kernel<<<(unsigned)(ns1 - ns0), kSolveThreads, 0, s>>>(a);
-    }
-    for (int t : big_[(size_t)l]) {
-      const Front& f = fronts_[(size_t)t];
-      const int m = f.np + f.ns;
-      big_build_kernel<<<grid_for(m, 256), 256, 0, s>>>(a, t, ybuf_.p);
-      big_extend_kernel<<<grid_for(f.ns > 0 ? m : 1, 256), 256, 0, s>>>(a, t, 0, ybuf_.p);
-      big_extend_kernel<<<grid_for(f.ns > 0 ? m : 1, 256), 256, 0, s>>>(a, t, 1, ybuf_.p);
-      const double* L = L_.p + f.loff;
-      cublas_check(cublasDtrsv(cublas_, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
-                               f.np, L, m, ybuf_.p, 1),
-                   "trsv");
-      if (f.ns > 0)
-        cublas_check(cublasDgemv(cublas_, CUBLAS_OP_N, f.ns, f.np, &minus_one, L + f.np, m,
-                                 ybuf_.p, 1, &one, ybuf_.p + f.np, 1),
-                     "gemv");
-      big_fwd_store_kernel<<<grid_for(m, 256), 256, 0, s>>>(a, t, ybuf_.p);
-    }
-    HXG_CUDA(cudaGetLastError());
+    const int nrt = lev_rt_[(size_t)l + 1] - lev_rt_[(size_t)l];
+    const int nft = lev_ft_[(size_t)l + 1] - lev_ft_[(size_t)l];
+    if (!nrt) continue;
+    nd_fwd_assemble<<<nrt, kFR, 0, s>>>(a, lev_rt_[(size_t)l]);
+    nd_fwd_gemv<<<nft, kFR, 0, s>>>(a, lev_ft_[(size_t)l]);
+    nd_fwd_finish<<<nrt, kFR, 0, s>>>(a, lev_rt_[(size_t)l]);
   }
   // Backward: root first.
   for (size_t l = 0; l < levels_.size(); ++l) {
-    for (int t : big_[l]) {
-      const Front& f = fronts_[(size_t)t];
-      const int m = f.np + f.ns;
-      big_bwd_load_kernel<<<grid_for(m, 256), 256, 0, s>>>(a, t, ybuf_.p);
-      const double* L = L_.p + f.loff;
-      if (f.ns > 0)
-        cublas_check(cublasDgemv(cublas_, CUBLAS_OP_T, f.ns, f.np, &minus_one, L + f.np, m,
-                                 ybuf_.p + f.np, 1, &one, ybuf_.p, 1),
-                     "gemv^T");
-      cublas_check(cublasDtrsv(cublas_, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
-                               f.np, L, m, ybuf_.p, 1),
-                   "trsv^T");
-      big_bwd_store_kernel<<<grid_for(f.np, 256), 256, 0, s>>>(a, t, ybuf_.p);
-    }
-    const size_t ns0 = small_off_[l], ns1 = small_off_[l + 1];
-    if (ns1 > ns0) {
-      a.fronts = small_lists_.p + ns0;
-      bwd_small_kernel<<<(unsigned)(ns1 - ns0), kSolveThreads, 0, s>>>(a);
-    }
-    HXG_CUDA(cudaGetLastError());
+    const int nrt = lev_rt_[l + 1] - lev_rt_[l];
+    const int nbt = lev_bt_[l + 1] - lev_bt_[l];
+    const int nct = lev_ct_[l + 1] - lev_ct_[l];
+    if (!nrt) continue;
+    nd_bwd_assemble<<<nrt, kFR, 0, s>>>(a, lev_rt_[l]);
+    nd_bwd_gemv<<<nbt, 256, 0, s>>>(a, lev_bt_[l]);
+    nd_bwd_finish<<<nct, kBC, 0, s>>>(a, lev_ct_[l]);
   }
   permute_scatter<<<grid_for(n_, 256), 256, 0, s>>>(wvec_.p, perm_.p, n_, x);
   HXG_CUDA(cudaGetLastError());

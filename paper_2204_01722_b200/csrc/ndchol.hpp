@@ -1,8 +1,10 @@
 // On-device sparse Cholesky of the assembled p = 1 coarse operator
 // (CholeskyCoarseSolver, coarse_solver.hpp:16-47, which uses Eigen's
 // SimplicialLLT): geometric nested dissection of the Q1 node lattice and a
-// multifrontal LL^T with dense fronts factored by cuSOLVER/cuBLAS FP64; the
-// per-V-cycle triangular solves run level by level over the dissection tree.
+// multifrontal LL^T with dense fronts factored by cuSOLVER/cuBLAS FP64.  Each
+// front keeps its panel in inverse form M = [L11^-1; L21 L11^-1], so the
+// per-V-cycle triangular solves are one bandwidth-bound GEMV per front and
+// direction, batched over every front of a dissection-tree level.
 #pragma once
 
 #include <cublas_v2.h>
@@ -29,6 +31,7 @@ class NdCholesky {
   void solve(const double* b, double* x, cudaStream_t s);
   bool ready() const { return ready_; }
   double factor_bytes() const { return (double)lsize_ * sizeof(double); }
+  int num_levels() const { return (int)levels_.size(); }
 
  private:
   struct Front {
@@ -58,17 +61,21 @@ class NdCholesky {
   DevBuf<int> asm_src_;      // assembly: CSR slot
   DevBuf<double> L_;         // factor panels
   DevBuf<double> work_;      // current front (m x m)
+  DevBuf<double> inv_;       // L11^-1 scratch (np x np)
   DevBuf<double> stack_;     // pending update matrices
   DevBuf<double> wvec_;      // solve work vector (new numbering)
   DevBuf<double> ubuf_;      // per-front update vectors (forward sweep)
-  DevBuf<double> ybuf_;      // large-front vector
+  DevBuf<double> yvec_;      // per-front front vectors
+  DevBuf<double> part_f_, part_b_;  // GEMV tile partial sums
   DevBuf<int> info_;
   DevBuf<double> potrf_ws_;
-  DevBuf<int> dfront_piv0_, dfront_np_, dfront_ns_, c0_, c1_;
-  DevBuf<long long> dfront_loff_, dfront_rows_off_, map0_, map1_, uoff_;
-  DevBuf<int> small_lists_;               // small fronts, grouped by level
-  std::vector<size_t> small_off_;         // per level offsets into small_lists_
-  std::vector<std::vector<int>> big_;     // large fronts per level
+  // Per-front solve metadata and the tile lists (see ndchol.cu).
+  DevBuf<int> dfront_piv0_, dfront_np_, dfront_ns_, c0_, c1_, ftile0_, btile0_;
+  DevBuf<long long> dfront_loff_, dfront_rows_off_, yoff_, uoff_;
+  DevBuf<int> src0_, src1_;  // front position -> child update index (or -1)
+  DevBuf<int> ftile_front_, btile_front_, rtile_front_, rtile_rb_, ctile_front_, ctile_cb_;
+  // Per level: [begin, end) into the forward / backward / row / column tile lists.
+  std::vector<int> lev_ft_, lev_bt_, lev_rt_, lev_ct_;
   std::vector<size_t> asm_begin_;  // per front range in the assembly lists
   cublasHandle_t cublas_ = nullptr;
   cusolverDnHandle_t cusolver_ = nullptr;

@@ -1,12 +1,60 @@
 #include "solver.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
 #include <random>
 
 namespace hxg {
 
 namespace {
+
+// Krylov work vectors and the dot workspace (pinned result slots), kept
+// across calls: cudaMalloc / cudaMallocHost / cudaFree per solve would
+// synchronise the device and cost more than a V-cycle.  One set per vector
+// length; handles are not reentrant (like the reference's operators), so a
+// process-wide pool is enough.
+struct KrylovWork {
+  DevBuf<double> v[5];
+  DotWorkspace ws;
+  explicit KrylovWork(size_t n) {
+    for (auto& b : v) b.alloc(n);
+  }
+};
+KrylovWork& krylov_work(size_t n) {
+  static std::mutex mu;
+  static std::vector<std::pair<size_t, KrylovWork*>>* pool =
+      new std::vector<std::pair<size_t, KrylovWork*>>();  // leaked: outlives the CUDA context
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& e : *pool)
+    if (e.first == n) return *e.second;
+  pool->emplace_back(n, new KrylovWork(n));
+  return *pool->back().second;
+}
+
+// HXG_PROFILE=1: print the phases of setup_numeric (device-synchronised).
+struct PhaseTimer {
+  bool on;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTimer(cudaStream_t st) : on(std::getenv("HXG_PROFILE") != nullptr), s(st) {
+    if (on) {
+      cudaStreamSynchronize(s);
+      t = std::chrono::steady_clock::now();
+    }
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hxg] %-28s %9.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 int sturm_count(const std::vector<double>& d, const std::vector<double>& e, double x) {
   int count = 0;
@@ -73,8 +121,9 @@ std::vector<double> rough_seed(long long n, const std::vector<uint8_t>& mask) {
 
 CgResult cg_solve(long long n, const DevOp& a, const DevOp& m, const double* b, double* x,
                   double rtol, int max_iterations, cudaStream_t s) {
-  DevBuf<double> r((size_t)n), z((size_t)n), p((size_t)n), ap((size_t)n);
-  DotWorkspace ws;
+  KrylovWork& w = krylov_work((size_t)n);
+  DevBuf<double>&r = w.v[0], &z = w.v[1], &p = w.v[2], &ap = w.v[3];
+  DotWorkspace& ws = w.ws;
   a(x, r.p);
   vsub_from(r.p, b, n, s);
   m(r.p, z.p);
@@ -124,8 +173,9 @@ CgResult cg_solve(long long n, const DevOp& a, const DevOp& m, const double* b, 
 
 double estimate_lambda_max(long long n, const DevOp& a, const double* inv_diag,
                            const double* seed, int iterations, cudaStream_t s) {
-  DevBuf<double> x((size_t)n), r((size_t)n), z((size_t)n), p((size_t)n), ap((size_t)n);
-  DotWorkspace ws;
+  KrylovWork& w = krylov_work((size_t)n);
+  DevBuf<double>&x = w.v[0], &r = w.v[1], &z = w.v[2], &p = w.v[3], &ap = w.v[4];
+  DotWorkspace& ws = w.ws;
   vzero(x.p, n, s);
   vcopy(r.p, seed, n, s);
   vscale_mul(z.p, inv_diag, r.p, n, s);
@@ -159,20 +209,19 @@ void Chebyshev::create(Operator& op, int degree_) {
   degree = degree_;
   long long n = op.size();
   cudaStream_t s = op.stream();
-  DevBuf<double> diag((size_t)n);
-  op.extract_diagonal(diag.p);
-  inv_diag.alloc((size_t)n);
-  if (!vreciprocal(inv_diag.p, diag.p, n, s))
+  if (inv_diag.n != (size_t)n) {  // first setup: buffers and the (constant) seed
+    inv_diag.alloc((size_t)n);
+    r.alloc((size_t)n);
+    d.alloc((size_t)n);
+    seed.upload(rough_seed(n, op.mask_host()));
+  }
+  op.extract_diagonal(d.p);  // d doubles as the diagonal scratch here
+  if (!vreciprocal(inv_diag.p, d.p, n, s))
     throw Error(HXG_ERR_INVALID_SMOOTHER, "invalid smoother: zero diagonal entry");
-  auto seed_h = rough_seed(n, op.mask_host());
-  DevBuf<double> seed;
-  seed.upload(seed_h);
   lambda_max = estimate_lambda_max(
       n, [&op](const double* x, double* y) { op.apply_jacobian(x, y); }, inv_diag.p, seed.p, 10, s);
   lo = 0.1 * lambda_max;
   hi = 1.1 * lambda_max;
-  r.alloc((size_t)n);
-  d.alloc((size_t)n);
   ready = true;
 }
 
@@ -243,11 +292,17 @@ Hierarchy::Hierarchy(Operator* fine, int fixed_face_mask, std::vector<int> sched
 }
 
 void Hierarchy::setup_numeric() {
-  for (int k = 1; k < num_levels(); ++k) level(k).smoother.create(*level(k).op, degree_);
+  PhaseTimer pt(stream());
+  for (int k = 1; k < num_levels(); ++k) {
+    level(k).smoother.create(*level(k).op, degree_);
+    pt.mark("smoother (diag + lambda_max)");
+  }
   if (!assembly_) assembly_ = std::make_unique<CoarseAssembly>(*level(0).op);
   assembly_->numeric(*level(0).op);
+  pt.mark("coarse assembly");
   coarse_.set_mode(coarse_mode_);
   coarse_.factorize(assembly_->matrix(), level(0).op->box().npd, stream());
+  pt.mark("coarse factorization");
 }
 
 void Hierarchy::prolong(int coarse_level, const double* xc, double* xf) {

@@ -43,6 +43,7 @@ struct Chebyshev {
   int degree = 2;
   double lambda_max = 0.0, lo = 0.0, hi = 0.0;
   DevBuf<double> inv_diag, r, d;
+  DevBuf<double> seed;  // rough_seed (cg.hpp:138-147), fixed per level
   bool ready = false;
   void create(Operator& op, int degree_);
   // One sweep; x_zero = x is known to be exactly zero (A x = 0 is skipped,

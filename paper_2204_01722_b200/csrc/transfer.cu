@@ -16,23 +16,13 @@ struct TransferParams {
   const double* ctof;  // Nf x Nc
   const double* in;    // L-vector (coarse for prolong, fine for restrict)
   double* evec;        // output E-vector (fine for prolong, coarse for restrict)
+  double C[5 * 4];     // ctof by value (uniform operands)
 };
 
 __device__ __forceinline__ long long lattice_node(const BoxDev& b, long long e, int i, int j, int k) {
   long long ex = e % b.cells[0], ey = (e / b.cells[0]) % b.cells[1],
             ez = e / ((long long)b.cells[0] * b.cells[1]);
   return (b.p * ex + i) + b.npd[0] * ((b.p * ey + j) + (long long)b.npd[1] * (b.p * ez + k));
-}
-
-// Multiplicity of a lattice node (build_restriction, mesh.hpp:136-137).
-__device__ __forceinline__ int multiplicity(const BoxDev& b, long long node) {
-  int g[3] = {(int)(node % b.npd[0]), (int)((node / b.npd[0]) % b.npd[1]),
-              (int)(node / ((long long)b.npd[0] * b.npd[1]))};
-  int m = 1;
-#pragma unroll
-  for (int d = 0; d < 3; ++d)
-    if (g[d] % b.p == 0 && g[d] > 0 && g[d] < b.npd[d] - 1) m *= 2;
-  return m;
 }
 
 // Prolong: out[e][c][k][j][i] = sum_kc C[k][kc] sum_jc C[j][jc] sum_ic C[i][ic] xc[..]
@@ -73,35 +63,62 @@ __global__ void prolong_element_kernel(TransferParams prm) {
 
 // Restrict (exact transpose, contraction order z, y, x as apply_transpose):
 // out[e][c][kc][jc][ic] = sum_if C[if][ic] sum_jf C[jf][jc] sum_kf C[kf][kc] s[..]
-// with s = x_f / m_f gathered on the fine lattice.
+// with s = x_f / m_f gathered on the fine lattice.  One thread per
+// (coarse element, component, kc) evaluates its NC^2 outputs with the
+// z-sums t1 and y-sums t2 shared between them: every output is the same
+// operation sequence as the per-entry formula (bitwise identical), with the
+// NF^3 gathers and the lattice arithmetic done once.  1/m_f is the product
+// of per-direction factors 1 or 1/2 (exact).
 template <int NF, int NC>
-__global__ void restrict_element_kernel(TransferParams prm) {
-  constexpr int NC3 = NC * NC * NC;
-  long long total = prm.coarse.num_elements() * 3 * NC3;
+__global__ void __launch_bounds__(128) restrict_element_kernel(TransferParams prm) {
+  constexpr int NC3 = NC * NC * NC, PF = NF - 1;
+  const BoxDev& f = prm.fine;
+  const long long total = prm.coarse.num_elements() * 3 * NC;
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < total;
        r += (long long)gridDim.x * blockDim.x) {
-    long long e = r / (3 * NC3);
-    int rem = (int)(r % (3 * NC3));
-    int c = rem / NC3, a = rem % NC3;
-    int ic = a % NC, jc = (a / NC) % NC, kc = a / (NC * NC);
-    double out = 0.0;
+    const long long e = r / (3 * NC);
+    const int rem = (int)(r - e * 3 * NC), c = rem / NC, kc = rem - c * NC;
+    const int ex = (int)(e % f.cells[0]), ey = (int)((e / f.cells[0]) % f.cells[1]),
+              ez = (int)(e / ((long long)f.cells[0] * f.cells[1]));
+    const double* base =
+        prm.in + 3 * ((PF * ex) + f.npd[0] * ((long long)(PF * ey) + (long long)f.npd[1] * (PF * ez))) + c;
+    const long long sy = 3LL * f.npd[0], sz = 3LL * f.npd[0] * f.npd[1];
+    auto half = [](int i, int ecell, int ncell) {
+      return (i == 0 && ecell > 0) || (i == PF && ecell < ncell - 1) ? 0.5 : 1.0;
+    };
+    double out[NC][NC];
+#pragma unroll
+    for (int jc = 0; jc < NC; ++jc)
+#pragma unroll
+      for (int ic = 0; ic < NC; ++ic) out[jc][ic] = 0.0;
 #pragma unroll
     for (int iff = 0; iff < NF; ++iff) {
-      double t2 = 0.0;
+      const double hx = half(iff, ex, f.cells[0]);
+      double t2[NC];
+#pragma unroll
+      for (int jc = 0; jc < NC; ++jc) t2[jc] = 0.0;
 #pragma unroll
       for (int jf = 0; jf < NF; ++jf) {
+        const double hxy = hx * half(jf, ey, f.cells[1]);
         double t1 = 0.0;
 #pragma unroll
         for (int kf = 0; kf < NF; ++kf) {
-          long long node = lattice_node(prm.fine, e, iff, jf, kf);
-          double s = prm.in[3 * node + c] * (1.0 / (double)multiplicity(prm.fine, node));
-          t1 += prm.ctof[kf * NC + kc] * s;
+          const double s = base[3 * iff + sy * jf + sz * kf] * (hxy * half(kf, ez, f.cells[2]));
+          t1 += prm.C[kf * NC + kc] * s;
         }
-        t2 += prm.ctof[jf * NC + jc] * t1;
+#pragma unroll
+        for (int jc = 0; jc < NC; ++jc) t2[jc] += prm.C[jf * NC + jc] * t1;
       }
-      out += prm.ctof[iff * NC + ic] * t2;
+#pragma unroll
+      for (int jc = 0; jc < NC; ++jc)
+#pragma unroll
+        for (int ic = 0; ic < NC; ++ic) out[jc][ic] += prm.C[iff * NC + ic] * t2[jc];
     }
-    prm.evec[(e * 3 + c) * NC3 + a] = out;
+    double* o = prm.evec + (e * 3 + c) * NC3 + kc * NC * NC;
+#pragma unroll
+    for (int jc = 0; jc < NC; ++jc)
+#pragma unroll
+      for (int ic = 0; ic < NC; ++ic) o[jc * NC + ic] = out[jc][ic];
   }
 }
 
@@ -128,6 +145,7 @@ Transfer::Transfer(const int cells[3], int fine_order, int coarse_order)
   std::vector<double> ctof;
   lagrange_tabulate(gauss_lobatto(coarse_order), gauss_lobatto(fine_order), &ctof, nullptr);
   ctof_.upload(ctof);
+  ctof_h_ = ctof;
   dispatch_transfer(pf_, pc_, [](auto, auto) {});
 }
 
@@ -135,7 +153,7 @@ void Transfer::prolong(const double* xc, double* xf, cudaStream_t s) {
   int nf = pf_ + 1;
   size_t need = (size_t)fine_.num_elements() * 3 * nf * nf * nf;
   if (evf_.n != need) evf_.alloc(need);
-  TransferParams prm{fine_, coarse_, ctof_.p, xc, evf_.p};
+  TransferParams prm{fine_, coarse_, ctof_.p, xc, evf_.p, {}};
   dispatch_transfer(pf_, pc_, [&](auto NFc, auto NCc) {
     constexpr int NF = decltype(NFc)::value, NC = decltype(NCc)::value;
     prolong_element_kernel<NF, NC><<<grid_for((long long)need, 128), 128, 0, s>>>(prm);
@@ -157,10 +175,12 @@ void Transfer::restrict_to(const double* xf, double* xc, cudaStream_t s) {
   int nc = pc_ + 1;
   size_t need = (size_t)coarse_.num_elements() * 3 * nc * nc * nc;
   if (evc_.n != need) evc_.alloc(need);
-  TransferParams prm{fine_, coarse_, ctof_.p, xf, evc_.p};
+  TransferParams prm{fine_, coarse_, ctof_.p, xf, evc_.p, {}};
+  for (size_t i = 0; i < ctof_h_.size(); ++i) prm.C[i] = ctof_h_[i];
   dispatch_transfer(pf_, pc_, [&](auto NFc, auto NCc) {
     constexpr int NF = decltype(NFc)::value, NC = decltype(NCc)::value;
-    restrict_element_kernel<NF, NC><<<grid_for((long long)need, 128), 128, 0, s>>>(prm);
+    const long long threads = (long long)coarse_.num_elements() * 3 * NC;
+    restrict_element_kernel<NF, NC><<<grid_for(threads, 128), 128, 0, s>>>(prm);
   });
   HXG_CUDA(cudaGetLastError());
   NodeParams np{};

@@ -17,6 +17,7 @@ class Transfer {
   int pf_, pc_;
   BoxDev fine_, coarse_;
   DevBuf<double> ctof_;
+  std::vector<double> ctof_h_;  // host copy (passed by value to the kernels)
   DevBuf<double> evf_, evc_;
 };
 
