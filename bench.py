@@ -264,32 +264,60 @@ def run_ours(args, rank, world, local_rank):
     # nested-dissection Cholesky), PCG to the reference's linear_rtol = 1e-3
     # (nonlinear.hpp:20), device-timed.
     newton = None
+    pmg = []
     if world == 1 and not args.no_newton:
         from paper_2204_01722_b200.hexmg import cg_solve
-        ev0, ev1, ev2, ev3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
-        prob_n = FemProblem(extents=(1.0, 1.0, 1.0), cells=(CELLS,) * 3, order=ORDER,
-                            fixed_faces=("-x",), traction_face="+x", traction=(0.0, 0.0, -0.02))
-        un = torch.zeros(prob_n.size(), dtype=torch.float64, device="cuda")
-        mg = prob_n.hierarchy
-        prob_n.op.apply_residual(un)
-        mg.setup_numeric()  # warm-up: symbolic analysis, allocations
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        fn = prob_n.op.apply_residual(un)
-        ev1.record(stream)
-        mg.setup_numeric()
-        ev2.record(stream)
-        rep = cg_solve(prob_n.op, -fn, rtol=1e-3, precond="mg", mg=mg)
-        un += rep["x"]
-        ev3.record(stream)
-        torch.cuda.synchronize()
-        newton = {"config": f"Q{ORDER} {CELLS}^3, fixed -x, traction (0,0,-0.02) on +x, u = 0",
-                  "step_ms": ev0.elapsed_time(ev3), "residual_ms": ev0.elapsed_time(ev1),
-                  "setup_numeric_ms": ev1.elapsed_time(ev2), "pcg_ms": ev2.elapsed_time(ev3),
-                  "cg_iterations": rep["iterations"], "linear_rtol": 1e-3,
-                  "condition": rep["eig_max"] / rep["eig_min"],
-                  "coarse_solver": "nested-dissection multifrontal Cholesky (device)"}
-        del prob_n, mg
+
+        def pmg_case(order, cells, newton_step):
+            """p-MG on the cube (fixed -x, traction (0,0,-0.02) on +x, u = 0):
+            residual (state), setup_numeric (diagonals, Chebyshev lambda_max,
+            coarse assembly + nested-dissection Cholesky), PCG; device-timed."""
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+            prob_n = FemProblem(extents=(1.0, 1.0, 1.0), cells=(cells,) * 3, order=order,
+                                fixed_faces=("-x",), traction_face="+x",
+                                traction=(0.0, 0.0, -0.02))
+            un = torch.zeros(prob_n.size(), dtype=torch.float64, device="cuda")
+            mg = prob_n.hierarchy
+            prob_n.op.apply_residual(un)
+            mg.setup_numeric()  # warm-up: symbolic analysis, allocations
+            torch.cuda.synchronize()
+            evs[0].record(stream)
+            fn = prob_n.op.apply_residual(un)
+            evs[1].record(stream)
+            mg.setup_numeric()
+            evs[2].record(stream)
+            rep = cg_solve(prob_n.op, -fn, rtol=1e-3, precond="mg", mg=mg)
+            evs[3].record(stream)
+            rep8 = cg_solve(prob_n.op, -fn, rtol=1e-8, precond="mg", mg=mg)
+            evs[4].record(stream)
+            mg.v_cycle(-fn)
+            evs[5].record(stream)
+            torch.cuda.synchronize()
+            if newton_step:
+                un += rep["x"]
+            out = {"config": f"Q{order} {cells}^3, levels {[mg.level_size(k) for k in range(mg.num_levels())]} DoF",
+                   "residual_ms": evs[0].elapsed_time(evs[1]),
+                   "setup_numeric_ms": evs[1].elapsed_time(evs[2]),
+                   "pcg_rtol1e-3_ms": evs[2].elapsed_time(evs[3]),
+                   "pcg_rtol1e-3_iterations": rep["iterations"],
+                   "pcg_rtol1e-8_ms": evs[3].elapsed_time(evs[4]),
+                   "pcg_rtol1e-8_iterations": rep8["iterations"],
+                   "vcycle_ms": evs[4].elapsed_time(evs[5]),
+                   "condition": rep8["eig_max"] / rep8["eig_min"]}
+            del prob_n, mg
+            torch.cuda.empty_cache()
+            return out
+
+        # BASELINE.json configs[1]: single Newton-Krylov step at Q2 64^3
+        # (linear_rtol = 1e-3, nonlinear.hpp:20); configs[2]: Q3 / Q4 p-MG.
+        nk = pmg_case(ORDER, CELLS, True)
+        newton = {"config": nk["config"] + ", fixed -x, traction (0,0,-0.02) on +x, u = 0",
+                  "step_ms": nk["residual_ms"] + nk["setup_numeric_ms"] + nk["pcg_rtol1e-3_ms"],
+                  "residual_ms": nk["residual_ms"], "setup_numeric_ms": nk["setup_numeric_ms"],
+                  "pcg_ms": nk["pcg_rtol1e-3_ms"], "cg_iterations": nk["pcg_rtol1e-3_iterations"],
+                  "linear_rtol": 1e-3,
+                  "coarse_solver": "nested-dissection multifrontal Cholesky (device, inverse-panel solve)"}
+        pmg = [nk] + [pmg_case(o, c, False) for o, c in ((3, 43), (4, 32))]
 
     # CPU baseline: the reference on the host cores, rank 0, N = 1 only.
     cpu = None
@@ -328,6 +356,7 @@ def run_ours(args, rank, world, local_rank):
             "clocks": sampler.summary(),
             "cpu_baseline": cpu,
             "newton_krylov_step": newton,
+            "pmg_solves": pmg,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -262,12 +262,22 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
     const int nbz = P * min(BZ, box.cells[2] - c.z * BZ) + 1;
     const int node0 = P * c.x * BX + npx * (P * c.y * BY + npy * (P * c.z * BZ));
     if (warp < WARPS && lane < 3 * nbx) {
-      for_rows(nby, nbz, [&](int iy, int iz) {
-        const double* src = prm.x + 3 * (node0 + npx * (iy + npy * iz)) + lane;
-        const unsigned d = (unsigned)__cvta_generic_to_shared(
-            dst + lc * D::NBP + (iz * D::NBYP + iy) * D::NBXP + lix);
+      const double* src0 = prm.x + 3 * node0 + lane;
+      const unsigned d0 = (unsigned)__cvta_generic_to_shared(dst + lc * D::NBP + lix);
+      auto row = [&](int iy, int iz) {
+        const double* src = src0 + 3 * npx * (iy + npy * iz);
+        const unsigned d = d0 + (unsigned)sizeof(double) * ((iz * D::NBYP + iy) * D::NBXP);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-      });
+      };
+      if (nbx == NBX && nby == NBY && nbz == D::NBZ) {
+#pragma unroll
+        for (int t = 0; t < (NBY * D::NBZ + WARPS - 1) / WARPS; ++t) {
+          const int r = warp + t * WARPS;
+          if (r < NBY * D::NBZ) row(r % NBY, r / NBY);
+        }
+      } else {
+        for_rows(nby, nbz, row);
+      }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -285,6 +295,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
   const int ecy = min(BY, box.cells[1] - by * BY);
   const int ecz = min(BZ, box.cells[2] - bz * BZ);
   const int nbx = P * ecx + 1, nby = P * ecy + 1, nbz = P * ecz + 1;
+  const bool full = ecx == BX && ecy == BY && ecz == BZ;
   const int node0 = P * bx * BX + npx * (P * by * BY + npy * (P * bz * BZ));
   const int gx0 = P * bx * BX, gy0 = P * by * BY, gz0 = P * bz * BZ;
   double* Xc = Xs + cur * (3 * D::NBP);
@@ -580,7 +591,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
       const double v = e[0];
       return twox ? e[DX] + v : v;
     };
-    for_rows(nby, nbz, [&](int iy, int iz) {
+    auto row = [&](int iy, int iz) {
       const int lzh = iz / P < BZ ? iz / P : BZ - 1, k = iz - P * lzh;
       const int lyh = iy / P < BY ? iy / P : BY - 1, j = iy - P * lyh;
       const bool twoy = j == 0 && lyh > 0;
@@ -599,7 +610,16 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
           s = fb >= 0 ? Xc[c * D::NBP + (iz * D::NBYP + iy) * D::NBXP + ix] : prm.x[dof];
         prm.y[dof] = s;
       }
-    });
+    };
+    if (full) {  // compile-time row walk (constant divisors, unrolled)
+#pragma unroll
+      for (int t = 0; t < (NBY * D::NBZ + WARPS - 1) / WARPS; ++t) {
+        const int r = warp + t * WARPS;
+        if (r < NBY * D::NBZ) row(r % NBY, r / NBY);
+      }
+    } else {
+      for_rows(nby, nbz, row);
+    }
   }
   // (the next iteration's first barrier orders these slab reads before the
   // slabs are rewritten)
@@ -612,54 +632,52 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
 }
 
 // Sums brick-boundary partials: nodes on planes g_d = k P B_d (or the domain's
-// far face) in increasing brick order.
-// One warp per (gy, gz) node row (blockDim = 32 x 4, grid = (ceil(npy/4), npz)).
-// Rows on a y or z brick plane are boundary along their whole length; other
-// rows only at the x brick planes.
+// far face) in increasing brick order.  One thread per (node, component) of
+// a (gy, gz) node row (blockDim 128, grid (ceil(3 npx / 128), npy, npz)):
+// rows on a y or z brick plane are boundary along their whole length, and
+// consecutive lanes read consecutive doubles of a brick's partial row
+// (coalesced); other rows only hold the x brick-plane nodes, which the
+// first block of the row covers.
 template <int P, int Q>
-__global__ void fused_fixup_kernel(const __grid_constant__ FusedParams prm) {
+__global__ void __launch_bounds__(128) fused_fixup_kernel(const __grid_constant__ FusedParams prm) {
   using D = FDims<P, Q>;
   constexpr int PB0 = P * D::BX, PB1 = P * D::BY, PB2 = P * D::BZ;
   const BoxDev& box = prm.box;
   const QLayout& lay = prm.lay;
-  const int gy = blockIdx.x * blockDim.y + threadIdx.y, gz = blockIdx.y + prm.gz0;
+  const int gy = blockIdx.y, gz = blockIdx.z + prm.gz0;
   const int npx = box.npd[0], npy = box.npd[1];
-  if (gy >= npy) return;
   const bool yb = gy % PB1 == 0 || gy == npy - 1;
   const bool zb = gz % PB2 == 0 || gz == box.npd[2] - 1;
-  const bool full = yb || zb;
-  // y / z brick ranges of this row.
-  const int b1 = gy / PB1, b2 = gz / PB2;
+  int gx, c;
+  if (yb || zb) {
+    const int e = blockIdx.x * 128 + threadIdx.x;
+    if (e >= 3 * npx) return;
+    gx = e / 3;
+    c = e - 3 * gx;
+  } else {
+    const int nx_planes = (npx - 1 + PB0 - 1) / PB0 + 1;  // x brick planes incl. far face
+    if (blockIdx.x != 0 || threadIdx.x >= 3 * nx_planes) return;
+    const int t = threadIdx.x / 3;
+    c = threadIdx.x - 3 * t;
+    gx = min(t * PB0, npx - 1);
+  }
+  const int b1 = gy / PB1, b2 = gz / PB2, b0 = gx / PB0;
   const int lo1 = (gy % PB1 == 0 && b1 > 0) ? b1 - 1 : b1, hi1 = min(b1, lay.nb[1] - 1);
   const int lo2 = (gz % PB2 == 0 && b2 > 0) ? b2 - 1 : b2, hi2 = min(b2, lay.nb[2] - 1);
+  const int lo0 = (gx % PB0 == 0 && b0 > 0) ? b0 - 1 : b0, hi0 = min(b0, lay.nb[0] - 1);
   const unsigned long long pol = policy_evict_first();
-  const int nx_planes = (npx - 1 + PB0 - 1) / PB0 + 1;  // x brick planes incl. far face
-  const int count = full ? npx : nx_planes;
-  for (int t = threadIdx.x; t < count; t += 32) {
-    const int gx = full ? t : min(t * PB0, npx - 1);
-    const int b0 = gx / PB0;
-    const int lo0 = (gx % PB0 == 0 && b0 > 0) ? b0 - 1 : b0, hi0 = min(b0, lay.nb[0] - 1);
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int c2 = lo2; c2 <= hi2; ++c2)
-      for (int c1 = lo1; c1 <= hi1; ++c1)
-        for (int c0 = lo0; c0 <= hi0; ++c0) {
-          const size_t brick = c0 + (size_t)lay.nb[0] * (c1 + (size_t)lay.nb[1] * c2);
-          const int ix = gx - PB0 * c0, iy = gy - PB1 * c1, iz = gz - PB2 * c2;
-          const double* p =
-              prm.partial + brick * (D::NB * 3) + ((iz * D::NBY + iy) * D::NBX + ix) * 3;
-          s0 += ld_once(p, pol);
-          s1 += ld_once(p + 1, pol);
-          s2 += ld_once(p + 2, pol);
-        }
-    const size_t dof0 = 3 * ((size_t)gx + (size_t)npx * (gy + (size_t)npy * gz));
-    const double s[3] = {s0, s1, s2};
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      double v = s[c];
-      if (prm.mask && prm.mask[dof0 + c]) v = prm.x[dof0 + c];
-      prm.y[dof0 + c] = v;
-    }
-  }
+  double s = 0.0;
+  for (int c2 = lo2; c2 <= hi2; ++c2)
+    for (int c1 = lo1; c1 <= hi1; ++c1)
+      for (int c0 = lo0; c0 <= hi0; ++c0) {
+        const size_t brick = c0 + (size_t)lay.nb[0] * (c1 + (size_t)lay.nb[1] * c2);
+        const int ix = gx - PB0 * c0, iy = gy - PB1 * c1, iz = gz - PB2 * c2;
+        s += ld_once(prm.partial + brick * (D::NB * 3) + ((iz * D::NBY + iy) * D::NBX + ix) * 3 + c,
+                     pol);
+      }
+  const size_t dof = 3 * ((size_t)gx + (size_t)npx * (gy + (size_t)npy * gz)) + c;
+  if (prm.mask && prm.mask[dof]) s = prm.x[dof];
+  prm.y[dof] = s;
 }
 
 // Persistent grid: every resident CTA slot of the device, capped by the work.
@@ -730,8 +748,8 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
     prm.nbricks = (int)op.lay_.num_bricks();
     k<<<persistent_grid(k, D::T, smem, prm.nbricks), D::T, smem, op.stream_>>>(prm);
     HXG_CUDA(cudaGetLastError());
-    dim3 fb(32, 4), fg((op.box_.npd[1] + 3) / 4, op.box_.npd[2]);
-    fused_fixup_kernel<P, Q><<<fg, fb, 0, op.stream_>>>(prm);
+    dim3 fg((3 * op.box_.npd[0] + 127) / 128, op.box_.npd[1], op.box_.npd[2]);
+    fused_fixup_kernel<P, Q><<<fg, 128, 0, op.stream_>>>(prm);
     HXG_CUDA(cudaGetLastError());
   });
 }
@@ -803,8 +821,8 @@ void fused_jacobian_host(Operator& op, const double* xh, double* yh) {
       const int zs = i == 0 ? 0 : pb2 * lb;
       const int ze = i == C - 1 ? npz : pb2 * le;
       pc.gz0 = zs;
-      dim3 fb(32, 4), fg((op.box_.npd[1] + 3) / 4, ze - zs);
-      fused_fixup_kernel<P, Q><<<fg, fb, 0, pp.comp>>>(pc);
+      dim3 fg((3 * op.box_.npd[0] + 127) / 128, op.box_.npd[1], ze - zs);
+      fused_fixup_kernel<P, Q><<<fg, 128, 0, pp.comp>>>(pc);
       HXG_CUDA(cudaGetLastError());
       HXG_CUDA(cudaEventRecord(pp.out_ready[i], pp.comp));
       HXG_CUDA(cudaStreamWaitEvent(pp.d2h, pp.out_ready[i], 0));

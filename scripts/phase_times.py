@@ -11,9 +11,11 @@ L = capi.lib(); buf = (ctypes.c_ulonglong * 10)()
 prob.op.apply_jacobian(x, y); L.hxg_debug_phase_cycles(buf, 1)
 for _ in range(5): prob.op.apply_jacobian(x, y)
 L.hxg_debug_phase_cycles(buf, 1)
-nb = (n + 3) // 4 * ((n + 3) // 4) * ((n + 1) // 2)
+nb = prob.op.num_bricks() if hasattr(prob.op, 'num_bricks') else (n + 3) // 4 * ((n + 3) // 4) * ((n + 1) // 2)
 v = np.array(list(buf), dtype=float) / 5 / nb
-names = ["load x", "P1", "P2+QF", "Q1", "Q2", "AX", "AY", "Z+store", "end"]
+names = {0: "x block wait+mask", 1: "P1 (x,y passes)", 2: "P2 z pass + QF", 3: "Q1 z adjoint",
+         4: "Q2 (y,x adjoint)", 5: "exp3", 8: "overlap-add+store"}
 tot = v[:9].sum()
-for nm, c in zip(names, v[:9]): print(f"{nm:10s} {c:8.0f} cycles/brick {100*c/tot:5.1f}%")
+for i, c in enumerate(v[:9]):
+    if c: print(f"{names.get(i, i)!s:20s} {c:8.0f} cycles/brick {100*c/tot:5.1f}%")
 print("total", tot)
