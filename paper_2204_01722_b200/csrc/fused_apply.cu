@@ -170,7 +170,7 @@ __device__ __forceinline__ void st_keep(double* a, double v, unsigned long long 
 }
 __device__ __forceinline__ double ld_once(const double* a, unsigned long long pol) {
   double v;
-  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+  asm("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
                : "=d"(v)
                : "l"(a), "l"(pol));
   return v;
@@ -270,8 +270,9 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
       };
       if (nbx == NBX && nby == NBY && nbz == D::NBZ) {
-#pragma unroll
-        for (int t = 0; t < (NBY * D::NBZ + WARPS - 1) / WARPS; ++t) {
+        constexpr int RPW = (NBY * D::NBZ + WARPS - 1) / WARPS;
+#pragma unroll(RPW <= 6 ? RPW : 1)
+        for (int t = 0; t < RPW; ++t) {
           const int r = warp + t * WARPS;
           if (r < NBY * D::NBZ) row(r % NBY, r / NBY);
         }
@@ -342,7 +343,11 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
   double* S = Ebase + le * D::ELEM;
   double* EOe = S + D::S;
   constexpr int Q2 = D::Q2;
-  __syncthreads(); HXG_PHASE(0);
+  // Only the general-mask zeroing above writes the landed block; the slab
+  // hazards with the previous brick are ordered by the barrier after the
+  // cp.async wait (P1 writes S, the overlap-add read EO).
+  if (fb < 0) __syncthreads();
+  HXG_PHASE(0);
 
   // ---- forward: G = (Bd (x) B (x) B, B (x) Bd (x) B, B (x) B (x) Bd) U -----
   // The direct tensor-product gradient (deriv tabulated at the points,
@@ -612,8 +617,9 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
       }
     };
     if (full) {  // compile-time row walk (constant divisors, unrolled)
-#pragma unroll
-      for (int t = 0; t < (NBY * D::NBZ + WARPS - 1) / WARPS; ++t) {
+      constexpr int RPW = (NBY * D::NBZ + WARPS - 1) / WARPS;
+#pragma unroll(RPW <= 6 ? RPW : 1)
+      for (int t = 0; t < RPW; ++t) {
         const int r = warp + t * WARPS;
         if (r < NBY * D::NBZ) row(r % NBY, r / NBY);
       }
@@ -631,6 +637,48 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
 #endif
 }
 
+template <int P, int Q>
+__device__ __forceinline__ void fixup_entry(const FusedParams& prm, int gx, int gy, int gz, int c) {
+  using D = FDims<P, Q>;
+  constexpr int PB0 = P * D::BX, PB1 = P * D::BY, PB2 = P * D::BZ;
+  const BoxDev& box = prm.box;
+  const QLayout& lay = prm.lay;
+  const int npx = box.npd[0], npy = box.npd[1];
+  const int b1 = gy / PB1, b2 = gz / PB2, b0 = gx / PB0;
+  const int lo1 = (gy % PB1 == 0 && b1 > 0) ? b1 - 1 : b1, hi1 = min(b1, lay.nb[1] - 1);
+  const int lo2 = (gz % PB2 == 0 && b2 > 0) ? b2 - 1 : b2, hi2 = min(b2, lay.nb[2] - 1);
+  const int lo0 = (gx % PB0 == 0 && b0 > 0) ? b0 - 1 : b0, hi0 = min(b0, lay.nb[0] - 1);
+  const unsigned long long pol = policy_evict_first();
+  // Up to 8 sharing bricks, q = i0 + 2 i1 + 4 i2 = (c0, c1, c2) offsets from
+  // (lo0, lo1, lo2): all loads issued together, then summed in increasing q
+  // = increasing brick order.
+  const int n0 = hi0 - lo0, n1 = hi1 - lo1, n2 = hi2 - lo2;  // 0 or 1
+  const double* p0 = prm.partial +
+                     (lo0 + (size_t)lay.nb[0] * (lo1 + (size_t)lay.nb[1] * lo2)) * (D::NB * 3) +
+                     (((gz - PB2 * lo2) * D::NBY + (gy - PB1 * lo1)) * D::NBX + (gx - PB0 * lo0)) * 3 + c;
+  double v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int i0 = q & 1, i1 = (q >> 1) & 1, i2 = q >> 2;
+    v[q] = 0.0;
+    if (i0 <= n0 && i1 <= n1 && i2 <= n2) {
+      // neighbour brick +i_d: brick index +i_d stride, local coordinate -i_d P B_d
+      const long long off = (i0 + (long long)lay.nb[0] * (i1 + (long long)lay.nb[1] * i2)) * (D::NB * 3) -
+                            3LL * ((i2 * PB2 * D::NBY + i1 * PB1) * D::NBX + i0 * PB0);
+      v[q] = ld_once(p0 + off, pol);
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int i0 = q & 1, i1 = (q >> 1) & 1, i2 = q >> 2;
+    if (i0 <= n0 && i1 <= n1 && i2 <= n2) s += v[q];
+  }
+  const size_t dof = 3 * ((size_t)gx + (size_t)npx * (gy + (size_t)npy * gz)) + c;
+  if (prm.mask && prm.mask[dof]) s = prm.x[dof];
+  prm.y[dof] = s;
+}
+
 // Sums brick-boundary partials: nodes on planes g_d = k P B_d (or the domain's
 // far face) in increasing brick order.  One thread per (node, component) of
 // a (gy, gz) node row (blockDim 128, grid (ceil(3 npx / 128), npy, npz)):
@@ -643,7 +691,6 @@ __global__ void __launch_bounds__(128) fused_fixup_kernel(const __grid_constant_
   using D = FDims<P, Q>;
   constexpr int PB0 = P * D::BX, PB1 = P * D::BY, PB2 = P * D::BZ;
   const BoxDev& box = prm.box;
-  const QLayout& lay = prm.lay;
   const int gy = blockIdx.y, gz = blockIdx.z + prm.gz0;
   const int npx = box.npd[0], npy = box.npd[1];
   const bool yb = gy % PB1 == 0 || gy == npy - 1;
@@ -661,23 +708,7 @@ __global__ void __launch_bounds__(128) fused_fixup_kernel(const __grid_constant_
     c = threadIdx.x - 3 * t;
     gx = min(t * PB0, npx - 1);
   }
-  const int b1 = gy / PB1, b2 = gz / PB2, b0 = gx / PB0;
-  const int lo1 = (gy % PB1 == 0 && b1 > 0) ? b1 - 1 : b1, hi1 = min(b1, lay.nb[1] - 1);
-  const int lo2 = (gz % PB2 == 0 && b2 > 0) ? b2 - 1 : b2, hi2 = min(b2, lay.nb[2] - 1);
-  const int lo0 = (gx % PB0 == 0 && b0 > 0) ? b0 - 1 : b0, hi0 = min(b0, lay.nb[0] - 1);
-  const unsigned long long pol = policy_evict_first();
-  double s = 0.0;
-  for (int c2 = lo2; c2 <= hi2; ++c2)
-    for (int c1 = lo1; c1 <= hi1; ++c1)
-      for (int c0 = lo0; c0 <= hi0; ++c0) {
-        const size_t brick = c0 + (size_t)lay.nb[0] * (c1 + (size_t)lay.nb[1] * c2);
-        const int ix = gx - PB0 * c0, iy = gy - PB1 * c1, iz = gz - PB2 * c2;
-        s += ld_once(prm.partial + brick * (D::NB * 3) + ((iz * D::NBY + iy) * D::NBX + ix) * 3 + c,
-                     pol);
-      }
-  const size_t dof = 3 * ((size_t)gx + (size_t)npx * (gy + (size_t)npy * gz)) + c;
-  if (prm.mask && prm.mask[dof]) s = prm.x[dof];
-  prm.y[dof] = s;
+  fixup_entry<P, Q>(prm, gx, gy, gz, c);
 }
 
 // Persistent grid: every resident CTA slot of the device, capped by the work.
