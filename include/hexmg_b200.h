@@ -58,6 +58,7 @@ const char* hxg_version(void);
 typedef struct hxg_state_s* hxg_state_t; /* QuadratureStateStore   operator.hpp:60-64 */
 typedef struct hxg_op_s* hxg_op_t;       /* MatrixFreeOperator     operator.hpp:70    */
 typedef struct hxg_mg_s* hxg_mg_t;       /* MultigridHierarchy     multigrid.hpp:88   */
+typedef struct hxg_chol_s* hxg_chol_t;   /* CholeskyCoarseSolver   coarse_solver.hpp:16 */
 
 /*
  * Operator descriptor = the arguments of the MatrixFreeOperator constructor
@@ -148,6 +149,10 @@ int hxg_mg_level_op(hxg_mg_t mg, int level, hxg_op_t* op); /* borrowed */
 /* setup_numeric (multigrid.hpp:100-113): diagonals, Chebyshev lambda_max by
  * 10 Lanczos steps, coarse assembly (assembly.hpp:142-230) + Cholesky. */
 int hxg_mg_setup_numeric(hxg_mg_t mg);
+/* coo_numeric only (assembly.hpp:178-230): assemble the p = 1 operator on the
+ * current state without building smoothers or factorizing (read it back with
+ * hxg_mg_coarse_csr_host). */
+int hxg_mg_assemble_coarse(hxg_mg_t mg);
 /* Coarse Cholesky backend: 0 automatic (dense below a few thousand DoFs,
  * else nested-dissection multifrontal), 1 dense, 2 nested-dissection
  * multifrontal, 3 cuSOLVER csrchol on the ND-permuted matrix.  Takes effect
@@ -166,6 +171,18 @@ int hxg_mg_coarse_nnz(hxg_mg_t mg, int64_t* nnz);
 int hxg_mg_coarse_csr_host(hxg_mg_t mg, int* row_ptr, int* cols, double* vals);
 /* Coarse Cholesky solve (coarse_solver.hpp:35-40). */
 int hxg_mg_coarse_solve(hxg_mg_t mg, const double* b, double* x);
+
+/* Standalone CholeskyCoarseSolver (coarse_solver.hpp:16-47) on a caller's
+ * assembled Q1 lattice matrix (CSR, both triangles, sorted columns, host
+ * arrays; npd = nodes per dimension, n = 3 * nodes).  analyzePattern on
+ * create, factorize per numeric setup, solve per V-cycle (device vectors).
+ * Used for the replicated coarse solve of the slab-partitioned p-MG. mode as
+ * hxg_mg_set_coarse_mode. */
+int hxg_chol_create(int n, const int* row_ptr, const int* cols, const int npd[3], int mode,
+                    hxg_chol_t* out);
+int hxg_chol_factorize(hxg_chol_t h, const double* vals_host);
+int hxg_chol_solve(hxg_chol_t h, const double* b, double* x);
+int hxg_chol_destroy(hxg_chol_t h);
 
 /* CgReport (cg.hpp:42-50). */
 typedef struct {

@@ -122,6 +122,11 @@ SIGNATURES = {
     "hxg_mg_coarse_nnz": [_vp, _P(_i64)],
     "hxg_mg_coarse_csr_host": [_vp, _vp, _vp, _vp],
     "hxg_mg_coarse_solve": [_vp, _vp, _vp],
+    "hxg_mg_assemble_coarse": [_vp],
+    "hxg_chol_create": [_i, _vp, _vp, _vp, _i, _vp],
+    "hxg_chol_factorize": [_vp, _vp],
+    "hxg_chol_solve": [_vp, _vp, _vp],
+    "hxg_chol_destroy": [_vp],
     "hxg_cg_solve": [_vp, _vp, _i, _vp, _vp, _d, _i, _vp, _vp, _i],
     "hxg_lambda_max_jacobi": [_vp, _i, _P(_d)],
     "hxg_dot": [_vp, _vp, _i64, _vp, _P(_d)],

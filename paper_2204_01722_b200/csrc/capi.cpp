@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "coarse.hpp"
 #include "common.hpp"
 #include "operator.hpp"
 #include "setup.hpp"
@@ -24,6 +25,12 @@ struct hxg_op_s {
 struct hxg_mg_s {
   std::unique_ptr<hxg::Hierarchy> h;
   std::vector<hxg_op_s> level_handles;
+};
+struct hxg_chol_s {
+  hxg::CsrMatrix a;
+  hxg::CoarseSolver solver;
+  int npd[3] = {0, 0, 0};
+  cudaStream_t stream = nullptr;
 };
 
 namespace {
@@ -251,6 +258,7 @@ int hxg_mg_level_op(hxg_mg_t mg, int level, hxg_op_t* op) {
   });
 }
 int hxg_mg_setup_numeric(hxg_mg_t mg) { return guarded([&] { MG(mg).setup_numeric(); }); }
+int hxg_mg_assemble_coarse(hxg_mg_t mg) { return guarded([&] { MG(mg).assemble_coarse(); }); }
 int hxg_mg_set_coarse_mode(hxg_mg_t mg, int mode) {
   return guarded([&] {
     if (mode < 0 || mode > 3)
@@ -414,3 +422,46 @@ int hxg_setup_traction_load(const double extents[3], const int cells[3], int p, 
 }
 
 }  // extern "C"
+
+/* Standalone coarse Cholesky on a Q1 lattice matrix (the replicated coarse
+ * solve of the distributed p-MG). */
+int hxg_chol_create(int n, const int* row_ptr, const int* cols, const int npd[3], int mode,
+                    hxg_chol_t* out) {
+  return guarded([&] {
+    if (!out || n <= 0 || !row_ptr || !cols || !npd)
+      throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "hxg_chol_create: bad arguments");
+    if ((long long)npd[0] * npd[1] * npd[2] * 3 != n)
+      throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "hxg_chol_create: n != 3 * nodes(npd)");
+    auto h = std::make_unique<hxg_chol_s>();
+    h->a.n = n;
+    h->a.row_ptr_h.assign(row_ptr, row_ptr + n + 1);
+    h->a.cols_h.assign(cols, cols + row_ptr[n]);
+    std::vector<int> rows((size_t)row_ptr[n]);
+    for (int i = 0; i < n; ++i)
+      for (int k = row_ptr[i]; k < row_ptr[i + 1]; ++k) rows[(size_t)k] = i;
+    h->a.row_ptr.upload(h->a.row_ptr_h);
+    h->a.cols.upload(h->a.cols_h);
+    h->a.rows.upload(rows);
+    h->a.vals.alloc((size_t)row_ptr[n]);
+    for (int d = 0; d < 3; ++d) h->npd[d] = npd[d];
+    h->solver.set_mode(mode);
+    *out = h.release();
+  });
+}
+int hxg_chol_factorize(hxg_chol_t h, const double* vals_host) {
+  return guarded([&] {
+    if (!h) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "null Cholesky handle");
+    HXG_CUDA(cudaMemcpy(h->a.vals.p, vals_host, sizeof(double) * h->a.cols_h.size(),
+                        cudaMemcpyHostToDevice));
+    h->solver.factorize(h->a, h->npd, h->stream);
+  });
+}
+int hxg_chol_solve(hxg_chol_t h, const double* b, double* x) {
+  return guarded([&] {
+    if (!h) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "null Cholesky handle");
+    h->solver.solve(b, x, h->stream);
+  });
+}
+int hxg_chol_destroy(hxg_chol_t h) {
+  return guarded([&] { delete h; });
+}

@@ -305,6 +305,11 @@ void Hierarchy::setup_numeric() {
   pt.mark("coarse factorization");
 }
 
+void Hierarchy::assemble_coarse() {
+  if (!assembly_) assembly_ = std::make_unique<CoarseAssembly>(*level(0).op);
+  assembly_->numeric(*level(0).op);
+}
+
 void Hierarchy::prolong(int coarse_level, const double* xc, double* xf) {
   level(coarse_level + 1).from_coarser->prolong(xc, xf, stream());
 }

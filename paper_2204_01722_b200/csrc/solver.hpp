@@ -67,11 +67,17 @@ class Hierarchy {
   int num_levels() const { return (int)levels_.size(); }
   Level& level(int k) { return *levels_[(size_t)k]; }
   void setup_numeric();
+  // coo_numeric only (assembly.hpp:178-230): the assembled coarse operator
+  // without smoothers or factorization (the distributed p-MG gathers it).
+  void assemble_coarse();
   void prolong(int coarse_level, const double* xc, double* xf);
   void restrict_to(int coarse_level, const double* xf, double* xc);
   void v_cycle(const double* b, double* x, bool x_zero = false);
   void coarse_solve(const double* b, double* x);
-  const CsrMatrix& coarse_matrix() const { return assembly_->matrix(); }
+  const CsrMatrix& coarse_matrix() const {
+    if (!assembly_) throw Error(HXG_ERR_STATE_NOT_INITIALIZED, "coarse operator not assembled");
+    return assembly_->matrix();
+  }
   // 0 automatic (dense below kDenseCoarseMax DoFs), 1 dense, 2 sparse ND.
   void set_coarse_mode(int m) { coarse_mode_ = m; }
   cudaStream_t stream() const { return levels_.back()->op->stream(); }

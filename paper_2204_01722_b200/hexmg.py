@@ -278,6 +278,10 @@ class MultigridHierarchy:
     def setup_numeric(self):
         check(lib().hxg_mg_setup_numeric(self.h))
 
+    def assemble_coarse(self):
+        """coo_numeric only (no smoothers / factorization)."""
+        check(lib().hxg_mg_assemble_coarse(self.h))
+
     def set_coarse_mode(self, mode):
         """0 automatic, 1 dense, 2 nested-dissection multifrontal, 3 cuSOLVER csrchol."""
         mode = {"auto": 0, "dense": 1, "sparse": 2, "nd": 2, "csrchol": 3}.get(mode, mode)
@@ -324,6 +328,42 @@ class MultigridHierarchy:
         b = _dev(b, self.level_size(0))
         x = torch.empty_like(b)
         check(lib().hxg_mg_coarse_solve(self.h, _ptr(b), _ptr(x)))
+        return x
+
+
+class CoarseCholesky:
+    """CholeskyCoarseSolver (coarse_solver.hpp:16-47) on a caller-assembled
+    Q1 lattice matrix: analyzePattern at construction, factorize(vals),
+    solve(b) on device vectors."""
+
+    def __init__(self, row_ptr, cols, npd, mode="auto"):
+        mode = {"auto": 0, "dense": 1, "sparse": 2, "nd": 2, "csrchol": 3}.get(mode, mode)
+        self._rp = np.ascontiguousarray(row_ptr, np.int32)
+        self._cols = np.ascontiguousarray(cols, np.int32)
+        self.n = len(self._rp) - 1
+        h = ctypes.c_void_p()
+        check(lib().hxg_chol_create(self.n, _ptr(self._rp), _ptr(self._cols),
+                                    _ptr(np.asarray(npd, np.int32)), int(mode), ctypes.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib().hxg_chol_destroy(self.h)
+            except Exception:  # interpreter shutdown
+                pass
+            self.h = None
+
+    def factorize(self, vals):
+        vals = np.ascontiguousarray(vals, np.float64)
+        if vals.size != self._cols.size:
+            raise ValueError("value array does not match the pattern")
+        check(lib().hxg_chol_factorize(self.h, _ptr(vals)))
+
+    def solve(self, b, x=None):
+        b = _dev(b, self.n)
+        x = torch.empty_like(b) if x is None else x
+        check(lib().hxg_chol_solve(self.h, _ptr(b), _ptr(x)))
         return x
 
 
