@@ -7,9 +7,9 @@
 // in the new numbering) plus its shell = lattice nodes adjacent to its
 // region, all of which are ancestor pivots.  Numeric phase (device, per
 // setup): postorder over fronts, assemble original entries + children's
-// update matrices (extend-add, fixed order), potrf / trsm / syrk on the
-// dense front, then keep the (np + ns) x np panel in inverse form
-// M = [L11^-1; L21 L11^-1] (two cuBLAS trsm).  Solve (per V-cycle): forward
+// update matrices (extend-add, fixed order), then the
+// dense front in inverse form: L11 = potrf(A11), W = L11^-1 (trtri),
+// L21 = A21 W^T and M = [W; L21 W] by GEMM, S = A22 - L21 L21^T by syrk.  Solve (per V-cycle): forward
 // sweep leaves -> root, z1 = L11^-1 y1 and u = y2 - L21 L11^-1 y1 in ONE
 // GEMV with M, update vectors passed up the tree; backward sweep root ->
 // leaves, x1 = M^T [z1; -x2] in one transposed GEMV.  Every front of a tree
@@ -28,6 +28,7 @@ namespace hxg {
 namespace {
 
 constexpr int kLeafNodes = 128;
+constexpr int kLaneDepth = 4;  // 16 concurrent subtree lanes in the factorization
 
 __global__ void assemble_kernel(const long long* __restrict__ dst, const int* __restrict__ src,
                                 long long n, const double* __restrict__ vals, double* front) {
@@ -205,12 +206,6 @@ __global__ void __launch_bounds__(kBC) nd_bwd_finish(NdSolve a, int ct0) {
   a.w[a.piv0[t] + j] = s;
 }
 
-__global__ void identity_kernel(double* a, int n) {
-  const long long total = (long long)n * n;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x)
-    a[e] = (e % (n + 1)) == 0 ? 1.0 : 0.0;
-}
 
 void cublas_check(cublasStatus_t s, const char* what) {
   if (s != CUBLAS_STATUS_SUCCESS) throw Error(HXG_ERR_CUDA, std::string(what) + " failed");
@@ -218,10 +213,8 @@ void cublas_check(cublasStatus_t s, const char* what) {
 
 }  // namespace
 
-NdCholesky::~NdCholesky() {
-  if (cublas_) cublasDestroy(cublas_);
-  if (cusolver_) cusolverDnDestroy(cusolver_);
-}
+NdCholesky::NdCholesky() = default;
+NdCholesky::~NdCholesky() = default;
 
 void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
   n_ = a.n;
@@ -287,7 +280,6 @@ void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
   std::vector<int> shell_rows;
   std::vector<std::vector<int>> shell((size_t)nf);
   lsize_ = 0;
-  max_front_ = 0;
   for (int t = 0; t < nf; ++t) {
     const Box& r = region[(size_t)t];
     int lo[3], hi[3];
@@ -315,7 +307,6 @@ void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
     f.loff = lsize_;
     const size_t m = (size_t)f.np + f.ns;
     lsize_ += m * (size_t)f.np;
-    max_front_ = std::max(max_front_, m * m);
   }
   // Position of a new index within front t's rows (pivots then shell).
   auto pos_in = [&](int t, int ni) -> int {
@@ -339,24 +330,6 @@ void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
         maps.push_back(p);
       }
     }
-  }
-  // Update-stack bound: simulate the postorder push/pop.
-  {
-    std::vector<size_t> stack;
-    size_t cur = 0, peak = 0;
-    for (int t = 0; t < nf; ++t) {
-      const Front& f = fronts_[(size_t)t];
-      int nch = (f.child[0] >= 0) + (f.child[1] >= 0);
-      for (int k = 0; k < nch; ++k) {
-        cur -= stack.back();
-        stack.pop_back();
-      }
-      size_t u = (size_t)f.ns * f.ns;
-      stack.push_back(u);
-      cur += u;
-      peak = std::max(peak, cur);
-    }
-    max_update_ = peak;
   }
   // Assembly lists: lower-triangle original entries with a pivot column.
   std::vector<long long> adst;
@@ -475,94 +448,244 @@ void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
   part_f_.alloc(std::max<size_t>(ftf.size(), 1) * kFR);
   part_b_.alloc(std::max<size_t>(btf.size(), 1) * kBC);
   L_.alloc(lsize_);
-  work_.alloc(max_front_);
   size_t maxnp = 1;
   for (const auto& f : fronts_) maxnp = std::max(maxnp, (size_t)f.np);
-  inv_.alloc(maxnp * maxnp);
-  stack_.alloc(std::max<size_t>(max_update_, 1));
   wvec_.alloc((size_t)n_);
-  info_.alloc((size_t)nf);
+  info_.alloc(2 * (size_t)nf);  // potrf, then trtri status per front
   analyzed_ = true;
 }
 
-void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s) {
-  if (!cublas_) {
-    cublas_check(cublasCreate(&cublas_), "cublasCreate");
-    if (cusolverDnCreate(&cusolver_) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "cusolverDnCreate failed");
+// Lane = one stream + handles + workspaces.  The dissection tree is cut at
+// depth kLaneDepth: each subtree there is factored on its own lane (its
+// fronts are contiguous in postorder, with a private update stack), so the
+// many small fronts of different subtrees run concurrently; the subtree
+// roots hand their update matrices over in dedicated buffers, and the top
+// fronts run on the caller's stream once every lane has finished.
+struct NdCholesky::Lane {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+  cublasHandle_t cublas = nullptr;
+  cusolverDnHandle_t cusolver = nullptr;
+  DevBuf<double> W, inv, tmp, potrf_ws, trtri_ws, stack;
+  std::vector<char> trtri_host;
+  std::vector<int> fronts;  // postorder
+  bool own_stream = false;
+  ~Lane() {
+    if (cublas) cublasDestroy(cublas);
+    if (cusolver) cusolverDnDestroy(cusolver);
+    if (done) cudaEventDestroy(done);
+    if (own_stream && stream) cudaStreamDestroy(stream);
   }
-  cublasSetStream(cublas_, s);
-  cusolverDnSetStream(cusolver_, s);
-  if (!analyzed_) analyze(a, npd);
-  ready_ = false;
-  HXG_CUDA(cudaMemsetAsync(info_.p, 0, sizeof(int) * fronts_.size(), s));
-  std::vector<std::pair<size_t, int>> stack;  // (offset, ns)
-  size_t top = 0;
-  const double one = 1.0, minus_one = -1.0;
-  for (int t = 0; t < (int)fronts_.size(); ++t) {
+};
+
+void NdCholesky::plan_lanes() {
+  const int nf = (int)fronts_.size();
+  int maxlev = 0;
+  for (const auto& f : fronts_) maxlev = std::max(maxlev, f.level);
+  const int depth = std::min(kLaneDepth, maxlev);
+  // subtree of each front: the ancestor at `depth` (or -1 for top fronts)
+  std::vector<int> sub((size_t)nf, -1);
+  std::vector<int> roots;
+  for (int t = nf - 1; t >= 0; --t) {  // parents after children in postorder
     const Front& f = fronts_[(size_t)t];
-    const int m = f.np + f.ns;
-    double* W = work_.p;
-    HXG_CUDA(cudaMemsetAsync(W, 0, sizeof(double) * (size_t)m * m, s));
-    const long long na = (long long)(asm_begin_[(size_t)t + 1] - asm_begin_[(size_t)t]);
-    if (na > 0)
-      assemble_kernel<<<grid_for(na, 256), 256, 0, s>>>(asm_dst_.p + asm_begin_[(size_t)t],
-                                                        asm_src_.p + asm_begin_[(size_t)t], na,
-                                                        a.vals.p, W);
-    // Children's updates sit on top of the stack: child[1] above child[0].
-    int nch = (f.child[0] >= 0) + (f.child[1] >= 0);
-    std::vector<std::pair<size_t, int>> ups(stack.end() - nch, stack.end());
-    for (int q = 0; q < nch; ++q) {
-      const int c = f.child[q];
-      const Front& fc = fronts_[(size_t)c];
-      const auto& up = ups[(size_t)q];
-      if (fc.ns > 0)
-        extend_add_kernel<<<grid_for((long long)fc.ns * fc.ns, 256), 256, 0, s>>>(
-            stack_.p + up.first, fc.ns, child_map_.p + f.map_off[q], W, m);
+    if (f.level == depth && depth > 0) {
+      sub[(size_t)t] = (int)roots.size();
+      roots.push_back(t);
+    } else if (f.level > depth) {
+      sub[(size_t)t] = sub[(size_t)f.parent];
     }
-    for (int q = 0; q < nch; ++q) stack.pop_back();
-    top = stack.empty() ? 0 : stack.back().first + (size_t)stack.back().second * stack.back().second;
-    HXG_CUDA(cudaGetLastError());
-    // Dense partial factorization.
-    int lwork = 0;
-    if (cusolverDnDpotrf_bufferSize(cusolver_, CUBLAS_FILL_MODE_LOWER, f.np, W, m, &lwork) !=
-        CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "potrf_bufferSize failed");
-    if (potrf_ws_.n < (size_t)lwork) potrf_ws_.alloc((size_t)lwork * 2);
-    if (cusolverDnDpotrf(cusolver_, CUBLAS_FILL_MODE_LOWER, f.np, W, m, potrf_ws_.p, lwork,
-                         info_.p + t) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "potrf failed");
-    if (f.ns > 0) {
-      cublas_check(cublasDtrsm(cublas_, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
-                               CUBLAS_DIAG_NON_UNIT, f.ns, f.np, &one, W, m, W + f.np, m),
-                   "trsm");
-      cublas_check(cublasDsyrk(cublas_, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, f.ns, f.np,
-                               &minus_one, W + f.np, m, &one, W + f.np + (size_t)f.np * m, m),
-                   "syrk");
-    }
-    // Inverse form of the panel: M_bot = L21 L11^-1 (in place, after syrk has
-    // consumed L21), M_top = L11^-1 (trsm against the identity: exact zeros
-    // above the diagonal).
-    if (f.ns > 0)
-      cublas_check(cublasDtrsm(cublas_, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
-                               CUBLAS_DIAG_NON_UNIT, f.ns, f.np, &one, W, m, W + f.np, m),
-                   "trsm (inverse panel)");
-    identity_kernel<<<grid_for((long long)f.np * f.np, 256), 256, 0, s>>>(inv_.p, f.np);
-    cublas_check(cublasDtrsm(cublas_, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
-                             CUBLAS_DIAG_NON_UNIT, f.np, f.np, &one, W, m, inv_.p, f.np),
-                 "trsm (L11 inverse)");
-    HXG_CUDA(cudaMemcpy2DAsync(W, sizeof(double) * m, inv_.p, sizeof(double) * f.np,
-                               sizeof(double) * f.np, f.np, cudaMemcpyDeviceToDevice, s));
-    HXG_CUDA(cudaMemcpyAsync(L_.p + f.loff, W, sizeof(double) * (size_t)m * f.np,
-                             cudaMemcpyDeviceToDevice, s));
-    if (f.ns > 0) {
-      HXG_CUDA(cudaMemcpy2DAsync(stack_.p + top, sizeof(double) * f.ns,
-                                 W + f.np + (size_t)f.np * m, sizeof(double) * m,
-                                 sizeof(double) * f.ns, f.ns, cudaMemcpyDeviceToDevice, s));
-    }
-    stack.emplace_back(top, f.ns);
-    top += (size_t)f.ns * f.ns;
   }
+  lanes_.clear();
+  lanes_.resize(roots.size() + 1);  // lane 0 = top fronts on the caller's stream
+  for (auto& l : lanes_) l = std::make_unique<Lane>();
+  lane_of_.assign((size_t)nf, 0);
+  for (int t = 0; t < nf; ++t) {
+    const int l = sub[(size_t)t] + 1;
+    lane_of_[(size_t)t] = l;
+    lanes_[(size_t)l]->fronts.push_back(t);
+  }
+  handoff_off_.assign((size_t)nf, (size_t)-1);
+  size_t hsize = 0;
+  for (int r : roots) {
+    handoff_off_[(size_t)r] = hsize;
+    hsize += (size_t)fronts_[(size_t)r].ns * fronts_[(size_t)r].ns;
+  }
+  handoff_.alloc(std::max<size_t>(hsize, 1));
+  for (size_t li = 0; li < lanes_.size(); ++li) {
+    Lane& L = *lanes_[li];
+    if (li > 0) {
+      HXG_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
+      L.own_stream = true;
+    }
+    HXG_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
+    cublas_check(cublasCreate(&L.cublas), "cublasCreate");
+    if (cusolverDnCreate(&L.cusolver) != CUSOLVER_STATUS_SUCCESS)
+      throw Error(HXG_ERR_CUDA, "cusolverDnCreate failed");
+    size_t mw = 1, mi = 1, mt = 1, mp = 1, mtd = 1, mth = 1, cur = 0, peak = 1;
+    std::vector<size_t> st;
+    for (int t : L.fronts) {
+      const Front& f = fronts_[(size_t)t];
+      const size_t m = (size_t)f.np + f.ns;
+      mw = std::max(mw, m * m);
+      mi = std::max(mi, (size_t)f.np * f.np);
+      mt = std::max(mt, (size_t)f.np * f.ns);
+      int lwork = 0;
+      if (cusolverDnDpotrf_bufferSize(L.cusolver, CUBLAS_FILL_MODE_LOWER, f.np, nullptr, (int)m,
+                                      &lwork) != CUSOLVER_STATUS_SUCCESS)
+        throw Error(HXG_ERR_CUDA, "potrf_bufferSize failed");
+      mp = std::max(mp, (size_t)lwork);
+      size_t wdev = 0, whost = 0;
+      if (cusolverDnXtrtri_bufferSize(L.cusolver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT,
+                                      f.np, CUDA_R_64F, nullptr, f.np, &wdev, &whost) !=
+          CUSOLVER_STATUS_SUCCESS)
+        throw Error(HXG_ERR_CUDA, "trtri_bufferSize failed");
+      mtd = std::max(mtd, wdev);
+      mth = std::max(mth, whost);
+      // private stack: children in this lane are popped, the front pushed
+      // (unless its update is handed over)
+      for (int q = 0; q < 2; ++q) {
+        const int c = f.child[q];
+        if (c >= 0 && lane_of_[(size_t)c] == (int)li && handoff_off_[(size_t)c] == (size_t)-1) {
+          cur -= st.back();
+          st.pop_back();
+        }
+      }
+      if (handoff_off_[(size_t)t] == (size_t)-1) {
+        st.push_back((size_t)f.ns * f.ns);
+        cur += st.back();
+        peak = std::max(peak, cur);
+      }
+    }
+    L.W.alloc(mw);
+    L.inv.alloc(mi);
+    L.tmp.alloc(mt);
+    L.potrf_ws.alloc(mp);
+    L.trtri_ws.alloc(mtd / sizeof(double) + 1);
+    L.trtri_host.resize(mth + 1);
+    L.stack.alloc(peak);
+  }
+}
+
+void NdCholesky::factor_front(int t, Lane& L, const CsrMatrix& a,
+                              std::vector<std::pair<size_t, int>>& stack) {
+  const Front& f = fronts_[(size_t)t];
+  const int m = f.np + f.ns;
+  cudaStream_t s = L.stream;
+  const double one = 1.0, minus_one = -1.0, zero = 0.0;
+  double* W = L.W.p;
+  HXG_CUDA(cudaMemsetAsync(W, 0, sizeof(double) * (size_t)m * m, s));
+  const long long na = (long long)(asm_begin_[(size_t)t + 1] - asm_begin_[(size_t)t]);
+  if (na > 0)
+    assemble_kernel<<<grid_for(na, 256), 256, 0, s>>>(asm_dst_.p + asm_begin_[(size_t)t],
+                                                      asm_src_.p + asm_begin_[(size_t)t], na,
+                                                      a.vals.p, W);
+  // Children's updates: handed-over buffers, else this lane's stack (child[1]
+  // above child[0]); extend-add in child order.
+  const double* up[2] = {nullptr, nullptr};
+  for (int q = 1; q >= 0; --q) {
+    const int c = f.child[q];
+    if (c < 0) continue;
+    if (handoff_off_[(size_t)c] != (size_t)-1) {
+      up[q] = handoff_.p + handoff_off_[(size_t)c];
+    } else {
+      up[q] = L.stack.p + stack.back().first;
+      stack.pop_back();
+    }
+  }
+  for (int q = 0; q < 2; ++q) {
+    const int c = f.child[q];
+    if (c < 0 || fronts_[(size_t)c].ns == 0) continue;
+    const int nsc = fronts_[(size_t)c].ns;
+    extend_add_kernel<<<grid_for((long long)nsc * nsc, 256), 256, 0, s>>>(
+        up[q], nsc, child_map_.p + f.map_off[q], W, m);
+  }
+  HXG_CUDA(cudaGetLastError());
+  // Dense partial factorization in inverse form, all level-3 work on FP64
+  // tensor-core GEMMs (the cuBLAS trsm kernels are not): L11 = potrf(A11);
+  // W = L11^-1 (trtri; the front's upper half is zero, so W's is too);
+  // L21 = A21 W^T; S = A22 - L21 L21^T (syrk); M = [W; L21 W] written
+  // straight into the factor.
+  if (cusolverDnDpotrf(L.cusolver, CUBLAS_FILL_MODE_LOWER, f.np, W, m, L.potrf_ws.p,
+                       (int)L.potrf_ws.n, info_.p + t) != CUSOLVER_STATUS_SUCCESS)
+    throw Error(HXG_ERR_CUDA, "potrf failed");
+  HXG_CUDA(cudaMemcpy2DAsync(L.inv.p, sizeof(double) * f.np, W, sizeof(double) * m,
+                             sizeof(double) * f.np, f.np, cudaMemcpyDeviceToDevice, s));
+  if (cusolverDnXtrtri(L.cusolver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, f.np, CUDA_R_64F,
+                       L.inv.p, f.np, L.trtri_ws.p, L.trtri_ws.n * sizeof(double),
+                       L.trtri_host.data(), L.trtri_host.size(),
+                       info_.p + fronts_.size() + t) != CUSOLVER_STATUS_SUCCESS)
+    throw Error(HXG_ERR_CUDA, "trtri failed");
+  double* Lp = L_.p + f.loff;
+  if (f.ns > 0) {
+    cublas_check(cublasDgemm(L.cublas, CUBLAS_OP_N, CUBLAS_OP_T, f.ns, f.np, f.np, &one, W + f.np,
+                             m, L.inv.p, f.np, &zero, L.tmp.p, f.ns),
+                 "gemm (L21)");
+    cublas_check(cublasDsyrk(L.cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, f.ns, f.np, &minus_one,
+                             L.tmp.p, f.ns, &one, W + f.np + (size_t)f.np * m, m),
+                 "syrk");
+    cublas_check(cublasDgemm(L.cublas, CUBLAS_OP_N, CUBLAS_OP_N, f.ns, f.np, f.np, &one, L.tmp.p,
+                             f.ns, L.inv.p, f.np, &zero, Lp + f.np, m),
+                 "gemm (L21 L11^-1)");
+  }
+  HXG_CUDA(cudaMemcpy2DAsync(Lp, sizeof(double) * m, L.inv.p, sizeof(double) * f.np,
+                             sizeof(double) * f.np, f.np, cudaMemcpyDeviceToDevice, s));
+  if (f.ns > 0) {
+    double* dst;
+    if (handoff_off_[(size_t)t] != (size_t)-1) {
+      dst = handoff_.p + handoff_off_[(size_t)t];
+    } else {
+      const size_t top = stack.empty() ? 0
+                                       : stack.back().first + (size_t)stack.back().second *
+                                                                  stack.back().second;
+      dst = L.stack.p + top;
+      stack.emplace_back(top, f.ns);
+    }
+    HXG_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * f.ns, W + f.np + (size_t)f.np * m,
+                               sizeof(double) * m, sizeof(double) * f.ns, f.ns,
+                               cudaMemcpyDeviceToDevice, s));
+  } else if (handoff_off_[(size_t)t] == (size_t)-1) {
+    const size_t top = stack.empty() ? 0
+                                     : stack.back().first + (size_t)stack.back().second *
+                                                                stack.back().second;
+    stack.emplace_back(top, 0);
+  }
+}
+
+void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s) {
+  if (!analyzed_) {
+    analyze(a, npd);
+    plan_lanes();
+  }
+  ready_ = false;
+  Lane& top = *lanes_[0];
+  top.stream = s;
+  for (auto& l : lanes_) {
+    cublasSetStream(l->cublas, l->stream);
+    cusolverDnSetStream(l->cusolver, l->stream);
+  }
+  HXG_CUDA(cudaMemsetAsync(info_.p, 0, 2 * sizeof(int) * fronts_.size(), s));
+  // The subtree lanes start after earlier work on the caller's stream.
+  HXG_CUDA(cudaEventRecord(top.done, s));
+  for (size_t li = 1; li < lanes_.size(); ++li)
+    HXG_CUDA(cudaStreamWaitEvent(lanes_[li]->stream, top.done, 0));
+  // Round-robin issue over the subtree lanes keeps every stream fed.
+  std::vector<std::vector<std::pair<size_t, int>>> stacks(lanes_.size());
+  std::vector<size_t> next(lanes_.size(), 0);
+  for (bool more = true; more;) {
+    more = false;
+    for (size_t li = 1; li < lanes_.size(); ++li) {
+      Lane& L = *lanes_[li];
+      if (next[li] < L.fronts.size()) {
+        factor_front(L.fronts[next[li]++], L, a, stacks[li]);
+        more = more || next[li] < L.fronts.size();
+      }
+    }
+  }
+  for (size_t li = 1; li < lanes_.size(); ++li) {
+    HXG_CUDA(cudaEventRecord(lanes_[li]->done, lanes_[li]->stream));
+    HXG_CUDA(cudaStreamWaitEvent(s, lanes_[li]->done, 0));
+  }
+  for (int t : top.fronts) factor_front(t, top, a, stacks[0]);
   std::vector<int> info(fronts_.size());
   HXG_CUDA(cudaMemcpyAsync(info.data(), info_.p, sizeof(int) * info.size(),
                            cudaMemcpyDeviceToHost, s));

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
+#include <memory>
+#include <utility>
 #include <vector>
 
 #include "coarse.hpp"
@@ -19,7 +21,7 @@ namespace hxg {
 
 class NdCholesky {
  public:
-  NdCholesky() = default;
+  NdCholesky();
   ~NdCholesky();
   NdCholesky(const NdCholesky&) = delete;
   NdCholesky& operator=(const NdCholesky&) = delete;
@@ -51,7 +53,7 @@ class NdCholesky {
   int n_ = 0;
   std::vector<Front> fronts_;           // postorder
   std::vector<std::vector<int>> levels_;  // fronts per depth
-  size_t lsize_ = 0, max_front_ = 0, max_update_ = 0;
+  size_t lsize_ = 0;
 
   // device
   DevBuf<int> perm_;         // new -> old DoF
@@ -60,15 +62,19 @@ class NdCholesky {
   DevBuf<long long> asm_dst_;  // assembly: destination offset in the front workspace
   DevBuf<int> asm_src_;      // assembly: CSR slot
   DevBuf<double> L_;         // factor panels
-  DevBuf<double> work_;      // current front (m x m)
-  DevBuf<double> inv_;       // L11^-1 scratch (np x np)
-  DevBuf<double> stack_;     // pending update matrices
+  struct Lane;
+  void plan_lanes();
+  void factor_front(int t, Lane& lane, const CsrMatrix& a,
+                    std::vector<std::pair<size_t, int>>& stack);
+  std::vector<std::unique_ptr<Lane>> lanes_;
+  std::vector<int> lane_of_;
+  std::vector<size_t> handoff_off_;  // subtree roots: offset of the handed-over update
+  DevBuf<double> handoff_;
   DevBuf<double> wvec_;      // solve work vector (new numbering)
   DevBuf<double> ubuf_;      // per-front update vectors (forward sweep)
   DevBuf<double> yvec_;      // per-front front vectors
   DevBuf<double> part_f_, part_b_;  // GEMV tile partial sums
   DevBuf<int> info_;
-  DevBuf<double> potrf_ws_;
   // Per-front solve metadata and the tile lists (see ndchol.cu).
   DevBuf<int> dfront_piv0_, dfront_np_, dfront_ns_, c0_, c1_, ftile0_, btile0_;
   DevBuf<long long> dfront_loff_, dfront_rows_off_, yoff_, uoff_;
@@ -77,8 +83,6 @@ class NdCholesky {
   // Per level: [begin, end) into the forward / backward / row / column tile lists.
   std::vector<int> lev_ft_, lev_bt_, lev_rt_, lev_ct_;
   std::vector<size_t> asm_begin_;  // per front range in the assembly lists
-  cublasHandle_t cublas_ = nullptr;
-  cusolverDnHandle_t cusolver_ = nullptr;
 };
 
 }  // namespace hxg
