@@ -43,7 +43,12 @@ constexpr int kGeoStride = 10;
 // shares one quadrature-data layout.
 __host__ __device__ constexpr int brick_x(int q) { return q == 2 ? 4 : q == 3 ? 4 : 2; }
 __host__ __device__ constexpr int brick_y(int q) { return q == 2 ? 4 : q == 3 ? 4 : 2; }
-__host__ __device__ constexpr int brick_z(int q) { return q == 2 ? 4 : q == 3 ? 2 : q == 4 ? 2 : 1; }
+#ifndef HXG_BRICK_Z3
+#define HXG_BRICK_Z3 2
+#endif
+__host__ __device__ constexpr int brick_z(int q) {
+  return q == 2 ? 4 : q == 3 ? HXG_BRICK_Z3 : q == 4 ? 2 : 1;
+}
 
 // Quadrature-data layout in HBM: brick-blocked structure-of-arrays so that
 // the thread owning column (element, qx, qy) reads one coalesced double per

@@ -37,6 +37,21 @@
 #ifndef HXG_SLOTS_Q2
 #define HXG_SLOTS_Q2 1
 #endif
+#ifndef HXG_MINB_Q4
+#define HXG_MINB_Q4 2
+#endif
+#ifndef HXG_SLOTS_Q4
+#define HXG_SLOTS_Q4 0
+#endif
+#ifndef HXG_NSG_Q2
+#define HXG_NSG_Q2 3
+#endif
+#ifndef HXG_NSH_Q2
+#define HXG_NSH_Q2 3
+#endif
+#ifndef HXG_STATE_PF
+#define HXG_STATE_PF 0  // software-pipelined state loads (needs register headroom)
+#endif
 #ifndef HXG_SLOTS_HIGHP
 #define HXG_SLOTS_HIGHP 0
 #endif
@@ -108,12 +123,12 @@ __host__ __device__ constexpr int pad_plane(int p, int q) {
 // Resident CTAs per SM the register allocation targets: two for the 9-warp
 // bricks; three for the 4-warp (3, 4) brick (shared memory allows it).
 __host__ __device__ constexpr int fused_min_blocks(int p, int q) {
-  return p * 10 + q == 34 ? HXG_MINB_HIGHP : p * 10 + q == 23 ? HXG_MINB_Q2 : 2;
+  return p * 10 + q == 34 ? HXG_MINB_HIGHP : p * 10 + q == 23 ? HXG_MINB_Q2 : p * 10 + q == 45 ? HXG_MINB_Q4 : 2;
 }
 // Column-private shared slots for the gradients (see P2).
 __host__ __device__ constexpr bool fused_slots(int p, int q) {
   return p * 10 + q == 12 || p * 10 + q == 13 || (HXG_SLOTS_Q2 && p * 10 + q == 23) ||
-         (HXG_SLOTS_HIGHP && (p * 10 + q == 34 || p * 10 + q == 45));
+         (HXG_SLOTS_HIGHP && p * 10 + q == 34) || (HXG_SLOTS_Q4 && p * 10 + q == 45);
 }
 
 template <int P, int Q>
@@ -420,10 +435,27 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
   // the two-CTA register cap), registers the remaining Q - N; elsewhere all Q
   // stay in registers (no spills there, and fewer shared accesses).  The slots are volatile so the compiler
   // does not forward them back into registers.
-  constexpr int NS = fused_slots(P, Q) ? N : 0;
-  constexpr int QR = Q - NS;
+  // NSG / NSH planes of the gradients / q-function outputs live in the
+  // slots, the rest in registers.
+  constexpr int NSG = fused_slots(P, Q) ? (P * 10 + Q == 23 ? HXG_NSG_Q2 : N) : 0;
+  constexpr int NSH = fused_slots(P, Q) ? (P * 10 + Q == 23 ? HXG_NSH_Q2 : N) : 0;
+  constexpr int QR = Q - NSG, QH = Q - NSH;
   volatile double* slot = S + te;
   double g[3][3][QR > 0 ? QR : 1];
+  double hr[3][3][QH > 0 ? QH : 1];
+  const double* sp0 = st_brick + tid;
+  const unsigned long long pol_stream = policy_evict_first();
+#if HXG_STATE_PF
+  // plane 0's state requested before the z pass; plane qz+1's before the
+  // q-function of plane qz
+  double stn[kStateStride];
+  auto load_state = [&](int qz) {
+    const double* sp = sp0 + qz * T * kStateStride;
+#pragma unroll
+    for (int s = 0; s < kStateStride; ++s) stn[s] = valid ? ld_stream(sp + s * T, pol_stream) : 0.0;
+  };
+  load_state(0);
+#endif
   auto gslot = [&](int c, int d, int z) { return ((c * 3 + d) * N + z) * Q2; };
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -443,25 +475,30 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
         gy += prm.B[z * N + k] * tdy[k];
         gz += prm.Bd[z * N + k] * tb[k];
       }
-      if (z < NS) {
+      if (z < NSG) {
         slot[gslot(c, 0, z)] = gx;
         slot[gslot(c, 1, z)] = gy;
         slot[gslot(c, 2, z)] = gz;
       } else {
-        g[c][0][z - NS] = gx;
-        g[c][1][z - NS] = gy;
-        g[c][2][z - NS] = gz;
+        g[c][0][z - NSG] = gx;
+        g[c][1][z - NSG] = gy;
+        g[c][2][z - NSG] = gz;
       }
     }
   }
 
   // ---- q-function on the streamed state --------------------------------
-  const double* sp0 = st_brick + tid;
-  const unsigned long long pol_stream = policy_evict_first();
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
     double H[9];
+#if HXG_STATE_PF
+    double st[kStateStride];
+#pragma unroll
+    for (int s = 0; s < kStateStride; ++s) st[s] = stn[s];
+    if (qz + 1 < Q) load_state(qz + 1);
+#endif
     if (valid) {
+#if !HXG_STATE_PF
       double st[kStateStride];
       const double* sp = sp0 + qz * T * kStateStride;
 #pragma unroll
@@ -472,12 +509,13 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
         st[s] = ld_stream(sp + s * T, pol_stream);
 #endif
       }
+#endif
       double G[9];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int d = 0; d < 3; ++d)
-          G[3 * c + d] = qz < NS ? slot[gslot(c, d, qz)] : g[c][d][qz - NS];
+          G[3 * c + d] = qz < NSG ? slot[gslot(c, d, qz)] : g[c][d][qz - NSG];
 #if HXG_EXPERIMENT == 2
       // timing experiment: trivial q-function (state still loaded)
 #pragma unroll
@@ -497,10 +535,10 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
     for (int c = 0; c < 3; ++c)
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        if (qz < NS)
+        if (qz < NSH)
           slot[gslot(c, d, qz)] = H[3 * c + d];
         else
-          g[c][d][qz - NS] = H[3 * c + d];
+          hr[c][d][qz - NSH] = H[3 * c + d];
       }
   }
   HXG_PHASE(2);
@@ -514,7 +552,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
-      for (int z = 0; z < Q; ++z) h[d][z] = z < NS ? slot[gslot(c, d, z)] : g[c][d][z - NS];
+      for (int z = 0; z < Q; ++z) h[d][z] = z < NSH ? slot[gslot(c, d, z)] : hr[c][d][z - NSH];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       double r0 = 0.0, r1 = 0.0, r2 = 0.0;
