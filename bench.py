@@ -372,6 +372,29 @@ def run_ours(args, rank, world, local_rank):
                   "coarse_solver": "nested-dissection multifrontal Cholesky (device, inverse-panel solve)"}
         pmg = [nk] + [pmg_case(o, c, False) for o, c in ((3, 43), (4, 32))]
 
+    # Full Newton solve of the compressed beam (BASELINE.json configs[3] on one
+    # GPU): FemProblem::solve with load continuation (1 step), critical-point
+    # line search, p-MG rebuilt at every Newton iterate; device-timed.
+    newton_full = None
+    if world == 1 and not args.no_newton:
+        prob_b = FemProblem(extents=(2.0, 1.0, 1.0), cells=(96, 48, 48), order=2,
+                            fixed_faces=("-x",), traction_face="+x", traction=(-0.02, 0.0, 0.0))
+        eb = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        torch.cuda.synchronize()
+        eb[0].record(stream)
+        rep_b = prob_b.solve(load_steps=1)
+        eb[1].record(stream)
+        torch.cuda.synchronize()
+        newton_full = {"config": "Q2 beam (96, 48, 48) cells, extents (2,1,1), fixed -x, traction "
+                                 "(-0.02,0,0) on +x, 1 load step, critical-point line search",
+                       "dofs": prob_b.size(), "solve_ms": eb[0].elapsed_time(eb[1]),
+                       "newton_iterations": rep_b["newton_iterations"],
+                       "cg_iterations": rep_b["cg_iterations"],
+                       "final_fnorm": rep_b["final_fnorm"], "converged": rep_b["converged"],
+                       "note": "includes the symbolic (first) p-MG setup"}
+        del prob_b, rep_b
+        torch.cuda.empty_cache()
+
     # Slab-partitioned p-MG PCG on the compressed beam (BASELINE.json
     # configs[3]: Q2, 96 x 48 x 48 cells over N GPUs, strong scaling; halo
     # exchange over NCCL, replicated coarse Cholesky), device-timed, max over
@@ -419,6 +442,7 @@ def run_ours(args, rank, world, local_rank):
             "newton_krylov_step": newton,
             "pmg_solves": pmg,
             "pmg_distributed": pmg_dist,
+            "newton_solve": newton_full,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -40,7 +40,8 @@ enum {
   HXG_ERR_INVALID_SMOOTHER = 6,   /* InvalidSmootherError      errors.hpp:62   */
   HXG_ERR_INVALID_ARGUMENT = 7,   /* std::invalid_argument (size mismatch etc.) */
   HXG_ERR_CUDA = 8,
-  HXG_ERR_UNSUPPORTED = 9
+  HXG_ERR_UNSUPPORTED = 9,
+  HXG_ERR_STEP_REJECTED = 10      /* StepRejectedError         errors.hpp       */
 };
 
 typedef struct {
@@ -197,6 +198,48 @@ typedef struct {
 int hxg_cg_solve(hxg_op_t op, hxg_mg_t mg, int precond, const double* b, double* x, double rtol,
                  int max_iterations, hxg_cg_report* report, double* history_host,
                  int history_capacity);
+
+/* Nonlinear driver (nonlinear.hpp): NewtonConfig (:16-24), IterationRecord
+ * (:26-36), SolveReport (:50-56).  reference_line_search_quirk = 1 reproduces
+ * the reference's functor-copy defect (residual read as zero after a line
+ * search); 0 runs the intended algorithm. */
+typedef struct {
+  int max_iterations;
+  double rtol, atol, linear_rtol;
+  int linear_max_iterations;
+  int use_line_search;
+  int load_steps;
+  int reference_line_search_quirk;
+} hxg_newton_config;
+typedef struct {
+  int load_step;
+  double time;
+  int iteration;
+  double fnorm, fnorm_rel;
+  int cg_iterations, cg_converged;
+  double condition_estimate, alpha;
+} hxg_iteration_record;
+typedef struct {
+  int converged;
+  int load_steps_taken;
+  int newton_iterations;
+  int cg_iterations;
+  double final_fnorm;
+  int num_records; /* records written (<= capacity) */
+} hxg_solve_report;
+/* The reference defaults (config.hpp:55-61). */
+int hxg_newton_config_default(hxg_newton_config* cfg);
+/* newton_solve (nonlinear.hpp:162-216) from the device iterate u (updated in
+ * place); the p-MG hierarchy is set up at every linearisation point. */
+int hxg_newton_solve(hxg_op_t op, hxg_mg_t mg, const hxg_newton_config* cfg, double* u,
+                     int load_step, double time, hxg_solve_report* report,
+                     hxg_iteration_record* records, int capacity);
+/* FemProblem::solve (problem.hpp:118-127): load_continuation
+ * (nonlinear.hpp:325-366) from u = 0 over cfg->load_steps, whole-face zero
+ * Dirichlet values; u (device) receives the solution. */
+int hxg_solve_continuation(hxg_op_t op, hxg_mg_t mg, const hxg_newton_config* cfg, double* u,
+                           int max_bisections, hxg_solve_report* report,
+                           hxg_iteration_record* records, int capacity);
 
 /* estimate_lambda_max (cg.hpp:152-184) of D^-1 A on `op` with rough_seed. */
 int hxg_lambda_max_jacobi(hxg_op_t op, int iterations, double* out);

@@ -23,6 +23,7 @@ ERR_INVALID_SMOOTHER = 6
 ERR_INVALID_ARGUMENT = 7
 ERR_CUDA = 8
 ERR_UNSUPPORTED = 9
+ERR_STEP_REJECTED = 10
 
 
 class HxgErrorStruct(ctypes.Structure):
@@ -58,16 +59,43 @@ class InvalidSmootherError(HxgError):
     pass
 
 
+class StepRejectedError(HxgError):
+    pass
+
+
 _CLASSES = {ERR_INVERTED_ELEMENT: InvertedElementError,
             ERR_STATE_NOT_INITIALIZED: StateNotInitializedError,
             ERR_INDEFINITE: IndefiniteOperatorError, ERR_NOT_SPD: NotSpdError,
-            ERR_INVALID_SMOOTHER: InvalidSmootherError}
+            ERR_INVALID_SMOOTHER: InvalidSmootherError, ERR_STEP_REJECTED: StepRejectedError}
 
 
 class CgReport(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int), ("converged", ctypes.c_int),
                 ("eig_min", ctypes.c_double), ("eig_max", ctypes.c_double),
                 ("initial_natural_norm", ctypes.c_double), ("final_natural_norm", ctypes.c_double)]
+
+
+class NewtonConfig(ctypes.Structure):
+    """NewtonConfig (nonlinear.hpp:16-24) + the line-search quirk switch."""
+    _fields_ = [("max_iterations", ctypes.c_int), ("rtol", ctypes.c_double),
+                ("atol", ctypes.c_double), ("linear_rtol", ctypes.c_double),
+                ("linear_max_iterations", ctypes.c_int), ("use_line_search", ctypes.c_int),
+                ("load_steps", ctypes.c_int), ("reference_line_search_quirk", ctypes.c_int)]
+
+
+class IterationRecord(ctypes.Structure):
+    """IterationRecord (nonlinear.hpp:26-36)."""
+    _fields_ = [("load_step", ctypes.c_int), ("time", ctypes.c_double),
+                ("iteration", ctypes.c_int), ("fnorm", ctypes.c_double),
+                ("fnorm_rel", ctypes.c_double), ("cg_iterations", ctypes.c_int),
+                ("cg_converged", ctypes.c_int), ("condition_estimate", ctypes.c_double),
+                ("alpha", ctypes.c_double)]
+
+
+class SolveReport(ctypes.Structure):
+    _fields_ = [("converged", ctypes.c_int), ("load_steps_taken", ctypes.c_int),
+                ("newton_iterations", ctypes.c_int), ("cg_iterations", ctypes.c_int),
+                ("final_fnorm", ctypes.c_double), ("num_records", ctypes.c_int)]
 
 
 class OpDesc(ctypes.Structure):
@@ -129,6 +157,9 @@ SIGNATURES = {
     "hxg_chol_destroy": [_vp],
     "hxg_cg_solve": [_vp, _vp, _i, _vp, _vp, _d, _i, _vp, _vp, _i],
     "hxg_lambda_max_jacobi": [_vp, _i, _P(_d)],
+    "hxg_newton_config_default": [_vp],
+    "hxg_newton_solve": [_vp, _vp, _vp, _vp, _i, _d, _vp, _vp, _i],
+    "hxg_solve_continuation": [_vp, _vp, _vp, _vp, _i, _vp, _vp, _i],
     "hxg_dot": [_vp, _vp, _i64, _vp, _P(_d)],
     "hxg_malloc": [_vp, _sz],
     "hxg_free": [_vp],

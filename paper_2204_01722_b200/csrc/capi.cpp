@@ -465,3 +465,69 @@ int hxg_chol_solve(hxg_chol_t h, const double* b, double* x) {
 int hxg_chol_destroy(hxg_chol_t h) {
   return guarded([&] { delete h; });
 }
+
+namespace {
+hxg::NewtonConfig to_config(const hxg_newton_config* c) {
+  hxg::NewtonConfig nc;
+  if (c) {
+    nc.max_iterations = c->max_iterations;
+    nc.rtol = c->rtol;
+    nc.atol = c->atol;
+    nc.linear_rtol = c->linear_rtol;
+    nc.linear_max_iterations = c->linear_max_iterations;
+    nc.use_line_search = c->use_line_search != 0;
+    nc.load_steps = c->load_steps;
+    nc.reference_line_search_quirk = c->reference_line_search_quirk != 0;
+  }
+  return nc;
+}
+void fill_report(const std::vector<hxg::SolveReport>& steps, bool converged,
+                 hxg_solve_report* rep, hxg_iteration_record* recs, int cap) {
+  if (!rep) return;
+  *rep = hxg_solve_report{};
+  rep->converged = converged ? 1 : 0;
+  rep->load_steps_taken = (int)steps.size();
+  int k = 0;
+  for (const auto& s : steps) {
+    rep->newton_iterations += s.iterations;
+    rep->cg_iterations += s.total_cg_iterations;
+    rep->final_fnorm = s.final_fnorm;
+    for (const auto& r : s.records) {
+      if (recs && k < cap)
+        recs[k++] = hxg_iteration_record{r.load_step, r.time, r.iteration, r.fnorm, r.fnorm_rel,
+                                         r.cg_iterations, r.cg_converged ? 1 : 0,
+                                         r.condition_estimate, r.alpha};
+    }
+  }
+  rep->num_records = k;
+}
+}  // namespace
+
+int hxg_newton_config_default(hxg_newton_config* cfg) {
+  return guarded([&] {
+    if (!cfg) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "null config");
+    hxg::NewtonConfig d;
+    *cfg = hxg_newton_config{d.max_iterations, d.rtol, d.atol, d.linear_rtol,
+                             d.linear_max_iterations, d.use_line_search ? 1 : 0, d.load_steps,
+                             d.reference_line_search_quirk ? 1 : 0};
+  });
+}
+
+int hxg_newton_solve(hxg_op_t op, hxg_mg_t mg, const hxg_newton_config* cfg, double* u,
+                     int load_step, double time, hxg_solve_report* report,
+                     hxg_iteration_record* records, int capacity) {
+  return guarded([&] {
+    auto r = hxg::newton_solve(OP(op), MG(mg), to_config(cfg), u, load_step, time);
+    const bool conv = r.converged;
+    fill_report({r}, conv, report, records, capacity);
+  });
+}
+
+int hxg_solve_continuation(hxg_op_t op, hxg_mg_t mg, const hxg_newton_config* cfg, double* u,
+                           int max_bisections, hxg_solve_report* report,
+                           hxg_iteration_record* records, int capacity) {
+  return guarded([&] {
+    auto steps = hxg::solve_continuation(OP(op), MG(mg), to_config(cfg), u, max_bisections, nullptr);
+    fill_report(steps, true, report, records, capacity);
+  });
+}

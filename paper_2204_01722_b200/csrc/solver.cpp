@@ -6,7 +6,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <limits>
 #include <random>
+#include <string>
 
 namespace hxg {
 
@@ -360,6 +362,185 @@ void Hierarchy::cycle(int k, const double* b, double* x, bool x_zero) {
   else
     vadd(x, r, n, s);
   for (int i = 0; i < post_; ++i) lv.smoother.apply(op, b, x, false);
+}
+
+}  // namespace hxg
+
+namespace hxg {
+
+namespace {
+
+// critical_point_line_search (nonlinear.hpp:77-129): one secant step on
+// g(a) = F(u + a du)^T du from g(0), g(1), clamped to [0.1, 2]; non-finite
+// samples halve the trial point up to five times.
+struct LineSearch {
+  double alpha = 1.0;
+};
+LineSearch critical_point_line_search(const std::function<double(double)>& g_eval, double g0) {
+  constexpr int kMaxHalvings = 5;
+  double trial = 1.0;
+  double g1 = g_eval(trial);
+  int halvings = 0;
+  while (!std::isfinite(g1) && halvings < kMaxHalvings) {
+    trial *= 0.5;
+    g1 = g_eval(trial);
+    ++halvings;
+  }
+  if (!std::isfinite(g1))
+    throw Error(HXG_ERR_STEP_REJECTED, "residual not evaluable along the search direction");
+  double alpha;
+  if (g0 >= 0.0) {
+    alpha = trial;  // ascent warning
+  } else if (g1 == g0) {
+    alpha = trial;  // degenerate secant
+  } else {
+    alpha = trial * g0 / (g0 - g1);
+    alpha = std::clamp(alpha, 0.1, 2.0);
+    if (halvings > 0) alpha = std::min(alpha, trial);
+  }
+  LineSearch res;
+  if (alpha == trial) {
+    res.alpha = alpha;
+    return res;
+  }
+  double ga = g_eval(alpha);
+  while (!std::isfinite(ga) && halvings < kMaxHalvings) {
+    alpha *= 0.5;
+    ga = g_eval(alpha);
+    ++halvings;
+  }
+  if (!std::isfinite(ga))
+    throw Error(HXG_ERR_STEP_REJECTED, "residual not evaluable at the line search result");
+  res.alpha = alpha;
+  return res;
+}
+
+}  // namespace
+
+SolveReport newton_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, double* u,
+                         int load_step, double time) {
+  const long long n = op.size();
+  cudaStream_t s = op.stream();
+  DevBuf<double> f((size_t)n), rhs((size_t)n), du((size_t)n), ut((size_t)n), ft((size_t)n);
+  DotWorkspace ws;
+  auto norm2 = [&](const double* v) { return std::sqrt(dot(v, v, n, ws, s)); };
+  op.apply_residual(u, f.p);
+  const double fnorm0 = norm2(f.p);
+  SolveReport report;
+  if (fnorm0 <= cfg.atol) {
+    report.converged = true;
+    report.final_fnorm = fnorm0;
+    return report;
+  }
+  DevOp jac = [&op](const double* x, double* y) { op.apply_jacobian(x, y); };
+  DevOp pre = [&mg, n, s](const double* r, double* z) {
+    vzero(z, n, s);
+    mg.v_cycle(r, z, true);
+  };
+  // g(a) = F(u + a du)^T du; F of the last evaluation stays in ft (and the
+  // quadrature state at u + a du).  Inverted elements read as NaN.
+  auto g_eval = [&](double a) {
+    vwaxpy(ut.p, u, a, du.p, n, s);
+    try {
+      op.apply_residual(ut.p, ft.p);
+    } catch (const Error& e) {
+      if (e.code != HXG_ERR_INVERTED_ELEMENT) throw;
+      return std::numeric_limits<double>::quiet_NaN();
+    }
+    const double g = dot(ft.p, du.p, n, ws, s);
+    return std::isfinite(g) ? g : std::numeric_limits<double>::quiet_NaN();
+  };
+  double fnorm = fnorm0;
+  for (int it = 1; it <= cfg.max_iterations; ++it) {
+    mg.setup_numeric();
+    vneg(rhs.p, f.p, n, s);
+    vzero(du.p, n, s);
+    CgResult cg = cg_solve(n, jac, pre, rhs.p, du.p, cfg.linear_rtol, cfg.linear_max_iterations, s);
+    IterationRecord rec;
+    rec.load_step = load_step;
+    rec.time = time;
+    rec.iteration = it;
+    rec.cg_iterations = cg.iterations;
+    rec.cg_converged = cg.converged;
+    rec.condition_estimate = cg.eig_min > 0.0 ? cg.eig_max / cg.eig_min : 0.0;
+    report.total_cg_iterations += cg.iterations;
+    if (cfg.use_line_search) {
+      rec.alpha = critical_point_line_search(g_eval, dot(f.p, du.p, n, ws, s)).alpha;
+    } else {
+      if (!std::isfinite(g_eval(1.0)))
+        throw Error(HXG_ERR_STEP_REJECTED, "residual not evaluable at the full Newton step");
+      rec.alpha = 1.0;
+    }
+    vwaxpy(u, u, rec.alpha, du.p, n, s);
+    // The search's last evaluation was at the accepted point.
+    if (cfg.use_line_search && cfg.reference_line_search_quirk)
+      vzero(f.p, n, s);
+    else
+      vcopy(f.p, ft.p, n, s);
+    fnorm = norm2(f.p);
+    rec.fnorm = fnorm;
+    rec.fnorm_rel = fnorm / fnorm0;
+    report.records.push_back(rec);
+    report.iterations = it;
+    if (fnorm <= std::max(cfg.rtol * fnorm0, cfg.atol)) {
+      report.converged = true;
+      break;
+    }
+  }
+  // Leave the quadrature state at the accepted iterate.
+  op.apply_residual(u, f.p);
+  report.final_fnorm = norm2(f.p);
+  return report;
+}
+
+std::vector<SolveReport> solve_continuation(Operator& op, Hierarchy& mg, const NewtonConfig& cfg,
+                                            double* u, int max_bisections,
+                                            std::vector<double>* times) {
+  if (cfg.load_steps < 1 || cfg.max_iterations < 1 || cfg.rtol <= 0 || cfg.atol <= 0 ||
+      cfg.linear_rtol <= 0)
+    throw Error(HXG_ERR_INVALID_ARGUMENT, "solver tolerances must be positive and counts >= 1");
+  const long long n = op.size();
+  cudaStream_t s = op.stream();
+  DevBuf<double> saved((size_t)n);
+  vzero(u, n, s);  // FemProblem::solve starts from zero (problem.hpp:119)
+  vcopy(saved.p, u, n, s);
+  std::vector<SolveReport> steps;
+  double t_done = 0.0;
+  for (int step = 1; step <= cfg.load_steps; ++step) {
+    const double target = (double)step / cfg.load_steps;
+    int bisections = 0;
+    double t_try = target;
+    while (true) {
+      op.set_load_scale(t_try);  // set_time (problem.hpp:70-73)
+      vcopy(u, saved.p, n, s);
+      // impose_dirichlet: whole-face zero values (u = t * 0 on the mask)
+      vmask_zero(u, op.mask(), n, s);
+      bool ok = false;
+      try {
+        SolveReport r = newton_solve(op, mg, cfg, u, step, t_try);
+        ok = r.converged;
+        if (ok) {
+          steps.push_back(std::move(r));
+          if (times) times->push_back(t_try);
+        }
+      } catch (const Error& e) {
+        if (e.code != HXG_ERR_STEP_REJECTED && e.code != HXG_ERR_INVERTED_ELEMENT) throw;
+        ok = false;
+      }
+      if (ok) {
+        t_done = t_try;
+        vcopy(saved.p, u, n, s);
+        if (t_try == target) break;
+        t_try = target;
+      } else {
+        if (++bisections > max_bisections)
+          throw Error(HXG_ERR_STEP_REJECTED,
+                      "load step failed after " + std::to_string(max_bisections) + " bisections");
+        t_try = 0.5 * (t_done + t_try);
+      }
+    }
+  }
+  return steps;
 }
 
 }  // namespace hxg

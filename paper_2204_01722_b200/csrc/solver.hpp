@@ -90,4 +90,43 @@ class Hierarchy {
   int pre_ = 1, post_ = 1, degree_ = 2, coarse_mode_ = 0;
 };
 
+// Nonlinear driver (nonlinear.hpp): Newton-CG with the critical-point line
+// search and load continuation, on device vectors.
+struct NewtonConfig {  // nonlinear.hpp:16-24
+  int max_iterations = 50;
+  double rtol = 1e-8, atol = 1e-10, linear_rtol = 1e-3;
+  int linear_max_iterations = 500;
+  bool use_line_search = true;
+  int load_steps = 1;
+  // Reproduce the reference's functor-copy defect:
+  // after a line search the residual is read from the un-invoked original
+  // evaluator, i.e. zero.  Off by default (the intended algorithm).
+  bool reference_line_search_quirk = false;
+};
+struct IterationRecord {  // nonlinear.hpp:26-36
+  int load_step = 0;
+  double time = 1.0;
+  int iteration = 0;
+  double fnorm = 0.0, fnorm_rel = 0.0;
+  int cg_iterations = 0;
+  bool cg_converged = true;
+  double condition_estimate = 0.0, alpha = 1.0;
+};
+struct SolveReport {  // nonlinear.hpp:50-56
+  bool converged = false;
+  int iterations = 0, total_cg_iterations = 0;
+  double final_fnorm = 0.0;
+  std::vector<IterationRecord> records;
+};
+// newton_solve (nonlinear.hpp:162-216) on op's residual / Jacobian with the
+// p-MG V-cycle rebuilt at every linearisation point.
+SolveReport newton_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, double* u,
+                         int load_step, double time);
+// FemProblem::solve (problem.hpp:118-127): load_continuation
+// (nonlinear.hpp:325-366) over t_k = k / load_steps with whole-face zero
+// Dirichlet values; returns the per-step reports.
+std::vector<SolveReport> solve_continuation(Operator& op, Hierarchy& mg, const NewtonConfig& cfg,
+                                            double* u, int max_bisections,
+                                            std::vector<double>* times);
+
 }  // namespace hxg

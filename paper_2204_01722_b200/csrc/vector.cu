@@ -108,6 +108,13 @@ __global__ void k_cheb_step(double* x, double* r, double* d, const double* b, co
   }
 }
 
+__global__ void k_waxpy(double* w, const double* x, double a, const double* y, long long n) {
+  GRID_STRIDE(i, n) { w[i] = x[i] + a * y[i]; }
+}
+__global__ void k_neg(double* y, const double* x, long long n) {
+  GRID_STRIDE(i, n) { y[i] = -x[i]; }
+}
+
 }  // namespace
 
 DotWorkspace::DotWorkspace() {
@@ -151,6 +158,12 @@ void vmask_copy(double* y, const double* src, const uint8_t* m, long long n, cud
 }
 void vadd(double* y, const double* x, long long n, cudaStream_t s) {
   k_add<<<grid(n), 256, 0, s>>>(y, x, n);
+}
+void vwaxpy(double* w, const double* x, double a, const double* y, long long n, cudaStream_t s) {
+  k_waxpy<<<grid(n), 256, 0, s>>>(w, x, a, y, n);
+}
+void vneg(double* y, const double* x, long long n, cudaStream_t s) {
+  k_neg<<<grid(n), 256, 0, s>>>(y, x, n);
 }
 void vscale_mul(double* y, const double* a, const double* x, long long n, cudaStream_t s) {
   k_mul<<<grid(n), 256, 0, s>>>(y, a, x, n);

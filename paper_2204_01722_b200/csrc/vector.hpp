@@ -34,6 +34,10 @@ void vmask_zero(double* y, const uint8_t* mask, long long n, cudaStream_t s);
 void vmask_copy(double* y, const double* src, const uint8_t* mask, long long n, cudaStream_t s);
 // y += x
 void vadd(double* y, const double* x, long long n, cudaStream_t s);
+// w = x + a y
+void vwaxpy(double* w, const double* x, double a, const double* y, long long n, cudaStream_t s);
+// y = -x
+void vneg(double* y, const double* x, long long n, cudaStream_t s);
 // y = a * x
 void vscale_mul(double* y, const double* a, const double* x, long long n, cudaStream_t s);
 // y[i] = 1 / d[i]; returns false (after sync) if any d[i] == 0.

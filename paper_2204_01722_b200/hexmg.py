@@ -382,6 +382,42 @@ def cg_solve(op: MatrixFreeOperator, b, x=None, rtol=1e-8, max_iterations=500,
                 history=hist[: rep.iterations + 1].copy())
 
 
+def newton_config(**overrides) -> capi.NewtonConfig:
+    """NewtonConfig with the reference defaults (config.hpp:55-61) and
+    keyword overrides (max_iterations, rtol, atol, linear_rtol,
+    linear_max_iterations, use_line_search, load_steps,
+    reference_line_search_quirk)."""
+    cfg = capi.NewtonConfig()
+    check(lib().hxg_newton_config_default(ctypes.byref(cfg)))
+    for k, v in overrides.items():
+        if not hasattr(cfg, k):
+            raise TypeError(f"unknown Newton option {k}")
+        setattr(cfg, k, int(v) if isinstance(v, bool) else v)
+    return cfg
+
+
+def _report(rep, recs):
+    keys = [f[0] for f in capi.IterationRecord._fields_]
+    return dict(converged=bool(rep.converged), load_steps=rep.load_steps_taken,
+                newton_iterations=rep.newton_iterations, cg_iterations=rep.cg_iterations,
+                final_fnorm=rep.final_fnorm,
+                records=[{k: getattr(recs[i], k) for k in keys} for i in range(rep.num_records)])
+
+
+def newton_solve(op: MatrixFreeOperator, mg: MultigridHierarchy, u, load_step=0, time=1.0,
+                 **config):
+    """newton_solve (nonlinear.hpp:162-216) on device vector u (updated in place)."""
+    u = _dev(u, op.size())
+    cfg = newton_config(**config)
+    rep = capi.SolveReport()
+    recs = (capi.IterationRecord * 512)()
+    check(lib().hxg_newton_solve(op.h, mg.h, ctypes.byref(cfg), _ptr(u), int(load_step),
+                                 float(time), ctypes.byref(rep), recs, 512))
+    out = _report(rep, recs)
+    out["u"] = u
+    return out
+
+
 class FemProblem:
     """The configured pieces of FemProblem (problem.hpp:19-58): box mesh,
     basis on q Gauss-Legendre points, geometry, whole-face Dirichlet sets,
@@ -407,6 +443,20 @@ class FemProblem:
 
     def size(self):
         return self.op.size()
+
+    def solve(self, max_bisections=3, **config):
+        """FemProblem::solve (problem.hpp:118-127): Newton with load
+        continuation from u = 0; returns the report with the solution u."""
+        u = torch.zeros(self.size(), dtype=torch.float64, device="cuda")
+        cfg = newton_config(**config)
+        rep = capi.SolveReport()
+        recs = (capi.IterationRecord * 2048)()
+        check(lib().hxg_solve_continuation(self.op.h, self.hierarchy.h, ctypes.byref(cfg),
+                                           _ptr(u), int(max_bisections), ctypes.byref(rep),
+                                           recs, 2048))
+        out = _report(rep, recs)
+        out["u"] = u
+        return out
 
     @property
     def hierarchy(self) -> MultigridHierarchy:
