@@ -19,6 +19,7 @@
 #include "ndchol.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <functional>
 
 #include "dispatch.hpp"
@@ -28,7 +29,8 @@ namespace hxg {
 namespace {
 
 constexpr int kLeafNodes = 128;
-constexpr int kLaneDepth = 4;  // 16 concurrent subtree lanes in the factorization
+constexpr int kLaneDepth = 4;
+constexpr int kCholBase = 256;  // cuSOLVER potrf / trtri below this block size  // 16 concurrent subtree lanes in the factorization
 
 __global__ void assemble_kernel(const long long* __restrict__ dst, const int* __restrict__ src,
                                 long long n, const double* __restrict__ vals, double* front) {
@@ -46,6 +48,18 @@ __global__ void extend_add_kernel(const double* __restrict__ U, int ns,
     const int c = (int)(e / ns), r = (int)(e % ns);
     if (r < c) continue;
     work[map[r] + (long long)map[c] * m] += U[e];
+  }
+}
+
+__global__ void accumulate_info(int* dst, const int* src) {
+  if (*src != 0 && *dst == 0) *dst = *src;
+}
+__global__ void zero_strict_upper(double* W, int ldw, int n) {
+  const long long total = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n), r = (int)(e % n);
+    if (r < c) W[r + (size_t)c * ldw] = 0.0;
   }
 }
 
@@ -466,7 +480,8 @@ struct NdCholesky::Lane {
   cudaEvent_t done = nullptr;
   cublasHandle_t cublas = nullptr;
   cusolverDnHandle_t cusolver = nullptr;
-  DevBuf<double> W, inv, tmp, potrf_ws, trtri_ws, stack;
+  DevBuf<double> W, inv, tmp, potrf_ws, trtri_ws, stack, rscr;
+  DevBuf<int> info;  // base-block potrf / trtri status
   std::vector<char> trtri_host;
   std::vector<int> fronts;  // postorder
   bool own_stream = false;
@@ -563,7 +578,57 @@ void NdCholesky::plan_lanes() {
     L.trtri_ws.alloc(mtd / sizeof(double) + 1);
     L.trtri_host.resize(mth + 1);
     L.stack.alloc(peak);
+    // recursion scratch n2 x n1 <= np^2 / 4 + 16 np
+    L.rscr.alloc(mi / 4 + 32 * (size_t)std::sqrt((double)mi) + 1024);
+    L.info.alloc(2);
   }
+}
+
+// Recursive blocked Cholesky that also forms the inverse factor, with all
+// the level-3 work on tensor-core GEMM / SYRK:
+//   [A11 .; A21 A22]:  (L11, W11) = rec(A11);  L21 = A21 W11^T;
+//   S = A22 - L21 L21^T;  (L22, W22) = rec(S);  W21 = -W22 (L21 W11).
+// A (lower, leading dimension lda) is overwritten by L; W (zeroed upper
+// part, ldw) receives L^-1.  Blocks of <= kCholBase use cuSOLVER potrf +
+// trtri; a failed pivot block records its info in *info.
+void NdCholesky::chol_inv(Lane& L, double* A, int lda, double* W, int ldw, int n, int* info) {
+  cudaStream_t s = L.stream;
+  if (n <= kCholBase) {
+    if (cusolverDnDpotrf(L.cusolver, CUBLAS_FILL_MODE_LOWER, n, A, lda, L.potrf_ws.p,
+                         (int)L.potrf_ws.n, L.info.p) != CUSOLVER_STATUS_SUCCESS)
+      throw Error(HXG_ERR_CUDA, "potrf failed");
+    accumulate_info<<<1, 1, 0, s>>>(info, L.info.p);
+    HXG_CUDA(cudaMemcpy2DAsync(W, sizeof(double) * ldw, A, sizeof(double) * lda,
+                               sizeof(double) * n, n, cudaMemcpyDeviceToDevice, s));
+    zero_strict_upper<<<grid_for((long long)n * n, 256), 256, 0, s>>>(W, ldw, n);
+    if (cusolverDnXtrtri(L.cusolver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F,
+                         W, ldw, L.trtri_ws.p, L.trtri_ws.n * sizeof(double),
+                         L.trtri_host.data(), L.trtri_host.size(), L.info.p + 1) !=
+        CUSOLVER_STATUS_SUCCESS)
+      throw Error(HXG_ERR_CUDA, "trtri failed");
+    return;
+  }
+  const double one = 1.0, minus_one = -1.0, zero = 0.0;
+  const int n1 = ((n / 2 + 31) / 32) * 32, n2 = n - n1;
+  double *A21 = A + n1, *A22 = A + n1 + (size_t)n1 * lda;
+  double *W21 = W + n1, *W22 = W + n1 + (size_t)n1 * ldw;
+  chol_inv(L, A, lda, W, ldw, n1, info);
+  double* T = L.rscr.p;  // n2 x n1 scratch
+  cublas_check(cublasDgemm(L.cublas, CUBLAS_OP_N, CUBLAS_OP_T, n2, n1, n1, &one, A21, lda, W, ldw,
+                           &zero, T, n2),
+               "gemm (L21)");
+  HXG_CUDA(cudaMemcpy2DAsync(A21, sizeof(double) * lda, T, sizeof(double) * n2,
+                             sizeof(double) * n2, n1, cudaMemcpyDeviceToDevice, s));
+  cublas_check(cublasDsyrk(L.cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, n2, n1, &minus_one, A21,
+                           lda, &one, A22, lda),
+               "syrk");
+  chol_inv(L, A22, lda, W22, ldw, n2, info);
+  cublas_check(cublasDgemm(L.cublas, CUBLAS_OP_N, CUBLAS_OP_N, n2, n1, n1, &one, A21, lda, W, ldw,
+                           &zero, T, n2),
+               "gemm (L21 W11)");
+  cublas_check(cublasDgemm(L.cublas, CUBLAS_OP_N, CUBLAS_OP_N, n2, n1, n2, &minus_one, W22, ldw, T,
+                           n2, &zero, W21, ldw),
+               "gemm (W21)");
 }
 
 void NdCholesky::factor_front(int t, Lane& L, const CsrMatrix& a,
@@ -605,16 +670,8 @@ void NdCholesky::factor_front(int t, Lane& L, const CsrMatrix& a,
   // W = L11^-1 (trtri; the front's upper half is zero, so W's is too);
   // L21 = A21 W^T; S = A22 - L21 L21^T (syrk); M = [W; L21 W] written
   // straight into the factor.
-  if (cusolverDnDpotrf(L.cusolver, CUBLAS_FILL_MODE_LOWER, f.np, W, m, L.potrf_ws.p,
-                       (int)L.potrf_ws.n, info_.p + t) != CUSOLVER_STATUS_SUCCESS)
-    throw Error(HXG_ERR_CUDA, "potrf failed");
-  HXG_CUDA(cudaMemcpy2DAsync(L.inv.p, sizeof(double) * f.np, W, sizeof(double) * m,
-                             sizeof(double) * f.np, f.np, cudaMemcpyDeviceToDevice, s));
-  if (cusolverDnXtrtri(L.cusolver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, f.np, CUDA_R_64F,
-                       L.inv.p, f.np, L.trtri_ws.p, L.trtri_ws.n * sizeof(double),
-                       L.trtri_host.data(), L.trtri_host.size(),
-                       info_.p + fronts_.size() + t) != CUSOLVER_STATUS_SUCCESS)
-    throw Error(HXG_ERR_CUDA, "trtri failed");
+  HXG_CUDA(cudaMemsetAsync(L.inv.p, 0, sizeof(double) * (size_t)f.np * f.np, s));
+  chol_inv(L, W, m, L.inv.p, f.np, f.np, info_.p + t);
   double* Lp = L_.p + f.loff;
   if (f.ns > 0) {
     cublas_check(cublasDgemm(L.cublas, CUBLAS_OP_N, CUBLAS_OP_T, f.ns, f.np, f.np, &one, W + f.np,

@@ -64,6 +64,7 @@ class NdCholesky {
   DevBuf<double> L_;         // factor panels
   struct Lane;
   void plan_lanes();
+  void chol_inv(Lane& lane, double* A, int lda, double* W, int ldw, int n, int* info);
   void factor_front(int t, Lane& lane, const CsrMatrix& a,
                     std::vector<std::pair<size_t, int>>& stack);
   std::vector<std::unique_ptr<Lane>> lanes_;
