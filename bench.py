@@ -192,8 +192,19 @@ def run_distributed_pmg(rank, world, dist, stream):
     rep = distributed_pcg(hier, b, rtol=1e-8)
     ev[4].record(stream)
     torch.cuda.synchronize()
+    # full Newton solve (1 load step, line search) on the slabs
+    from paper_2204_01722_b200.distributed import distributed_solve
+    en = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    en[0].record(stream)
+    nrep = distributed_solve(hier, load_steps=1)
+    en[1].record(stream)
+    torch.cuda.synchronize()
     t = torch.tensor([ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3]),
-                      ev[3].elapsed_time(ev[4])], dtype=torch.float64, device="cuda")
+                      ev[3].elapsed_time(ev[4]), en[0].elapsed_time(en[1])], dtype=torch.float64,
+                     device="cuda")
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     out = {"config": f"Q{order} beam {cells} cells, extents {ext}, fixed -x, traction "
@@ -202,6 +213,8 @@ def run_distributed_pmg(rank, world, dist, stream):
            "residual_ms": t[0].item(), "setup_numeric_ms": t[1].item(),
            "pcg_rtol1e-8_ms": t[2].item(), "pcg_rtol1e-8_iterations": rep["iterations"],
            "condition": rep["eig_max"] / rep["eig_min"],
+           "newton_solve_ms": t[3].item(), "newton_iterations": nrep["newton_iterations"],
+           "newton_cg_iterations": nrep["cg_iterations"], "newton_final_fnorm": nrep["final_fnorm"],
            "coarse": "global Q1 matrix summed over slabs, replicated device Cholesky",
            "timing": "device events, max over ranks"}
     del hier, prob

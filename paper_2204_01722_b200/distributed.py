@@ -29,7 +29,8 @@ algorithm from them:
 The level operations come from a *backend* (duck-typed):
 ``levels`` (orders, coarse first), ``size(k)``, ``npd(k)``, ``mask(k)``,
 ``apply(k, x)``, ``diagonal(k)``, ``prolong(kc, xc)``, ``restrict(kc, xf)``,
-``coarse_csr()``, ``coarse_solver(row_ptr, cols, npd)`` and ``device``.
+``coarse_csr()``, ``coarse_solver(row_ptr, cols, npd)``, ``device`` and, for
+the Newton driver, ``residual(u)`` and ``set_time(t)``.
 ``SlabBackend`` is the GPU one (libhexmg_b200 through the C-ABI); the CPU
 tests plug the numpy oracle in the same place.
 """
@@ -397,6 +398,150 @@ def distributed_pcg(h: DistributedHierarchy, b, rtol=1e-8, max_iterations=500, p
     return rep
 
 
+class StepRejected(RuntimeError):
+    """StepRejectedError (errors.hpp) of the distributed driver."""
+
+
+def _critical_point_line_search(g_eval, g0):
+    """critical_point_line_search (nonlinear.hpp:77-129)."""
+    trial, halvings = 1.0, 0
+    g1 = g_eval(trial)
+    while not math.isfinite(g1) and halvings < 5:
+        trial *= 0.5
+        g1 = g_eval(trial)
+        halvings += 1
+    if not math.isfinite(g1):
+        raise StepRejected("residual not evaluable along the search direction")
+    if g0 >= 0.0 or g1 == g0:
+        alpha = trial
+    else:
+        alpha = min(max(trial * g0 / (g0 - g1), 0.1), 2.0)
+        if halvings > 0:
+            alpha = min(alpha, trial)
+    if alpha == trial:
+        return alpha
+    ga = g_eval(alpha)
+    while not math.isfinite(ga) and halvings < 5:
+        alpha *= 0.5
+        ga = g_eval(alpha)
+        halvings += 1
+    if not math.isfinite(ga):
+        raise StepRejected("residual not evaluable at the line search result")
+    return alpha
+
+
+def distributed_newton(h: DistributedHierarchy, u, max_iterations=50, rtol=1e-8, atol=1e-10,
+                       linear_rtol=1e-3, linear_max_iterations=500, use_line_search=True,
+                       load_step=0, time=1.0):
+    """newton_solve (nonlinear.hpp:162-216) on the slab-partitioned system:
+    the residual is the backend's local residual + interface exchange (and
+    leaves the shared quadrature state at the evaluated iterate), norms and
+    line-search slopes are owned-entry dots, the p-MG is rebuilt at every
+    linearisation point.  An inverted element on any rank reads as NaN on
+    every rank (max all-reduce of the failure flag)."""
+    k = h.L - 1
+    npd = h.npd(k)
+
+    def residual(v):
+        bad = torch.zeros(1, dtype=torch.float64, device=v.device)
+        f = None
+        try:
+            f = h.b.residual(v)
+        except Exception as exc:  # noqa: BLE001  (InvertedElementError of either backend)
+            if "nvert" not in type(exc).__name__:
+                raise
+            bad += 1.0
+        if h.comm.dist is not None:
+            h.comm.dist.all_reduce(bad, op=h.comm.dist.ReduceOp.MAX)
+        if bad.item() > 0:
+            return None
+        return h.comm.exchange(f, npd)
+
+    def norm(v):
+        return math.sqrt(max(h.dot(k, v, v), 0.0))
+
+    f = residual(u)
+    if f is None:
+        raise StepRejected("inverted element at the initial iterate")
+    fnorm0 = norm(f)
+    rep = dict(converged=False, iterations=0, total_cg_iterations=0, records=[])
+    if fnorm0 <= atol:
+        rep.update(converged=True, final_fnorm=fnorm0)
+        return rep
+    for it in range(1, max_iterations + 1):
+        h.setup_numeric()
+        cg = distributed_pcg(h, -f, rtol=linear_rtol, max_iterations=linear_max_iterations)
+        du = cg["x"]
+        rep["total_cg_iterations"] += cg["iterations"]
+        last = {}
+
+        def g_eval(a):
+            ft = residual(u + a * du)
+            if ft is None:
+                return float("nan")
+            last["f"] = ft
+            g = h.dot(k, ft, du)
+            return g if math.isfinite(g) else float("nan")
+
+        if use_line_search:
+            alpha = _critical_point_line_search(g_eval, h.dot(k, f, du))
+        else:
+            if not math.isfinite(g_eval(1.0)):
+                raise StepRejected("residual not evaluable at the full Newton step")
+            alpha = 1.0
+        u += alpha * du
+        f = last["f"]  # the search's last evaluation was at the accepted point
+        fnorm = norm(f)
+        rep["records"].append(dict(load_step=load_step, time=time, iteration=it, fnorm=fnorm,
+                                   fnorm_rel=fnorm / fnorm0, cg_iterations=cg["iterations"],
+                                   alpha=alpha))
+        rep["iterations"] = it
+        if fnorm <= max(rtol * fnorm0, atol):
+            rep["converged"] = True
+            break
+    f = residual(u)
+    rep["final_fnorm"] = norm(f)
+    return rep
+
+
+def distributed_solve(h: DistributedHierarchy, load_steps=1, max_bisections=3, **newton):
+    """FemProblem::solve (problem.hpp:118-127): load_continuation
+    (nonlinear.hpp:325-366) from u = 0 with whole-face zero Dirichlet values;
+    the backend scales the external load (set_time)."""
+    k = h.L - 1
+    u = torch.zeros(h.b.size(k), dtype=torch.float64, device=h.b.device)
+    saved = u.clone()
+    steps, t_done = [], 0.0
+    for step in range(1, load_steps + 1):
+        target, bisections, t_try = step / load_steps, 0, step / load_steps
+        while True:
+            h.b.set_time(t_try)
+            u.copy_(saved)
+            u[h.b.mask(k)] = 0.0
+            ok = False
+            try:
+                r = distributed_newton(h, u, load_step=step, time=t_try, **newton)
+                ok = r["converged"]
+                if ok:
+                    steps.append(r)
+            except StepRejected:
+                ok = False
+            if ok:
+                t_done = t_try
+                saved.copy_(u)
+                if t_try == target:
+                    break
+                t_try = target
+            else:
+                bisections += 1
+                if bisections > max_bisections:
+                    raise StepRejected(f"load step failed after {max_bisections} bisections")
+                t_try = 0.5 * (t_done + t_try)
+    return dict(u=u, steps=steps, newton_iterations=sum(r["iterations"] for r in steps),
+                cg_iterations=sum(r["total_cg_iterations"] for r in steps),
+                final_fnorm=steps[-1]["final_fnorm"] if steps else 0.0)
+
+
 # --------------------------------------------------------------------------
 # GPU backend: the slab's hexmg objects through the C-ABI
 # --------------------------------------------------------------------------
@@ -448,3 +593,11 @@ class SlabBackend:
         from .hexmg import CoarseCholesky
 
         return CoarseCholesky(row_ptr, cols, npd)
+
+    def residual(self, u):
+        """apply_residual (operator.hpp:146-180): local residual; writes the
+        quadrature state every level shares."""
+        return self.prob.op.apply_residual(u)
+
+    def set_time(self, t):
+        self.prob.op.set_load_scale(t)

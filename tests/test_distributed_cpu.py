@@ -18,7 +18,8 @@ import torch.multiprocessing as mp
 
 from oracle import hexmg_np as H
 from paper_2204_01722_b200.distributed import (DistributedHierarchy, SlabComm, distributed_pcg,
-                                               global_rough_seed_slice, q1_lattice_pattern)
+                                               distributed_solve, global_rough_seed_slice,
+                                               q1_lattice_pattern)
 from paper_2204_01722_b200.partition import slab_partition
 
 EXT = (3.0, 1.0, 1.0)
@@ -88,6 +89,12 @@ class OracleSlabBackend:
 
     def coarse_solver(self, row_ptr, cols, npd):
         return _DenseChol(row_ptr, cols, npd)
+
+    def residual(self, u):
+        return torch.from_numpy(self.prob.op.apply_residual(u.numpy()))
+
+    def set_time(self, t):
+        self.prob.op.load_scale = t
 
 
 def _global_reference(cells, order):
@@ -194,3 +201,46 @@ def test_q1_pattern_matches_assembled_operator():
     assert set(zip(nz_rows.tolist(), nz_cols.tolist())) <= pat
     for i in range(len(rp) - 1):
         assert np.all(np.diff(cols[rp[i]:rp[i + 1]]) > 0)
+
+
+def _newton_worker(rank, world, port, traction, steps, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.set_default_dtype(torch.float64)
+        cells, order, ext = (4, 2, 2), 2, (2.0, 1.0, 1.0)
+        slab = slab_partition(cells, world, rank, order)
+        h = ext[0] / cells[0]
+        fixed = (0,) if rank == 0 else ()
+        P = H.make_problem((h * slab.cells[0], ext[1], ext[2]), slab.cells, order,
+                           fixed_faces=fixed, traction_face=1 if rank == world - 1 else -1,
+                           traction=traction)
+        hier = DistributedHierarchy(OracleSlabBackend(P, fixed), SlabComm(rank, world, dist),
+                                    cells, slab.x0,
+                                    lambda p: H.build_constraints(H.build_box_mesh(ext, cells, p), (0,)))
+        rep = distributed_solve(hier, load_steps=steps, use_line_search=False)
+        out[rank] = (rep["newton_iterations"], rep["cg_iterations"], rep["final_fnorm"],
+                     rep["u"].numpy(), slab.node_x0, slab.npd[0])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,traction,steps", [("compress1_ls0", (-0.05, 0.0, 0.0), 1),
+                                                 ("bend_ls0", (0.0, 0.0, -0.02), 5)])
+def test_distributed_newton_matches_reference(case, traction, steps):
+    """Slab-partitioned Newton + p-MG + load continuation (2 ranks) against
+    the UNMODIFIED reference's FemProblem::solve on the whole bar
+    (tests/golden/newton.npz): iteration counts and the solution."""
+    G = np.load(os.path.join(os.path.dirname(__file__), "golden", "newton.npz"))
+    ni, ci, fn = G[f"{case}_stats"]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_newton_worker, args=(2, _free_port(), traction, steps, out), nprocs=2, join=True)
+    npd_g = (9, 5, 5)
+    for r in range(2):
+        its, cgits, fnorm, u, x0, nx = out[r]
+        assert abs(its - ni) <= steps and abs(cgits - ci) <= its
+        assert fnorm < 1e-9
+        ur = _slice(G[f"{case}_u"], npd_g, x0, nx)
+        assert np.linalg.norm(u - ur) < 1e-9 * np.linalg.norm(ur)
