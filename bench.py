@@ -346,6 +346,7 @@ def run_ours(args, rank, world, local_rank):
             mg = prob_n.hierarchy
             prob_n.op.apply_residual(un)
             mg.setup_numeric()  # warm-up: symbolic analysis, allocations
+            cg_solve(prob_n.op, torch.ones_like(un), rtol=1e-1, precond="mg", mg=mg)  # workspaces
             torch.cuda.synchronize()
             evs[0].record(stream)
             fn = prob_n.op.apply_residual(un)
