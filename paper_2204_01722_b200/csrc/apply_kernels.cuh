@@ -126,9 +126,10 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams
 #pragma unroll
         for (int d = 0; d < 3; ++d) G[3 * c + d] = g[c][d][qz];
       jacobian_qf(prm.mu, prm.lambda, G, st, H);
-      if (prm.perturb != 0.0) {
+      if (prm.perturb != 0.0) {  // fault-injection hook: + eps w detJ G
+        const double wdet = prm.geo[(base + (long long)qz * T) * kGeoStride + 9 * T + threadIdx.x];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) H[k] += prm.perturb * st[0] * G[k];
+        for (int k = 0; k < 9; ++k) H[k] += prm.perturb * wdet * G[k];
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c)
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams
       const double* gp = prm.geo + (base + (long long)qz * T) * kGeoStride + threadIdx.x;
 #pragma unroll
       for (int s = 0; s < kGeoStride; ++s) geo[s] = __ldg(gp + s * T);
-      double G[9], H[9], st[kStateStride];
+      double G[9], H[9], st[kRefStateScalars];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -160,7 +161,10 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams
         for (int k = 0; k < 9; ++k) H[k] = 0.0;
       } else if (tp.e >= 0) {
 #pragma unroll
-        for (int s = 0; s < kStateStride; ++s) so[s * T] = st[s];
+        double sp[kStateStride];
+        pack_state(prm.mu, st, sp);
+#pragma unroll
+        for (int s = 0; s < kStateStride; ++s) so[s * T] = sp[s];
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c)

@@ -19,6 +19,7 @@ struct DiagParams {
   const double* interp;  // Q x N
   const double* deriv;   // Q x N
   const double* state;
+  const double* geo;  // geometric factors (w detJ for the perturbation hook)
   double mu, lambda, perturb;
   double* out;  // diag: E-vector (e, c, a); assembly: (e, 3N^3, 3N^3)
 };
@@ -47,7 +48,10 @@ __device__ __forceinline__ void point_tensor(const DiagParams& prm, long long e,
     double G[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, H[9];
     G[u] = 1.0;
     jacobian_qf(prm.mu, prm.lambda, G, st, H);
-    if (prm.perturb != 0.0) H[u] += prm.perturb * st[0];
+    if (prm.perturb != 0.0) {  // + eps w detJ G (w detJ = geometry scalar 9, same point)
+      const long long T = prm.lay.T, row = off / T / kStateStride, t = off % T;
+      H[u] += prm.perturb * prm.geo[(row * kGeoStride + 9) * T + t];
+    }
 #pragma unroll
     for (int k = 0; k < 9; ++k) d81[k * 9 + u] = H[k];
   }

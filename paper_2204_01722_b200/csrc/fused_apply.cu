@@ -68,6 +68,7 @@ struct FusedParams {
   const uint8_t* mask;
   const double* tab;  // B (Q x N) then Dc (Q x Q)
   const double* state;
+  const double* geo;  // geometric factors (w detJ for the perturbation hook)
   double mu, lambda, perturb;
   double* partial;
   int brick0;   // first brick of this launch (pipelined host path)
@@ -523,9 +524,11 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
 #else
       jacobian_qf(prm.mu, prm.lambda, G, st, H);
 #endif
-      if (prm.perturb != 0.0) {
+      if (prm.perturb != 0.0) {  // fault-injection hook: + eps w detJ G
+        const double wdet =
+            prm.geo[((size_t)lay.brick_points() * brick + (size_t)qz * T) * kGeoStride + 9 * T + tid];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) H[k] += prm.perturb * st[0] * G[k];
+        for (int k = 0; k < 9; ++k) H[k] += prm.perturb * wdet * G[k];
       }
     } else {
 #pragma unroll
@@ -797,6 +800,9 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
   prm.face_bits = op.face_bits();
   prm.tab = op.tab_.p;
   prm.state = op.state_->data.p;
+  prm.geo = op.geometry_ ? op.geometry_->data.p : nullptr;
+  if (op.perturb_ != 0.0 && !prm.geo)
+    throw Error(HXG_ERR_INVALID_ARGUMENT, "the perturbation hook needs geometric factors");
   prm.mu = op.mu_;
   prm.lambda = op.lambda_;
   prm.perturb = op.perturb_;
@@ -845,6 +851,9 @@ void fused_jacobian_host(Operator& op, const double* xh, double* yh) {
   prm.face_bits = op.face_bits();
   prm.tab = op.tab_.p;
   prm.state = op.state_->data.p;
+  prm.geo = op.geometry_ ? op.geometry_->data.p : nullptr;
+  if (op.perturb_ != 0.0 && !prm.geo)
+    throw Error(HXG_ERR_INVALID_ARGUMENT, "the perturbation hook needs geometric factors");
   prm.mu = op.mu_;
   prm.lambda = op.lambda_;
   prm.perturb = op.perturb_;

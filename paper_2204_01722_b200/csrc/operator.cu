@@ -1,6 +1,8 @@
 // MatrixFreeOperator on device (operator.hpp:70-373).
 #include "operator.hpp"
 
+#include <cmath>
+
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -109,7 +111,7 @@ void Operator::set_external_load(const double* host) {
 double Operator::stored_bytes_per_dof() const {
   // operator.hpp:137-141 — the reference's byte model (state in its own
   // layout: E * q^3 * 17 doubles, plus input and output vectors).
-  double state_bytes = (double)num_elements() * q_ * q_ * q_ * kStateStride * sizeof(double);
+  double state_bytes = (double)num_elements() * q_ * q_ * q_ * kRefStateScalars * sizeof(double);
   double vec_bytes = 2.0 * (double)size() * sizeof(double);
   return (state_bytes + vec_bytes) / (double)size();
 }
@@ -127,6 +129,8 @@ void Operator::launch_element(int mode, const double* x, bool mask_input) {
   prm.mu = mu_;
   prm.lambda = lambda_;
   prm.perturb = perturb_;
+  if (perturb_ != 0.0 && !prm.geo)
+    throw Error(HXG_ERR_INVALID_ARGUMENT, "the perturbation hook needs geometric factors");
   prm.fail = fail_.p;
   size_t ev_need = (size_t)num_elements() * 3 * (p_ + 1) * (p_ + 1) * (p_ + 1);
   if (evec_.n != ev_need) evec_.alloc(ev_need);
@@ -247,9 +251,12 @@ void Operator::extract_diagonal(double* d) {
   prm.interp = interp_d_.p;
   prm.deriv = deriv_d_.p;
   prm.state = state_->data.p;
+  prm.geo = geometry_ ? geometry_->data.p : nullptr;
   prm.mu = mu_;
   prm.lambda = lambda_;
   prm.perturb = perturb_;
+  if (perturb_ != 0.0 && !prm.geo)
+    throw Error(HXG_ERR_INVALID_ARGUMENT, "the perturbation hook needs geometric factors");
   prm.out = evec_.p;
   dispatch_pq(p_, q_, [&](auto Pc, auto Qc) {
     constexpr int P = decltype(Pc)::value, Q = decltype(Qc)::value;
@@ -272,9 +279,12 @@ void Operator::element_matrices(double* out) {
   prm.interp = interp_d_.p;
   prm.deriv = deriv_d_.p;
   prm.state = state_->data.p;
+  prm.geo = geometry_ ? geometry_->data.p : nullptr;
   prm.mu = mu_;
   prm.lambda = lambda_;
   prm.perturb = perturb_;
+  if (perturb_ != 0.0 && !prm.geo)
+    throw Error(HXG_ERR_INVALID_ARGUMENT, "the perturbation hook needs geometric factors");
   prm.out = out;
   if (p_ != 1) throw Error(HXG_ERR_UNSUPPORTED, "assembly is implemented for the p = 1 coarse level");
   dispatch_q(q_, [&](auto Qc) {
@@ -332,18 +342,29 @@ double Operator::total_strain_energy(const double* u) {
 }
 
 void Operator::export_state(double* host) const {
+  // Stored [sqrt(w detJ) xi (9), tau (6), 2 (mu - lambda log J)] back to the
+  // reference's (e, q, 17) Current layout; w detJ from the geometry.
+  if (!geometry_) throw Error(HXG_ERR_INVALID_ARGUMENT, "state export needs geometric factors");
   size_t tot = (size_t)lay_.total_points() * kStateStride;
-  std::vector<double> blocked(tot);
+  std::vector<double> blocked(tot), geo((size_t)lay_.total_points() * kGeoStride);
   HXG_CUDA(cudaMemcpy(blocked.data(), state_->data.p, tot * sizeof(double), cudaMemcpyDeviceToHost));
+  HXG_CUDA(cudaMemcpy(geo.data(), geometry_->data.p, geo.size() * sizeof(double),
+                      cudaMemcpyDeviceToHost));
   int nq = q_ * q_ * q_;
   for (long long e = 0; e < num_elements(); ++e)
     for (int qp = 0; qp < nq; ++qp) {
       long long brick;
       int qz, t;
       lay_.locate(e, qp, brick, qz, t);
-      size_t base = (size_t)(((brick * lay_.Q + qz) * kStateStride) * lay_.T + t);
-      for (int s = 0; s < kStateStride; ++s)
-        host[((size_t)e * nq + qp) * kStateStride + s] = blocked[base + (size_t)s * lay_.T];
+      const size_t row = (size_t)(brick * lay_.Q + qz);
+      const size_t base = row * kStateStride * lay_.T + t;
+      const double wdet = geo[(row * kGeoStride + 9) * lay_.T + t];
+      const double isw = 1.0 / std::sqrt(wdet);
+      double* out = host + ((size_t)e * nq + qp) * kRefStateScalars;
+      out[0] = wdet;
+      for (int k = 0; k < 9; ++k) out[1 + k] = blocked[base + (size_t)k * lay_.T] * isw;
+      for (int k = 0; k < 6; ++k) out[10 + k] = blocked[base + (size_t)(9 + k) * lay_.T];
+      out[16] = mu_ - 0.5 * blocked[base + (size_t)15 * lay_.T];
     }
 }
 

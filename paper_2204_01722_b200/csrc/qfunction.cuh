@@ -4,17 +4,20 @@
 
 #include <cuda_runtime.h>
 
+#include "common.hpp"
+
 namespace hxg {
 
-// state = [w detJ, dxi/dx (9), tau (00,11,22,01,02,12), lambda log J]
-// (material.hpp:145-148).  Jacobian action (material.hpp:179-194):
+// Jacobian action (material.hpp:179-194) on the stored state
+// st = [A = sqrt(w detJ) dxi/dx (9), tau (00,11,22,01,02,12), c = 2 (mu - lambda log J)]:
 //   grad_du = G dxi/dx, deps = sym(grad_du),
 //   k = grad_du tau + lambda tr(deps) I + 2 (mu - lambda log J) deps,
-//   H = w detJ * k dxi/dx^T.
-__device__ __forceinline__ void jacobian_qf(double mu, double lambda, const double G[9],
-                                            const double st[17], double H[9]) {
-  const double w = st[0];
-  const double* xi = st + 1;
+//   H = w detJ * k dxi/dx^T
+// computed as gd = G A (= sqrt(w) grad_du), k~ from gd (linear: = sqrt(w) k),
+// H = k~ A^T.
+__device__ __forceinline__ void jacobian_qf(double /*mu*/, double lambda, const double G[9],
+                                            const double st[kStateStride], double H[9]) {
+  const double* xi = st;
   double gd[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -25,7 +28,7 @@ __device__ __forceinline__ void jacobian_qf(double mu, double lambda, const doub
       s = s + G[3 * i + 2] * xi[6 + j];
       gd[3 * i + j] = s;
     }
-  const double tau[9] = {st[10], st[13], st[14], st[13], st[11], st[15], st[14], st[15], st[12]};
+  const double tau[9] = {st[9], st[12], st[13], st[12], st[10], st[14], st[13], st[14], st[11]};
   double k[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -37,7 +40,7 @@ __device__ __forceinline__ void jacobian_qf(double mu, double lambda, const doub
       k[3 * i + j] = s;
     }
   const double tr = lambda * (gd[0] + gd[4] + gd[8]);
-  const double c = 2.0 * (mu - st[16]);
+  const double c = st[15];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     k[3 * i + i] += tr;
@@ -51,8 +54,19 @@ __device__ __forceinline__ void jacobian_qf(double mu, double lambda, const doub
       double s = k[3 * i + 0] * xi[3 * j + 0];
       s = s + k[3 * i + 1] * xi[3 * j + 1];
       s = s + k[3 * i + 2] * xi[3 * j + 2];
-      H[3 * i + j] = w * s;
+      H[3 * i + j] = s;
     }
+}
+
+// Reference-layout state (residual_qf's output) -> stored state.
+__device__ __forceinline__ void pack_state(double mu, const double r[kRefStateScalars],
+                                           double st[kStateStride]) {
+  const double sw = sqrt(r[0]);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) st[k] = sw * r[1 + k];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) st[9 + k] = r[10 + k];
+  st[15] = 2.0 * (mu - r[16]);
 }
 
 __device__ __forceinline__ double det3(const double m[9]) {
@@ -64,7 +78,7 @@ __device__ __forceinline__ double det3(const double m[9]) {
 // outputs are unspecified and the caller records the inverted point.
 __device__ __forceinline__ double residual_qf(double mu, double lambda, const double G[9],
                                               const double dxidX[9], double wdet, double H[9],
-                                              double st[17]) {
+                                              double st[kRefStateScalars]) {
   double F[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
