@@ -37,9 +37,9 @@ constexpr int kMaxQ = 5;
 // lambda log J] -- the byte model and hxg_op_export_state use this layout.
 constexpr int kRefStateScalars = 17;
 // Stored on the device: the same data in 16 scalars,
-// [sqrt(w detJ) dxi/dx (9), tau (6), 2 (mu - lambda log J)]: w detJ folds into
+// [sqrt(w detJ) dxi/dx (9), tau (6), mu - lambda log J]: w detJ folds into
 // the two dxi/dx products of the Jacobian q-function (sqrt(w) on each side),
-// one scalar less to stream and 11 fewer flops per point.  w detJ itself is
+// one scalar less to stream and ~20 fewer flops per point.  w detJ itself is
 // the geometry's (undeformed) weight, kept in the geometric factors.
 constexpr int kStateStride = 16;
 // Geometry per qpt: dxi/dX (9, row-major) then w * detJ (mesh.hpp:169-189).

@@ -342,7 +342,7 @@ double Operator::total_strain_energy(const double* u) {
 }
 
 void Operator::export_state(double* host) const {
-  // Stored [sqrt(w detJ) xi (9), tau (6), 2 (mu - lambda log J)] back to the
+  // Stored [sqrt(w detJ) xi (9), tau (6), mu - lambda log J] back to the
   // reference's (e, q, 17) Current layout; w detJ from the geometry.
   if (!geometry_) throw Error(HXG_ERR_INVALID_ARGUMENT, "state export needs geometric factors");
   size_t tot = (size_t)lay_.total_points() * kStateStride;
@@ -364,7 +364,7 @@ void Operator::export_state(double* host) const {
       out[0] = wdet;
       for (int k = 0; k < 9; ++k) out[1 + k] = blocked[base + (size_t)k * lay_.T] * isw;
       for (int k = 0; k < 6; ++k) out[10 + k] = blocked[base + (size_t)(9 + k) * lay_.T];
-      out[16] = mu_ - 0.5 * blocked[base + (size_t)15 * lay_.T];
+      out[16] = mu_ - blocked[base + (size_t)15 * lay_.T];
     }
 }
 

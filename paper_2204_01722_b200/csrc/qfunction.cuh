@@ -9,7 +9,7 @@
 namespace hxg {
 
 // Jacobian action (material.hpp:179-194) on the stored state
-// st = [A = sqrt(w detJ) dxi/dx (9), tau (00,11,22,01,02,12), c = 2 (mu - lambda log J)]:
+// st = [A = sqrt(w detJ) dxi/dx (9), tau (00,11,22,01,02,12), h = mu - lambda log J]:
 //   grad_du = G dxi/dx, deps = sym(grad_du),
 //   k = grad_du tau + lambda tr(deps) I + 2 (mu - lambda log J) deps,
 //   H = w detJ * k dxi/dx^T
@@ -39,14 +39,19 @@ __device__ __forceinline__ void jacobian_qf(double /*mu*/, double lambda, const 
       s = s + gd[3 * i + 2] * tau[6 + j];
       k[3 * i + j] = s;
     }
+  // + lambda tr(deps) I + 2 h sym(gd): the symmetric part once per pair
   const double tr = lambda * (gd[0] + gd[4] + gd[8]);
-  const double c = st[15];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    k[3 * i + i] += tr;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) k[3 * i + j] += c * (0.5 * (gd[3 * i + j] + gd[3 * j + i]));
-  }
+  const double h = st[15], h2 = h + h;
+  k[0] += fma(h2, gd[0], tr);
+  k[4] += fma(h2, gd[4], tr);
+  k[8] += fma(h2, gd[8], tr);
+  const double s01 = h * (gd[1] + gd[3]), s02 = h * (gd[2] + gd[6]), s12 = h * (gd[5] + gd[7]);
+  k[1] += s01;
+  k[3] += s01;
+  k[2] += s02;
+  k[6] += s02;
+  k[5] += s12;
+  k[7] += s12;
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -66,7 +71,7 @@ __device__ __forceinline__ void pack_state(double mu, const double r[kRefStateSc
   for (int k = 0; k < 9; ++k) st[k] = sw * r[1 + k];
 #pragma unroll
   for (int k = 0; k < 6; ++k) st[9 + k] = r[10 + k];
-  st[15] = 2.0 * (mu - r[16]);
+  st[15] = mu - r[16];
 }
 
 __device__ __forceinline__ double det3(const double m[9]) {
