@@ -160,7 +160,6 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams
 #pragma unroll
         for (int k = 0; k < 9; ++k) H[k] = 0.0;
       } else if (tp.e >= 0) {
-#pragma unroll
         double sp[kStateStride];
         pack_state(prm.mu, st, sp);
 #pragma unroll
