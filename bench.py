@@ -33,6 +33,13 @@ UNIT = "GDoF/s"
 ORDER, CELLS = 2, 64
 
 
+def peak_gbs():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)
+    except Exception:
+        return 6650.0
+
+
 def algorithmic_bytes(num_elements, q, ndof):
     """Reference byte model (operator.hpp:137-141 = PAPER.md:476):
     8 (17 E q^3 + 2 N_dof) per Jacobian apply."""
@@ -302,6 +309,50 @@ def run_ours(args, rank, world, local_rank):
     except Exception:
         pass
 
+    # BASELINE.json configs[4] scale: Q2 160^3 elements per GPU (99.2 M DoF,
+    # ~1e8 DoF per GPU), geometry built on the device; same slab weak scaling.
+    cfg5 = None
+    if not args.no_cfg5:
+        c5 = 160
+        prob5 = FemProblem(extents=(1.0, 1.0, 1.0), cells=(c5,) * 3, order=ORDER, fixed_faces=fixed,
+                           geometry="box")
+        n5 = prob5.size()
+        prob5.op.apply_residual(torch.zeros(n5, dtype=torch.float64, device="cuda"))
+        x5 = 1e-3 * torch.sin(0.7 * (torch.arange(n5, dtype=torch.float64, device="cuda") + rank * n5))
+        y5 = torch.empty_like(x5)
+        npd5 = (ORDER * c5 + 1,) * 3
+
+        def step5():
+            prob5.op.apply_jacobian(x5, y5)
+            if dist is not None:
+                exchange_faces(y5, npd5, rank, world, dist)
+
+        for _ in range(3):
+            step5()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        e5 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        reps5 = 20
+        e5[0].record(stream)
+        for _ in range(reps5):
+            step5()
+        e5[1].record(stream)
+        torch.cuda.synchronize()
+        ms5 = e5[0].elapsed_time(e5[1]) / reps5
+        if dist is not None:
+            t5 = torch.tensor([ms5], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t5, op=dist.ReduceOp.MAX)
+            ms5 = t5.item()
+        b5 = algorithmic_bytes(prob5.num_elements, prob5.q, n5)
+        cfg5 = {"config": f"Q2 {c5}^3 elements per GPU, Jacobian apply (BASELINE configs[4] per-GPU "
+                          "size), device-built box geometry", "dofs_per_gpu": n5,
+                "ms_per_apply": ms5, "GDoF_s": n5 * world / (ms5 * 1e-3) / 1e9,
+                "algorithmic_GB_s_per_gpu": b5 / (ms5 * 1e-3) / 1e9,
+                "roofline_frac": b5 / (ms5 * 1e-3) / 1e9 / peak_gbs()}
+        del prob5, x5, y5
+        torch.cuda.empty_cache()
+
     # End-to-end through the C-ABI host-buffer entry point (pinned host x/y).
     xh = x.cpu().pin_memory()
     yh = torch.empty_like(xh).pin_memory()
@@ -457,6 +508,7 @@ def run_ours(args, rank, world, local_rank):
             "pmg_solves": pmg,
             "pmg_distributed": pmg_dist,
             "newton_solve": newton_full,
+            "apply_cfg5": cfg5,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -473,6 +525,7 @@ def main():
     ap.add_argument("--cpu-applies", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-newton", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))

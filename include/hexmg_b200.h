@@ -82,6 +82,13 @@ typedef struct {
   double mu, lambda;     /* NeoHookean                         */
   int storage;           /* JacobianStorage; 0 = Current       */
   const uint8_t* mask;   /* 3*num_nodes Constraints::mask or NULL */
+  /* Device-side geometry: when dxidX/weight are NULL
+   * and both of these are given, the geometric factors of the axis-aligned
+   * box BoxMesh (build_box_mesh, mesh.hpp:35-60; affine elements) are
+   * computed on the device: dxi/dX = diag(2 cells / extents), w detJ =
+   * w_x w_y w_z prod(extents / (2 cells)) -- no E*q^3*10 host arrays. */
+  const double* extents; /* 3, or NULL                          */
+  const double* qweights;/* q Gauss-Legendre weights, or NULL   */
 } hxg_op_desc;
 
 /* QuadratureStateStore shared by all levels of a hierarchy

@@ -103,7 +103,8 @@ class OpDesc(ctypes.Structure):
                 ("interp", ctypes.c_void_p), ("deriv", ctypes.c_void_p),
                 ("colloc", ctypes.c_void_p), ("dxidX", ctypes.c_void_p),
                 ("weight", ctypes.c_void_p), ("mu", ctypes.c_double),
-                ("lam", ctypes.c_double), ("storage", ctypes.c_int), ("mask", ctypes.c_void_p)]
+                ("lam", ctypes.c_double), ("storage", ctypes.c_int), ("mask", ctypes.c_void_p),
+                ("extents", ctypes.c_void_p), ("qweights", ctypes.c_void_p)]
 
 
 # name -> argtypes (all return int unless listed in _RESTYPE)

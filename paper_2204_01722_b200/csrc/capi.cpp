@@ -106,7 +106,10 @@ int hxg_op_create(const hxg_op_desc* d, hxg_state_t state, hxg_op_t* out) {
     std::vector<double> deriv(d->deriv, d->deriv + q * n);
     std::vector<double> colloc(d->colloc, d->colloc + q * q);
     std::shared_ptr<hxg::Geometry> geo;
-    if (d->dxidX && d->weight) geo = hxg::Operator::make_geometry(d->cells, q, d->dxidX, d->weight);
+    if (d->dxidX && d->weight)
+      geo = hxg::Operator::make_geometry(d->cells, q, d->dxidX, d->weight);
+    else if (d->extents && d->qweights)
+      geo = hxg::Operator::make_box_geometry(d->cells, q, d->extents, d->qweights);
     auto* h = new hxg_op_s();
     h->owned = std::make_unique<hxg::Operator>(d->order, q, d->cells, interp, deriv, colloc, d->mu,
                                                d->lambda, d->mask, state ? state->s : nullptr, geo);

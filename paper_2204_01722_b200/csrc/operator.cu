@@ -47,6 +47,49 @@ std::shared_ptr<Geometry> Operator::make_geometry(const int cells[3], int q, con
   return g;
 }
 
+namespace {
+// Box geometry in the blocked layout ((brick, qz, s, t), 10 scalars): every
+// element of build_box_mesh is the same affine map, so dxi/dX = diag(2/h)
+// and w detJ = w_qx w_qy w_qz h_x h_y h_z / 8 at every point.
+__global__ void box_geometry_kernel(QLayout lay, double gx, double gy, double gz, double jac,
+                                    const double* __restrict__ qw, double* __restrict__ geo) {
+  const long long total = lay.total_points();
+  const int Q = lay.Q, NE = lay.B[0] * lay.B[1] * lay.B[2];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i / lay.T;  // brick * Q + qz
+    const int t = (int)(i - row * lay.T), qz = (int)(row % Q);
+    const int col = t / NE, qx = col % Q, qy = col / Q;
+    double* g = geo + row * kGeoStride * lay.T + t;
+    for (int s = 0; s < 9; ++s) g[(long long)s * lay.T] = 0.0;
+    g[0] = gx;
+    g[4LL * lay.T] = gy;
+    g[8LL * lay.T] = gz;
+    g[9LL * lay.T] = qw[qx] * qw[qy] * qw[qz] * jac;
+  }
+}
+}  // namespace
+
+std::shared_ptr<Geometry> Operator::make_box_geometry(const int cells[3], int q,
+                                                      const double extents[3],
+                                                      const double* qweights) {
+  auto g = std::make_shared<Geometry>();
+  g->lay = QLayout::make(cells, q);
+  g->data.alloc((size_t)g->lay.total_points() * kGeoStride);
+  DevBuf<double> qw;
+  qw.upload(qweights, (size_t)q);
+  double h[3];
+  for (int d = 0; d < 3; ++d) {
+    if (!(extents[d] > 0.0)) throw Error(HXG_ERR_INVALID_ARGUMENT, "box extents must be positive");
+    h[d] = extents[d] / cells[d];
+  }
+  box_geometry_kernel<<<grid_for(g->lay.total_points(), 256), 256>>>(
+      g->lay, 2.0 / h[0], 2.0 / h[1], 2.0 / h[2], 0.125 * h[0] * h[1] * h[2], qw.p, g->data.p);
+  HXG_CUDA(cudaGetLastError());
+  HXG_CUDA(cudaDeviceSynchronize());  // qw is released on return
+  return g;
+}
+
 Operator::Operator(int p, int q, const int cells[3], const std::vector<double>& interp,
                    const std::vector<double>& deriv, const std::vector<double>& colloc, double mu,
                    double lambda, const uint8_t* mask_host, std::shared_ptr<State> state,

@@ -91,6 +91,10 @@ class Operator {
            std::shared_ptr<Geometry> geometry);
 
   // Builds a Geometry from reference-layout host arrays (e, q, 9) / (e, q).
+  // Affine box geometry computed on the device (no host arrays).
+  static std::shared_ptr<Geometry> make_box_geometry(const int cells[3], int q,
+                                                     const double extents[3],
+                                                     const double* qweights);
   static std::shared_ptr<Geometry> make_geometry(const int cells[3], int q, const double* dxidX,
                                                  const double* weight);
 

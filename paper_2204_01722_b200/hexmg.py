@@ -119,7 +119,7 @@ class MatrixFreeOperator:
     """MatrixFreeOperator (operator.hpp:70-373) on the GPU."""
 
     def __init__(self, cells, basis: Basis1D, dxidX, weight, mu, lam, mask=None, state=None,
-                 _handle=None):
+                 _handle=None, extents=None):
         self._owner = _handle is None
         if _handle is not None:
             self.h = _handle
@@ -135,6 +135,11 @@ class MatrixFreeOperator:
                 w = np.ascontiguousarray(weight, np.float64)
                 self._keep += [dx, w]
                 desc.dxidX, desc.weight = _ptr(dx).value, _ptr(w).value
+            elif extents is not None:  # affine box geometry computed on the device
+                ext = np.ascontiguousarray(extents, np.float64)
+                qw = np.ascontiguousarray(basis.weights, np.float64)
+                self._keep += [ext, qw]
+                desc.extents, desc.qweights = _ptr(ext).value, _ptr(qw).value
             desc.mu, desc.lam, desc.storage = mu, lam, 0
             if mask is not None:
                 m = np.ascontiguousarray(mask, np.uint8)
@@ -432,10 +437,13 @@ class FemProblem:
         self.mu, self.lam = lame_from_young_poisson(young, poisson)
         self.mask, self.fixed_face_mask = constraint_mask(cells, order, fixed_faces)
         dx = w = None
-        if geometry:
+        if geometry is True:  # host restatement of compute_geometric_factors
             dx, w = geometric_factors(extents, cells, order, self.q)
-        self.op = MatrixFreeOperator(cells, self.basis, dx, w, self.mu, self.lam, self.mask)
-        self.load = traction_load(extents, cells, order, self.q, traction_face, traction)
+        self.op = MatrixFreeOperator(cells, self.basis, dx, w, self.mu, self.lam, self.mask,
+                                     extents=extents if geometry == "box" else None)
+        self.load = None
+        if traction_face is not None:  # assemble_traction_load (operator.hpp:381-443)
+            self.load = traction_load(extents, cells, order, self.q, traction_face, traction)
         self.op.set_external_load(self.load)
         self.num_elements = cells[0] * cells[1] * cells[2]
         self.nq = self.q**3
