@@ -217,6 +217,9 @@ typedef struct {
   int use_line_search;
   int load_steps;
   int reference_line_search_quirk;
+  int solver;          /* 0 Newton-CG, 1 L-BFGS (config.hpp:15)            */
+  int lbfgs_memory;    /* L-BFGS pairs (config.hpp:62)                      */
+  int precond_refresh; /* L-BFGS preconditioner rebuild interval, 0 = never */
 } hxg_newton_config;
 typedef struct {
   int load_step;
@@ -241,6 +244,11 @@ int hxg_newton_config_default(hxg_newton_config* cfg);
 int hxg_newton_solve(hxg_op_t op, hxg_mg_t mg, const hxg_newton_config* cfg, double* u,
                      int load_step, double time, hxg_solve_report* report,
                      hxg_iteration_record* records, int capacity);
+/* lbfgs_solve (nonlinear.hpp:226-308): V-cycle as H0 of the two-loop
+ * recursion, critical-point line search. */
+int hxg_lbfgs_solve(hxg_op_t op, hxg_mg_t mg, const hxg_newton_config* cfg, double* u,
+                    int load_step, double time, hxg_solve_report* report,
+                    hxg_iteration_record* records, int capacity);
 /* FemProblem::solve (problem.hpp:118-127): load_continuation
  * (nonlinear.hpp:325-366) from u = 0 over cfg->load_steps, whole-face zero
  * Dirichlet values; u (device) receives the solution. */

@@ -391,6 +391,38 @@ int ref_newton(void* p, int load_steps, int line_search, double linear_rtol, dou
   });
 }
 
+// Same through the configured nonlinear solver (config.hpp:15, :60-64):
+// solver 0 Newton-CG, 1 L-BFGS with `memory` pairs, preconditioner refresh.
+int ref_solve(void* p, int load_steps, int line_search, double linear_rtol, int solver,
+              int memory, int refresh, double* u, int* iterations, int* cg_its,
+              double* final_fnorm) {
+  auto* h = static_cast<RefProblem*>(p);
+  return guarded([&] {
+    ProblemConfig cfg = h->cfg;
+    cfg.load_steps = load_steps;
+    cfg.line_search = line_search != 0;
+    cfg.linear_rtol = linear_rtol;
+    cfg.solver = solver == 1 ? SolverKind::Lbfgs : SolverKind::NewtonCg;
+    cfg.lbfgs_memory = memory;
+    cfg.precond_refresh = refresh;
+    h->problem = std::make_unique<FemProblem>(cfg);
+    h->cfg = cfg;
+    ContinuationReport rep = h->problem->solve();
+    int ni = 0, ci = 0;
+    double fn = 0.0;
+    for (const auto& st : rep.steps) {
+      ni += st.iterations;
+      ci += st.total_cg_iterations;
+      fn = st.final_fnorm;
+    }
+    *iterations = ni;
+    *cg_its = ci;
+    *final_fnorm = fn;
+    const auto& sol = h->problem->solution();
+    std::memcpy(u, sol.data(), sizeof(double) * sol.size());
+  });
+}
+
 // The reference invariant suite; writes "name:pass:detail\n" lines.
 int ref_verify(int threads, double perturbation, char* out, int cap) {
   std::string s;

@@ -65,6 +65,7 @@ def lib():
         L.ref_time_jacobian.argtypes = [vp, vp, i, i]
         L.ref_time_jacobian.restype = d
         L.ref_newton.argtypes = [vp, i, i, d, vp, vp, vp, vp]
+        L.ref_solve.argtypes = [vp, i, i, d, i, i, i, vp, vp, vp, vp]
         L.ref_verify.argtypes = [i, d, vp, i]
         _lib = L
     return _lib
@@ -282,6 +283,16 @@ class RefProblem:
         _check(lib().ref_newton(self.h, load_steps, int(line_search), linear_rtol, _p(u),
                                 ctypes.byref(ni), ctypes.byref(ci), ctypes.byref(fn)))
         return dict(u=u, newton_iterations=ni.value, cg_iterations=ci.value, final_fnorm=fn.value)
+
+    def solve(self, load_steps=1, line_search=True, linear_rtol=1e-3, solver=0, memory=5,
+              refresh=0):
+        """FemProblem::solve with the configured solver (0 Newton, 1 L-BFGS)."""
+        u = np.zeros(self.n)
+        ni, ci, fn = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+        _check(lib().ref_solve(self.h, load_steps, int(line_search), linear_rtol, solver, memory,
+                               refresh, _p(u), ctypes.byref(ni), ctypes.byref(ci),
+                               ctypes.byref(fn)))
+        return dict(u=u, iterations=ni.value, cg_iterations=ci.value, final_fnorm=fn.value)
 
 
 def rough_seed(n, mask=None):

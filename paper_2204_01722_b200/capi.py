@@ -80,7 +80,9 @@ class NewtonConfig(ctypes.Structure):
     _fields_ = [("max_iterations", ctypes.c_int), ("rtol", ctypes.c_double),
                 ("atol", ctypes.c_double), ("linear_rtol", ctypes.c_double),
                 ("linear_max_iterations", ctypes.c_int), ("use_line_search", ctypes.c_int),
-                ("load_steps", ctypes.c_int), ("reference_line_search_quirk", ctypes.c_int)]
+                ("load_steps", ctypes.c_int), ("reference_line_search_quirk", ctypes.c_int),
+                ("solver", ctypes.c_int), ("lbfgs_memory", ctypes.c_int),
+                ("precond_refresh", ctypes.c_int)]
 
 
 class IterationRecord(ctypes.Structure):
@@ -160,6 +162,7 @@ SIGNATURES = {
     "hxg_lambda_max_jacobi": [_vp, _i, _P(_d)],
     "hxg_newton_config_default": [_vp],
     "hxg_newton_solve": [_vp, _vp, _vp, _vp, _i, _d, _vp, _vp, _i],
+    "hxg_lbfgs_solve": [_vp, _vp, _vp, _vp, _i, _d, _vp, _vp, _i],
     "hxg_solve_continuation": [_vp, _vp, _vp, _vp, _i, _vp, _vp, _i],
     "hxg_dot": [_vp, _vp, _i64, _vp, _P(_d)],
     "hxg_malloc": [_vp, _sz],

@@ -481,6 +481,9 @@ hxg::NewtonConfig to_config(const hxg_newton_config* c) {
     nc.use_line_search = c->use_line_search != 0;
     nc.load_steps = c->load_steps;
     nc.reference_line_search_quirk = c->reference_line_search_quirk != 0;
+    nc.solver = c->solver;
+    nc.lbfgs_memory = c->lbfgs_memory;
+    nc.precond_refresh = c->precond_refresh;
   }
   return nc;
 }
@@ -512,7 +515,8 @@ int hxg_newton_config_default(hxg_newton_config* cfg) {
     hxg::NewtonConfig d;
     *cfg = hxg_newton_config{d.max_iterations, d.rtol, d.atol, d.linear_rtol,
                              d.linear_max_iterations, d.use_line_search ? 1 : 0, d.load_steps,
-                             d.reference_line_search_quirk ? 1 : 0};
+                             d.reference_line_search_quirk ? 1 : 0, d.solver, d.lbfgs_memory,
+                             d.precond_refresh};
   });
 }
 
@@ -521,6 +525,16 @@ int hxg_newton_solve(hxg_op_t op, hxg_mg_t mg, const hxg_newton_config* cfg, dou
                      hxg_iteration_record* records, int capacity) {
   return guarded([&] {
     auto r = hxg::newton_solve(OP(op), MG(mg), to_config(cfg), u, load_step, time);
+    const bool conv = r.converged;
+    fill_report({r}, conv, report, records, capacity);
+  });
+}
+
+int hxg_lbfgs_solve(hxg_op_t op, hxg_mg_t mg, const hxg_newton_config* cfg, double* u,
+                    int load_step, double time, hxg_solve_report* report,
+                    hxg_iteration_record* records, int capacity) {
+  return guarded([&] {
+    auto r = hxg::lbfgs_solve(OP(op), MG(mg), to_config(cfg), u, load_step, time);
     const bool conv = r.converged;
     fill_report({r}, conv, report, records, capacity);
   });

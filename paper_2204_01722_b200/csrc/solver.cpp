@@ -493,6 +493,107 @@ SolveReport newton_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, d
   return report;
 }
 
+SolveReport lbfgs_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, double* u,
+                        int load_step, double time) {
+  const long long n = op.size();
+  cudaStream_t s = op.stream();
+  const int mem = std::max(cfg.lbfgs_memory, 0);
+  DevBuf<double> f((size_t)n), q((size_t)n), d((size_t)n), ut((size_t)n), ft((size_t)n);
+  DevBuf<double> ts((size_t)n), ty((size_t)n);
+  std::vector<DevBuf<double>> S(mem), Y(mem);
+  for (int i = 0; i < mem; ++i) {
+    S[i].alloc((size_t)n);
+    Y[i].alloc((size_t)n);
+  }
+  DotWorkspace ws;
+  auto dotp = [&](const double* a, const double* b) { return dot(a, b, n, ws, s); };
+  auto norm2 = [&](const double* v) { return std::sqrt(dotp(v, v)); };
+  op.apply_residual(u, f.p);
+  const double fnorm0 = norm2(f.p);
+  SolveReport report;
+  if (fnorm0 <= cfg.atol) {
+    report.converged = true;
+    report.final_fnorm = fnorm0;
+    return report;
+  }
+  mg.setup_numeric();
+  auto g_eval = [&](double a) {
+    vwaxpy(ut.p, u, a, d.p, n, s);
+    try {
+      op.apply_residual(ut.p, ft.p);
+    } catch (const Error& e) {
+      if (e.code != HXG_ERR_INVERTED_ELEMENT) throw;
+      return std::numeric_limits<double>::quiet_NaN();
+    }
+    const double g = dotp(ft.p, d.p);
+    return std::isfinite(g) ? g : std::numeric_limits<double>::quiet_NaN();
+  };
+  // history ring: slot of pair i (oldest first) = (head + i) % mem
+  int head = 0, h = 0;
+  std::vector<double> rho(mem > 0 ? mem : 1), acoef(mem > 0 ? mem : 1);
+  for (int it = 1; it <= cfg.max_iterations; ++it) {
+    // two-loop recursion: d = -H f, H0 = the V-cycle
+    vcopy(q.p, f.p, n, s);
+    for (int i = h - 1; i >= 0; --i) {
+      const int k = (head + i) % mem;
+      acoef[(size_t)i] = rho[(size_t)k] * dotp(S[k].p, q.p);
+      vwaxpy(q.p, q.p, -acoef[(size_t)i], Y[k].p, n, s);
+    }
+    vzero(d.p, n, s);
+    mg.v_cycle(q.p, d.p, true);
+    for (int i = 0; i < h; ++i) {
+      const int k = (head + i) % mem;
+      const double beta = rho[(size_t)k] * dotp(Y[k].p, d.p);
+      vwaxpy(d.p, d.p, acoef[(size_t)i] - beta, S[k].p, n, s);
+    }
+    vneg(d.p, d.p, n, s);
+    IterationRecord rec;
+    rec.load_step = load_step;
+    rec.time = time;
+    rec.iteration = it;
+    rec.alpha = critical_point_line_search(g_eval, dotp(f.p, d.p)).alpha;
+    // s = alpha d, u += s, y = F_new - F (the quirk reads F_new as zero)
+    const bool quirk = cfg.reference_line_search_quirk;
+    vzero(ts.p, n, s);
+    vwaxpy(ts.p, ts.p, rec.alpha, d.p, n, s);
+    vwaxpy(u, u, 1.0, ts.p, n, s);
+    if (quirk) {
+      vneg(ty.p, f.p, n, s);
+      vzero(f.p, n, s);
+    } else {
+      vwaxpy(ty.p, ft.p, -1.0, f.p, n, s);
+      vcopy(f.p, ft.p, n, s);
+    }
+    const double sy = dotp(ts.p, ty.p);
+    if (mem > 0 && sy > 0.0) {  // push back; drop the oldest beyond `memory`
+      const int slot = h < mem ? (head + h) % mem : head;
+      vcopy(S[slot].p, ts.p, n, s);
+      vcopy(Y[slot].p, ty.p, n, s);
+      rho[(size_t)slot] = 1.0 / sy;
+      if (h < mem)
+        ++h;
+      else
+        head = (head + 1) % mem;
+    }
+    const double fnorm = norm2(f.p);
+    rec.fnorm = fnorm;
+    rec.fnorm_rel = fnorm / fnorm0;
+    report.records.push_back(rec);
+    report.iterations = it;
+    if (fnorm <= std::max(cfg.rtol * fnorm0, cfg.atol)) {
+      report.converged = true;
+      break;
+    }
+    if (cfg.precond_refresh > 0 && it % cfg.precond_refresh == 0) {
+      op.apply_residual(u, f.p);  // pin the state to the current iterate
+      mg.setup_numeric();
+    }
+  }
+  op.apply_residual(u, f.p);
+  report.final_fnorm = norm2(f.p);
+  return report;
+}
+
 std::vector<SolveReport> solve_continuation(Operator& op, Hierarchy& mg, const NewtonConfig& cfg,
                                             double* u, int max_bisections,
                                             std::vector<double>* times) {
@@ -517,7 +618,8 @@ std::vector<SolveReport> solve_continuation(Operator& op, Hierarchy& mg, const N
       vmask_zero(u, op.mask(), n, s);
       bool ok = false;
       try {
-        SolveReport r = newton_solve(op, mg, cfg, u, step, t_try);
+        SolveReport r = cfg.solver == 1 ? lbfgs_solve(op, mg, cfg, u, step, t_try)
+                                        : newton_solve(op, mg, cfg, u, step, t_try);
         ok = r.converged;
         if (ok) {
           steps.push_back(std::move(r));

@@ -102,6 +102,12 @@ struct NewtonConfig {  // nonlinear.hpp:16-24
   // after a line search the residual is read from the un-invoked original
   // evaluator, i.e. zero.  Off by default (the intended algorithm).
   bool reference_line_search_quirk = false;
+  // ProblemConfig::solver (config.hpp:15, :60-64): 0 Newton-CG, 1 L-BFGS with
+  // `lbfgs_memory` pairs and the V-cycle as H0, rebuilt every
+  // `precond_refresh` iterations (0 = never).
+  int solver = 0;
+  int lbfgs_memory = 5;
+  int precond_refresh = 10;
 };
 struct IterationRecord {  // nonlinear.hpp:26-36
   int load_step = 0;
@@ -122,6 +128,10 @@ struct SolveReport {  // nonlinear.hpp:50-56
 // p-MG V-cycle rebuilt at every linearisation point.
 SolveReport newton_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, double* u,
                          int load_step, double time);
+// lbfgs_solve (nonlinear.hpp:226-308) with the V-cycle as the initial
+// inverse Hessian of the two-loop recursion.
+SolveReport lbfgs_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, double* u,
+                        int load_step, double time);
 // FemProblem::solve (problem.hpp:118-127): load_continuation
 // (nonlinear.hpp:325-366) over t_k = k / load_steps with whole-face zero
 // Dirichlet values; returns the per-step reports.

@@ -30,4 +30,12 @@ for name, (tr, steps, ls) in CASES.items():
     out[f"{name}_u"] = r["u"]
     out[f"{name}_stats"] = np.array([r["newton_iterations"], r["cg_iterations"], r["final_fnorm"]])
     print(name, r["newton_iterations"], r["cg_iterations"], r["final_fnorm"])
+# L-BFGS (config.hpp:15, memory 5, refresh 10) with the line search (its
+# functor-copy defect makes it stop after one step per load step)
+rp = R.RefProblem(extents=(2.0, 1.0, 1.0), cells=(4, 2, 2), order=2, fixed=("-x",),
+                  traction_face="+x", traction=(-0.05, 0.0, 0.0))
+r = rp.solve(load_steps=1, line_search=True, solver=1, memory=5, refresh=10)
+out["lbfgs_compress1_u"] = r["u"]
+out["lbfgs_compress1_stats"] = np.array([r["iterations"], r["cg_iterations"], r["final_fnorm"]])
+print("lbfgs_compress1", r["iterations"], r["cg_iterations"], r["final_fnorm"])
 np.savez(os.path.join(HERE, "newton.npz"), **out)

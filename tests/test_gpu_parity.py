@@ -362,3 +362,23 @@ def test_device_box_geometry_matches_host_geometry(order, cells):
     assert np.abs(sa - sb).max() < 1e-12 * np.abs(sa).max()
     x = cuda(np.sin(0.37 * np.arange(a.size())))
     assert rel(b.op.apply_jacobian(x), a.op.apply_jacobian(x).cpu().numpy()) < 1e-12
+
+
+def test_lbfgs_solver():
+    """lbfgs_solve (nonlinear.hpp:226-308, V-cycle as H0): with the
+    reference's line-search defect reproduced it stops like the reference
+    (one step, the same residual); the intended algorithm converges to the
+    Newton solution."""
+    from paper_2204_01722_b200.hexmg import FemProblem
+    kw = dict(extents=(2, 1, 1), cells=(4, 2, 2), order=2, fixed_faces=("-x",),
+              traction_face="+x", traction=(-0.05, 0, 0))
+    G = np.load(os.path.join(GOLD, "newton.npz"))
+    it_ref, _, fn_ref = G["lbfgs_compress1_stats"]
+    q = FemProblem(**kw).solve(load_steps=1, solver=1, lbfgs_memory=5, precond_refresh=10,
+                               reference_line_search_quirk=True)
+    assert q["newton_iterations"] == it_ref
+    assert abs(q["final_fnorm"] - fn_ref) < 1e-6 * fn_ref
+    assert rel(q["u"], G["lbfgs_compress1_u"]) < 1e-8
+    good = FemProblem(**kw).solve(load_steps=1, solver=1, lbfgs_memory=5, precond_refresh=10)
+    assert good["converged"] and good["final_fnorm"] < 1e-9
+    assert rel(good["u"], G["compress1_ls0_u"]) < 1e-7
