@@ -235,11 +235,15 @@ def run_ours(args, rank, world, local_rank):
 
     from paper_2204_01722_b200.hexmg import FemProblem
 
-    torch.cuda.set_device(local_rank)
+    # --dist-backend gloo: every rank may share one GPU (multi-rank test mode)
+    torch.cuda.set_device(local_rank % torch.cuda.device_count())
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     # Slab `rank` of a (64 N) x 64 x 64 box; only the global -x face is fixed.
     fixed = ("-x",) if rank == 0 else ()
     prob = FemProblem(extents=(1.0, 1.0, 1.0), cells=(CELLS,) * 3, order=ORDER, fixed_faces=fixed)
@@ -526,6 +530,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-newton", action="store_true")
     ap.add_argument("--no-cfg5", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test the N > 1 path with every rank on one GPU")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))

@@ -54,14 +54,17 @@ def exchange_faces(y, npd, rank, world, dist):
 
     nx, ny, nz = npd
     v = y.view(nz, ny, nx, 3)
+    # gloo moves host buffers only (the single-GPU multi-rank test mode)
+    host = y.is_cuda and dist.get_backend() == "gloo"
+    stage = (lambda t: t.cpu()) if host else (lambda t: t)
     ops, bufs = [], {}
     if rank + 1 < world:
-        send_hi = v[:, :, nx - 1, :].contiguous()
+        send_hi = stage(v[:, :, nx - 1, :].contiguous())
         recv_hi = torch.empty_like(send_hi)
         ops += [dist.P2POp(dist.isend, send_hi, rank + 1), dist.P2POp(dist.irecv, recv_hi, rank + 1)]
         bufs["hi"] = (send_hi, recv_hi)
     if rank > 0:
-        send_lo = v[:, :, 0, :].contiguous()
+        send_lo = stage(v[:, :, 0, :].contiguous())
         recv_lo = torch.empty_like(send_lo)
         ops += [dist.P2POp(dist.isend, send_lo, rank - 1), dist.P2POp(dist.irecv, recv_lo, rank - 1)]
         bufs["lo"] = (send_lo, recv_lo)
@@ -70,10 +73,10 @@ def exchange_faces(y, npd, rank, world, dist):
             r.wait()
     if "hi" in bufs:
         s, r = bufs["hi"]
-        v[:, :, nx - 1, :] = s + r  # this rank is the lower one
+        v[:, :, nx - 1, :] = (s + r).to(y.device)  # this rank is the lower one
     if "lo" in bufs:
         s, r = bufs["lo"]
-        v[:, :, 0, :] = r + s  # the neighbour is the lower one
+        v[:, :, 0, :] = (r + s).to(y.device)  # the neighbour is the lower one
     return y
 
 
