@@ -19,6 +19,9 @@
 #include "ndchol.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <functional>
 
@@ -80,23 +83,32 @@ constexpr int kFC = 1024;   //                    columns (y1 chunk in smem)
 constexpr int kBC = 64;     // backward GEMV tile: columns (8 warps x 8)
 constexpr int kBR = 2048;   //                     rows (v chunk in smem)
 
+// The panel of a front is [W; L21] (W = L11^-1): part 0 = the np x np top
+// block (lower triangular), part 1 = the ns x np bottom block.
 struct NdSolve {
-  const int *piv0, *np, *ns, *child0, *child1, *ftile0, *btile0;
+  const int *piv0, *np, *ns, *child0, *child1;
   const long long *loff, *rows_off, *yoff, *uoff;
   const int *src0, *src1, *shell;
-  const int *ftile_front, *btile_front, *rtile_front, *rtile_rb, *ctile_front, *ctile_cb;
+  const int* ftile0[2];       // per front: first forward tile of each part
+  const int* btile0[2];       // per front: first backward tile of each part
+  const int* ftile_front[2];  // forward tile -> front
+  const int* btile_front[2];  // backward tile -> front
+  const int* rtile_front[3];  // row tiles (front, rb): 0 top, 1 bottom, 2 whole front
+  const int* rtile_rb[3];
+  const int *ctile_front, *ctile_cb;  // column tiles (front, cb)
   const double* M;
   double *w, *u, *y, *part_f, *part_b;
 };
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+__device__ __forceinline__ int part_rows(int part, int np, int ns) { return part ? ns : np; }
 
 // Forward front vector y = [w(piv); 0] + extend(u_child0) + extend(u_child1)
 // (the children's update rows gathered through the inverse extend maps).
 __global__ void __launch_bounds__(kFR) nd_fwd_assemble(NdSolve a, int rt0) {
-  const int rt = rt0 + blockIdx.x, t = a.rtile_front[rt];
+  const int rt = rt0 + blockIdx.x, t = a.rtile_front[2][rt];
   const int np = a.np[t], m = np + a.ns[t];
-  const int r = a.rtile_rb[rt] * kFR + threadIdx.x;
+  const int r = a.rtile_rb[2][rt] * kFR + threadIdx.x;
   if (r >= m) return;
   const long long yo = a.yoff[t];
   double v = r < np ? a.w[a.piv0[t] + r] : 0.0;
@@ -106,17 +118,19 @@ __global__ void __launch_bounds__(kFR) nd_fwd_assemble(NdSolve a, int rt0) {
   a.y[yo + r] = v;
 }
 
-// Tile (row block rb, column chunk cc) of M y1: one row per thread.
-__global__ void __launch_bounds__(kFR) nd_fwd_gemv(NdSolve a, int ft0) {
+// Tile (row block rb of the part, column chunk cc) of part x y[0:np]: one
+// row per thread.  Part 0: z1 = W y1; part 1: L21 z1 (z1 written back into
+// y[0:np] by the part-0 finish).
+__global__ void __launch_bounds__(kFR) nd_fwd_gemv(NdSolve a, int part, int ft0) {
   __shared__ double ys[kFC];
-  const int tile = ft0 + blockIdx.x, t = a.ftile_front[tile];
-  const int np = a.np[t], m = np + a.ns[t];
-  const int ncc = ceil_div(np, kFC), local = tile - a.ftile0[t];
+  const int tile = ft0 + blockIdx.x, t = a.ftile_front[part][tile];
+  const int np = a.np[t], ns = a.ns[t], m = np + ns, nr = part_rows(part, np, ns);
+  const int ncc = ceil_div(np, kFC), local = tile - a.ftile0[part][t];
   const int rb = local / ncc, cc = local - rb * ncc;
   const int row0 = rb * kFR, col0 = cc * kFC, ncols = min(kFC, np - col0);
-  const int rend = min(row0 + kFR, m);
+  const int rend = min(row0 + kFR, nr);
   double* out = a.part_f + (size_t)tile * kFR;
-  if (rend <= np && rend - 1 < col0) {  // strictly above the diagonal of L11^-1: zeros
+  if (part == 0 && rend - 1 < col0) {  // strictly above the diagonal of W: zeros
     out[threadIdx.x] = 0.0;
     return;
   }
@@ -125,8 +139,8 @@ __global__ void __launch_bounds__(kFR) nd_fwd_gemv(NdSolve a, int ft0) {
   __syncthreads();
   const int r = row0 + threadIdx.x;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  if (r < m) {
-    const double* col = a.M + a.loff[t] + (size_t)col0 * m + r;
+  if (r < nr) {
+    const double* col = a.M + a.loff[t] + (size_t)col0 * m + (part ? np : 0) + r;
     int k = 0;
     for (; k + 8 <= ncols; k += 8) {
       double mv[8];
@@ -140,50 +154,54 @@ __global__ void __launch_bounds__(kFR) nd_fwd_gemv(NdSolve a, int ft0) {
   out[threadIdx.x] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
-// z1 = (M y1)_top -> w(piv);  u = y2 - (M y1)_bottom -> update vector.
-__global__ void __launch_bounds__(kFR) nd_fwd_finish(NdSolve a, int rt0) {
-  const int rt = rt0 + blockIdx.x, t = a.rtile_front[rt];
-  const int np = a.np[t], m = np + a.ns[t];
-  const int rb = a.rtile_rb[rt], r = rb * kFR + threadIdx.x;
-  if (r >= m) return;
+// Part 0: z1 -> w(piv) and y[0:np]; part 1: u = y2 - L21 z1 -> update vector.
+__global__ void __launch_bounds__(kFR) nd_fwd_finish(NdSolve a, int part, int rt0) {
+  const int rt = rt0 + blockIdx.x, t = a.rtile_front[part][rt];
+  const int np = a.np[t], ns = a.ns[t], nr = part_rows(part, np, ns);
+  const int rb = a.rtile_rb[part][rt], r = rb * kFR + threadIdx.x;
+  if (r >= nr) return;
   const int ncc = ceil_div(np, kFC);
-  const double* p = a.part_f + ((size_t)a.ftile0[t] + (size_t)rb * ncc) * kFR + threadIdx.x;
+  const double* p = a.part_f + ((size_t)a.ftile0[part][t] + (size_t)rb * ncc) * kFR + threadIdx.x;
   double s = 0.0;
   for (int cc = 0; cc < ncc; ++cc) s += p[(size_t)cc * kFR];
-  if (r < np)
+  const long long yo = a.yoff[t];
+  if (part == 0) {
     a.w[a.piv0[t] + r] = s;
-  else
-    a.u[a.uoff[t] + (r - np)] = a.y[a.yoff[t] + r] - s;
+    a.y[yo + r] = s;
+  } else {
+    a.u[a.uoff[t] + r] = a.y[yo + np + r] - s;
+  }
 }
 
-// Backward front vector v = [z1; -x2] (x2 = ancestor solution values).
+// Backward front vector [z1; x2] (x2 = ancestor solution values).
 __global__ void __launch_bounds__(kFR) nd_bwd_assemble(NdSolve a, int rt0) {
-  const int rt = rt0 + blockIdx.x, t = a.rtile_front[rt];
+  const int rt = rt0 + blockIdx.x, t = a.rtile_front[2][rt];
   const int np = a.np[t], m = np + a.ns[t];
-  const int r = a.rtile_rb[rt] * kFR + threadIdx.x;
+  const int r = a.rtile_rb[2][rt] * kFR + threadIdx.x;
   if (r >= m) return;
-  a.y[a.yoff[t] + r] = r < np ? a.w[a.piv0[t] + r] : -a.w[a.shell[a.rows_off[t] + (r - np)]];
+  a.y[a.yoff[t] + r] = r < np ? a.w[a.piv0[t] + r] : a.w[a.shell[a.rows_off[t] + (r - np)]];
 }
 
-// Tile (column block cb, row chunk rc) of M^T v: 8 warps x 8 columns, lanes
-// stride the (contiguous) column, fixed-order warp reduction.
-__global__ void __launch_bounds__(256) nd_bwd_gemv(NdSolve a, int bt0) {
+// Tile (column block cb, row chunk rc of the part) of part^T v: 8 warps x 8
+// columns, lanes stride the (contiguous) column, fixed-order warp reduction.
+// Part 1: L21^T x2; part 0: W^T t.
+__global__ void __launch_bounds__(256) nd_bwd_gemv(NdSolve a, int part, int bt0) {
   __shared__ double vs[kBR];
-  const int tile = bt0 + blockIdx.x, t = a.btile_front[tile];
-  const int np = a.np[t], m = np + a.ns[t];
-  const int nrc = ceil_div(m, kBR), local = tile - a.btile0[t];
+  const int tile = bt0 + blockIdx.x, t = a.btile_front[part][tile];
+  const int np = a.np[t], ns = a.ns[t], m = np + ns, nr = part_rows(part, np, ns);
+  const int nrc = ceil_div(nr, kBR), local = tile - a.btile0[part][t];
   const int cb = local / nrc, rc = local - cb * nrc;
-  const int col0 = cb * kBC, row0 = rc * kBR, nrows = min(kBR, m - row0);
+  const int col0 = cb * kBC, row0 = rc * kBR, nrows = min(kBR, nr - row0);
   double* out = a.part_b + (size_t)tile * kBC;
-  if (row0 + nrows <= col0) {  // rows above the diagonal block of every column: zeros
+  if (part == 0 && row0 + nrows <= col0) {  // rows above the diagonal of every column: zeros
     if (threadIdx.x < kBC) out[threadIdx.x] = 0.0;
     return;
   }
-  const long long yo = a.yoff[t];
+  const long long yo = a.yoff[t] + (part ? np : 0);
   for (int k = threadIdx.x; k < nrows; k += 256) vs[k] = a.y[yo + row0 + k];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* base = a.M + a.loff[t] + row0;
+  const double* base = a.M + a.loff[t] + (part ? np : 0) + row0;
   double acc[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) acc[q] = 0.0;
@@ -207,19 +225,21 @@ __global__ void __launch_bounds__(256) nd_bwd_gemv(NdSolve a, int bt0) {
   }
 }
 
-// x1 = sum over row chunks -> w(piv).
-__global__ void __launch_bounds__(kBC) nd_bwd_finish(NdSolve a, int ct0) {
+// Part 1: t = z1 - L21^T x2 -> y[0:np]; part 0: x1 = W^T t -> w(piv).
+__global__ void __launch_bounds__(kBC) nd_bwd_finish(NdSolve a, int part, int ct0) {
   const int ct = ct0 + blockIdx.x, t = a.ctile_front[ct];
-  const int np = a.np[t], m = np + a.ns[t];
+  const int np = a.np[t], ns = a.ns[t], nr = part_rows(part, np, ns);
   const int cb = a.ctile_cb[ct], j = cb * kBC + threadIdx.x;
   if (j >= np) return;
-  const int nrc = ceil_div(m, kBR);
-  const double* p = a.part_b + ((size_t)a.btile0[t] + (size_t)cb * nrc) * kBC + threadIdx.x;
+  const int nrc = ceil_div(nr, kBR);
+  const double* p = a.part_b + ((size_t)a.btile0[part][t] + (size_t)cb * nrc) * kBC + threadIdx.x;
   double s = 0.0;
   for (int rc = 0; rc < nrc; ++rc) s += p[(size_t)rc * kBC];
-  a.w[a.piv0[t] + j] = s;
+  if (part == 1)
+    a.y[a.yoff[t] + j] -= s;
+  else
+    a.w[a.piv0[t] + j] = s;
 }
-
 
 void cublas_check(cublasStatus_t s, const char* what) {
   if (s != CUBLAS_STATUS_SUCCESS) throw Error(HXG_ERR_CUDA, std::string(what) + " failed");
@@ -375,32 +395,40 @@ void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
   levels_.assign((size_t)maxlev + 1, {});
   for (int t = 0; t < nf; ++t) levels_[(size_t)fronts_[(size_t)t].level].push_back(t);
   auto cdiv = [](long long x, long long y) { return (int)((x + y - 1) / y); };
-  std::vector<int> piv0(nf), np(nf), ns(nf), c0(nf), c1(nf), ft0(nf), bt0(nf);
+  std::vector<int> piv0(nf), np(nf), ns(nf), c0(nf), c1(nf);
+  std::vector<int> ft0[2] = {std::vector<int>(nf), std::vector<int>(nf)};
+  std::vector<int> bt0[2] = {std::vector<int>(nf), std::vector<int>(nf)};
   std::vector<long long> loff(nf), roff(nf), yoff(nf), uoff(nf);
-  std::vector<int> ftf, btf, rtf, rtb, ctf, ctb;
-  lev_ft_.assign(levels_.size() + 1, 0);
-  lev_bt_ = lev_rt_ = lev_ct_ = lev_ft_;
+  std::vector<int> ftf[2], btf[2], rtf[3], rtb[3], ctf, ctb;
+  for (int q = 0; q < 2; ++q) {
+    lev_ft_[q].assign(levels_.size() + 1, 0);
+    lev_bt_[q].assign(levels_.size() + 1, 0);
+  }
+  for (int q = 0; q < 3; ++q) lev_rt_[q].assign(levels_.size() + 1, 0);
+  lev_ct_.assign(levels_.size() + 1, 0);
   long long ucount = 0, ycount = 0;
-  for (size_t l = 0; l < levels_.size(); ++l) {
-    lev_ft_[l] = (int)ftf.size();
-    lev_bt_[l] = (int)btf.size();
-    lev_rt_[l] = (int)rtf.size();
+  for (size_t l = 0; l <= levels_.size(); ++l) {
+    for (int q = 0; q < 2; ++q) {
+      lev_ft_[q][l] = (int)ftf[q].size();
+      lev_bt_[q][l] = (int)btf[q].size();
+    }
+    for (int q = 0; q < 3; ++q) lev_rt_[q][l] = (int)rtf[q].size();
     lev_ct_[l] = (int)ctf.size();
+    if (l == levels_.size()) break;
     for (int t : levels_[l]) {
       const Front& f = fronts_[(size_t)t];
-      const int m = f.np + f.ns;
-      ft0[t] = (int)ftf.size();
-      for (int k = 0, n = cdiv(m, kFR) * cdiv(f.np, kFC); k < n; ++k) ftf.push_back(t);
-      bt0[t] = (int)btf.size();
-      for (int k = 0, n = cdiv(f.np, kBC) * cdiv(m, kBR); k < n; ++k) btf.push_back(t);
-      for (int rb = 0; rb < cdiv(m, kFR); ++rb) rtf.push_back(t), rtb.push_back(rb);
+      const int rows[3] = {f.np, f.ns, f.np + f.ns};
+      for (int q = 0; q < 2; ++q) {
+        ft0[q][t] = (int)ftf[q].size();
+        for (int k = 0, n = cdiv(rows[q], kFR) * cdiv(f.np, kFC); k < n; ++k) ftf[q].push_back(t);
+        bt0[q][t] = (int)btf[q].size();
+        for (int k = 0, n = cdiv(f.np, kBC) * cdiv(rows[q], kBR); k < n; ++k) btf[q].push_back(t);
+      }
+      for (int q = 0; q < 3; ++q)
+        for (int rb = 0; rb < cdiv(rows[q], kFR); ++rb) rtf[q].push_back(t), rtb[q].push_back(rb);
       for (int cb = 0; cb < cdiv(f.np, kBC); ++cb) ctf.push_back(t), ctb.push_back(cb);
     }
   }
-  lev_ft_[levels_.size()] = (int)ftf.size();
-  lev_bt_[levels_.size()] = (int)btf.size();
-  lev_rt_[levels_.size()] = (int)rtf.size();
-  lev_ct_[levels_.size()] = (int)ctf.size();
   for (int t = 0; t < nf; ++t) {
     const Front& f = fronts_[(size_t)t];
     piv0[t] = f.piv0;
@@ -443,24 +471,28 @@ void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
   up(dfront_ns_, ns);
   up(c0_, c0);
   up(c1_, c1);
-  up(ftile0_, ft0);
-  up(btile0_, bt0);
+  for (int q = 0; q < 2; ++q) {
+    up(ftile0_[q], ft0[q]);
+    up(btile0_[q], bt0[q]);
+    up(ftile_front_[q], ftf[q]);
+    up(btile_front_[q], btf[q]);
+  }
+  for (int q = 0; q < 3; ++q) {
+    up(rtile_front_[q], rtf[q]);
+    up(rtile_rb_[q], rtb[q]);
+  }
   dfront_loff_.upload(loff);
   dfront_rows_off_.upload(roff);
   yoff_.upload(yoff);
   uoff_.upload(uoff);
   up(src0_, src0);
   up(src1_, src1);
-  up(ftile_front_, ftf);
-  up(btile_front_, btf);
-  up(rtile_front_, rtf);
-  up(rtile_rb_, rtb);
   up(ctile_front_, ctf);
   up(ctile_cb_, ctb);
   ubuf_.alloc((size_t)std::max<long long>(ucount, 1));
   yvec_.alloc((size_t)std::max<long long>(ycount, 1));
-  part_f_.alloc(std::max<size_t>(ftf.size(), 1) * kFR);
-  part_b_.alloc(std::max<size_t>(btf.size(), 1) * kBC);
+  part_f_.alloc(std::max<size_t>(std::max(ftf[0].size(), ftf[1].size()), 1) * kFR);
+  part_b_.alloc(std::max<size_t>(std::max(btf[0].size(), btf[1].size()), 1) * kBC);
   L_.alloc(lsize_);
   size_t maxnp = 1;
   for (const auto& f : fronts_) maxnp = std::max(maxnp, (size_t)f.np);
@@ -674,15 +706,13 @@ void NdCholesky::factor_front(int t, Lane& L, const CsrMatrix& a,
   chol_inv(L, W, m, L.inv.p, f.np, f.np, info_.p + t);
   double* Lp = L_.p + f.loff;
   if (f.ns > 0) {
+    // L21 = A21 W^T straight into the factor panel, then S = A22 - L21 L21^T
     cublas_check(cublasDgemm(L.cublas, CUBLAS_OP_N, CUBLAS_OP_T, f.ns, f.np, f.np, &one, W + f.np,
-                             m, L.inv.p, f.np, &zero, L.tmp.p, f.ns),
+                             m, L.inv.p, f.np, &zero, Lp + f.np, m),
                  "gemm (L21)");
     cublas_check(cublasDsyrk(L.cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, f.ns, f.np, &minus_one,
-                             L.tmp.p, f.ns, &one, W + f.np + (size_t)f.np * m, m),
+                             Lp + f.np, m, &one, W + f.np + (size_t)f.np * m, m),
                  "syrk");
-    cublas_check(cublasDgemm(L.cublas, CUBLAS_OP_N, CUBLAS_OP_N, f.ns, f.np, f.np, &one, L.tmp.p,
-                             f.ns, L.inv.p, f.np, &zero, Lp + f.np, m),
-                 "gemm (L21 L11^-1)");
   }
   HXG_CUDA(cudaMemcpy2DAsync(Lp, sizeof(double) * m, L.inv.p, sizeof(double) * f.np,
                              sizeof(double) * f.np, f.np, cudaMemcpyDeviceToDevice, s));
@@ -742,7 +772,19 @@ void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s)
     HXG_CUDA(cudaEventRecord(lanes_[li]->done, lanes_[li]->stream));
     HXG_CUDA(cudaStreamWaitEvent(s, lanes_[li]->done, 0));
   }
+  static const bool prof = std::getenv("HXG_PROFILE") != nullptr;
+  std::chrono::steady_clock::time_point t0;
+  if (prof) {
+    HXG_CUDA(cudaStreamSynchronize(s));
+    t0 = std::chrono::steady_clock::now();
+  }
   for (int t : top.fronts) factor_front(t, top, a, stacks[0]);
+  if (prof) {
+    HXG_CUDA(cudaStreamSynchronize(s));
+    std::fprintf(stderr, "[hxg]   top fronts (%zu) %.2f ms\n", top.fronts.size(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                     .count());
+  }
   std::vector<int> info(fronts_.size());
   HXG_CUDA(cudaMemcpyAsync(info.data(), info_.p, sizeof(int) * info.size(),
                            cudaMemcpyDeviceToHost, s));
@@ -762,8 +804,6 @@ void NdCholesky::solve(const double* b, double* x, cudaStream_t s) {
   a.ns = dfront_ns_.p;
   a.child0 = c0_.p;
   a.child1 = c1_.p;
-  a.ftile0 = ftile0_.p;
-  a.btile0 = btile0_.p;
   a.loff = dfront_loff_.p;
   a.rows_off = dfront_rows_off_.p;
   a.yoff = yoff_.p;
@@ -771,10 +811,16 @@ void NdCholesky::solve(const double* b, double* x, cudaStream_t s) {
   a.src0 = src0_.p;
   a.src1 = src1_.p;
   a.shell = shell_rows_.p;
-  a.ftile_front = ftile_front_.p;
-  a.btile_front = btile_front_.p;
-  a.rtile_front = rtile_front_.p;
-  a.rtile_rb = rtile_rb_.p;
+  for (int q = 0; q < 2; ++q) {
+    a.ftile0[q] = ftile0_[q].p;
+    a.btile0[q] = btile0_[q].p;
+    a.ftile_front[q] = ftile_front_[q].p;
+    a.btile_front[q] = btile_front_[q].p;
+  }
+  for (int q = 0; q < 3; ++q) {
+    a.rtile_front[q] = rtile_front_[q].p;
+    a.rtile_rb[q] = rtile_rb_[q].p;
+  }
   a.ctile_front = ctile_front_.p;
   a.ctile_cb = ctile_cb_.p;
   a.M = L_.p;
@@ -783,25 +829,31 @@ void NdCholesky::solve(const double* b, double* x, cudaStream_t s) {
   a.y = yvec_.p;
   a.part_f = part_f_.p;
   a.part_b = part_b_.p;
+  auto n_of = [](const std::vector<int>& lev, size_t l) { return lev[l + 1] - lev[l]; };
   permute_gather<<<grid_for(n_, 256), 256, 0, s>>>(b, perm_.p, n_, wvec_.p);
-  // Forward: deepest level first.
+  // Forward, deepest level first: y = [y1; y2] assembled; z1 = W y1;
+  // u = y2 - L21 z1 passed up.
   for (int l = (int)levels_.size() - 1; l >= 0; --l) {
-    const int nrt = lev_rt_[(size_t)l + 1] - lev_rt_[(size_t)l];
-    const int nft = lev_ft_[(size_t)l + 1] - lev_ft_[(size_t)l];
-    if (!nrt) continue;
-    nd_fwd_assemble<<<nrt, kFR, 0, s>>>(a, lev_rt_[(size_t)l]);
-    nd_fwd_gemv<<<nft, kFR, 0, s>>>(a, lev_ft_[(size_t)l]);
-    nd_fwd_finish<<<nrt, kFR, 0, s>>>(a, lev_rt_[(size_t)l]);
+    const size_t L = (size_t)l;
+    if (!n_of(lev_rt_[2], L)) continue;
+    nd_fwd_assemble<<<n_of(lev_rt_[2], L), kFR, 0, s>>>(a, lev_rt_[2][L]);
+    for (int part = 0; part < 2; ++part) {
+      if (n_of(lev_ft_[part], L))
+        nd_fwd_gemv<<<n_of(lev_ft_[part], L), kFR, 0, s>>>(a, part, lev_ft_[part][L]);
+      if (n_of(lev_rt_[part], L))
+        nd_fwd_finish<<<n_of(lev_rt_[part], L), kFR, 0, s>>>(a, part, lev_rt_[part][L]);
+    }
   }
-  // Backward: root first.
+  // Backward, root first: t = z1 - L21^T x2; x1 = W^T t.
   for (size_t l = 0; l < levels_.size(); ++l) {
-    const int nrt = lev_rt_[l + 1] - lev_rt_[l];
-    const int nbt = lev_bt_[l + 1] - lev_bt_[l];
-    const int nct = lev_ct_[l + 1] - lev_ct_[l];
-    if (!nrt) continue;
-    nd_bwd_assemble<<<nrt, kFR, 0, s>>>(a, lev_rt_[l]);
-    nd_bwd_gemv<<<nbt, 256, 0, s>>>(a, lev_bt_[l]);
-    nd_bwd_finish<<<nct, kBC, 0, s>>>(a, lev_ct_[l]);
+    if (!n_of(lev_rt_[2], l)) continue;
+    nd_bwd_assemble<<<n_of(lev_rt_[2], l), kFR, 0, s>>>(a, lev_rt_[2][l]);
+    for (int part = 1; part >= 0; --part) {
+      if (n_of(lev_bt_[part], l))
+        nd_bwd_gemv<<<n_of(lev_bt_[part], l), 256, 0, s>>>(a, part, lev_bt_[part][l]);
+      if (part == 0 || n_of(lev_bt_[part], l))
+        nd_bwd_finish<<<n_of(lev_ct_, l), kBC, 0, s>>>(a, part, lev_ct_[l]);
+    }
   }
   permute_scatter<<<grid_for(n_, 256), 256, 0, s>>>(wvec_.p, perm_.p, n_, x);
   HXG_CUDA(cudaGetLastError());

@@ -1,10 +1,10 @@
 // On-device sparse Cholesky of the assembled p = 1 coarse operator
 // (CholeskyCoarseSolver, coarse_solver.hpp:16-47, which uses Eigen's
 // SimplicialLLT): geometric nested dissection of the Q1 node lattice and a
-// multifrontal LL^T with dense fronts factored by cuSOLVER/cuBLAS FP64.  Each
-// front keeps its panel in inverse form M = [L11^-1; L21 L11^-1], so the
-// per-V-cycle triangular solves are one bandwidth-bound GEMV per front and
-// direction, batched over every front of a dissection-tree level.
+// multifrontal LL^T with dense fronts factored on FP64 tensor-core GEMMs.
+// Each front keeps its panel as [L11^-1; L21], so the per-V-cycle triangular
+// solves are bandwidth-bound GEMVs (two dependent ones per front and
+// direction), batched over every front of a dissection-tree level.
 #pragma once
 
 #include <cublas_v2.h>
@@ -77,12 +77,15 @@ class NdCholesky {
   DevBuf<double> part_f_, part_b_;  // GEMV tile partial sums
   DevBuf<int> info_;
   // Per-front solve metadata and the tile lists (see ndchol.cu).
-  DevBuf<int> dfront_piv0_, dfront_np_, dfront_ns_, c0_, c1_, ftile0_, btile0_;
+  DevBuf<int> dfront_piv0_, dfront_np_, dfront_ns_, c0_, c1_;
   DevBuf<long long> dfront_loff_, dfront_rows_off_, yoff_, uoff_;
   DevBuf<int> src0_, src1_;  // front position -> child update index (or -1)
-  DevBuf<int> ftile_front_, btile_front_, rtile_front_, rtile_rb_, ctile_front_, ctile_cb_;
-  // Per level: [begin, end) into the forward / backward / row / column tile lists.
-  std::vector<int> lev_ft_, lev_bt_, lev_rt_, lev_ct_;
+  // GEMV tiles per panel part (0 = W block, 1 = L21 block), row tiles per
+  // part and for the whole front (2), column tiles.
+  DevBuf<int> ftile0_[2], btile0_[2], ftile_front_[2], btile_front_[2];
+  DevBuf<int> rtile_front_[3], rtile_rb_[3], ctile_front_, ctile_cb_;
+  // Per level: [begin, end) into the tile lists.
+  std::vector<int> lev_ft_[2], lev_bt_[2], lev_rt_[3], lev_ct_;
   std::vector<size_t> asm_begin_;  // per front range in the assembly lists
 };
 
