@@ -142,12 +142,12 @@ __global__ void __launch_bounds__(kFR) nd_fwd_gemv(NdSolve a, int part, int ft0)
   if (r < nr) {
     const double* col = a.M + a.loff[t] + (size_t)col0 * m + (part ? np : 0) + r;
     int k = 0;
-    for (; k + 8 <= ncols; k += 8) {
-      double mv[8];
+    for (; k + 16 <= ncols; k += 16) {  // 16 loads in flight per thread
+      double mv[16];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) mv[q] = __ldg(col + (size_t)(k + q) * m);
+      for (int q = 0; q < 16; ++q) mv[q] = __ldg(col + (size_t)(k + q) * m);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q & 3] = fma(mv[q], ys[k + q], acc[q & 3]);
+      for (int q = 0; q < 16; ++q) acc[q & 3] = fma(mv[q], ys[k + q], acc[q & 3]);
     }
     for (; k < ncols; ++k) acc[k & 3] = fma(__ldg(col + (size_t)k * m), ys[k], acc[k & 3]);
   }
@@ -206,11 +206,29 @@ __global__ void __launch_bounds__(256) nd_bwd_gemv(NdSolve a, int part, int bt0)
 #pragma unroll
   for (int q = 0; q < 8; ++q) acc[q] = 0.0;
   const int j0 = col0 + warp * 8;
-  for (int k = lane; k < nrows; k += 32) {
+  const int nq = min(8, np - j0);  // columns of this warp (warp-uniform)
+  // 4 row strides per step: 32 loads in flight per lane
+  int k = lane;
+  if (nq == 8) {
+    for (; k + 96 < nrows; k += 128) {
+      double mv[4][8];
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mv[h][q] = __ldg(base + (size_t)(j0 + q) * m + k + 32 * h);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double vk = vs[k + 32 * h];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = fma(mv[h][q], vk, acc[q]);
+      }
+    }
+  }
+  for (; k < nrows; k += 32) {
     const double vk = vs[k];
 #pragma unroll
     for (int q = 0; q < 8; ++q)
-      if (j0 + q < np) acc[q] = fma(__ldg(base + (size_t)(j0 + q) * m + k), vk, acc[q]);
+      if (q < nq) acc[q] = fma(__ldg(base + (size_t)(j0 + q) * m + k), vk, acc[q]);
   }
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
