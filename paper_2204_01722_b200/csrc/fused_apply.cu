@@ -26,7 +26,7 @@
 #include "operator.hpp"
 
 #ifndef HXG_EXPERIMENT
-#define HXG_EXPERIMENT 0
+#define HXG_EXPERIMENT 0  // 4: per-phase clock64 accounting (scripts/phase_times.py)
 #endif
 #ifndef HXG_MINB_HIGHP
 #define HXG_MINB_HIGHP 3
@@ -42,15 +42,6 @@
 #endif
 #ifndef HXG_SLOTS_Q4
 #define HXG_SLOTS_Q4 0
-#endif
-#ifndef HXG_NSG_Q2
-#define HXG_NSG_Q2 3
-#endif
-#ifndef HXG_NSH_Q2
-#define HXG_NSH_Q2 3
-#endif
-#ifndef HXG_STATE_PF
-#define HXG_STATE_PF 0  // software-pipelined state loads (needs register headroom)
 #endif
 #ifndef HXG_SLOTS_HIGHP
 #define HXG_SLOTS_HIGHP 0
@@ -209,7 +200,6 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
   // brick's quadrature state is one contiguous run, pulled into L2 one brick
   // ahead so the q-function loads hit L2.
   auto prefetch_state = [&](int b) {
-#if HXG_EXPERIMENT != 1
     constexpr unsigned bytes = (unsigned)(sizeof(double) * Q * kStateStride * T);
     constexpr unsigned chunk = 32768;
     const char* base = reinterpret_cast<const char*>(
@@ -217,7 +207,6 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
 #pragma unroll
     for (unsigned off = 0; off < bytes; off += chunk)
       prefetch_l2(base + off, off + chunk <= bytes ? chunk : bytes - off);
-#endif
   };
   if (tid == 0 && (int)blockIdx.x < prm.nbricks) prefetch_state(prm.brick0 + blockIdx.x);
 #if HXG_EXPERIMENT == 4
@@ -438,25 +427,14 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
   // does not forward them back into registers.
   // NSG / NSH planes of the gradients / q-function outputs live in the
   // slots, the rest in registers.
-  constexpr int NSG = fused_slots(P, Q) ? (P * 10 + Q == 23 ? HXG_NSG_Q2 : N) : 0;
-  constexpr int NSH = fused_slots(P, Q) ? (P * 10 + Q == 23 ? HXG_NSH_Q2 : N) : 0;
+  constexpr int NSG = fused_slots(P, Q) ? N : 0;
+  constexpr int NSH = NSG;
   constexpr int QR = Q - NSG, QH = Q - NSH;
   volatile double* slot = S + te;
   double g[3][3][QR > 0 ? QR : 1];
   double hr[3][3][QH > 0 ? QH : 1];
   const double* sp0 = st_brick + tid;
   const unsigned long long pol_stream = policy_evict_first();
-#if HXG_STATE_PF
-  // plane 0's state requested before the z pass; plane qz+1's before the
-  // q-function of plane qz
-  double stn[kStateStride];
-  auto load_state = [&](int qz) {
-    const double* sp = sp0 + qz * T * kStateStride;
-#pragma unroll
-    for (int s = 0; s < kStateStride; ++s) stn[s] = valid ? ld_stream(sp + s * T, pol_stream) : 0.0;
-  };
-  load_state(0);
-#endif
   auto gslot = [&](int c, int d, int z) { return ((c * 3 + d) * N + z) * Q2; };
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -492,38 +470,20 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
     double H[9];
-#if HXG_STATE_PF
-    double st[kStateStride];
-#pragma unroll
-    for (int s = 0; s < kStateStride; ++s) st[s] = stn[s];
-    if (qz + 1 < Q) load_state(qz + 1);
-#endif
     if (valid) {
-#if !HXG_STATE_PF
       double st[kStateStride];
       const double* sp = sp0 + qz * T * kStateStride;
 #pragma unroll
       for (int s = 0; s < kStateStride; ++s) {
-#if HXG_EXPERIMENT == 1
-        st[s] = 1.0 + 0.01 * s + 1e-3 * tid + 0.0 * sp[0];
-#else
         st[s] = ld_stream(sp + s * T, pol_stream);
-#endif
       }
-#endif
       double G[9];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int d = 0; d < 3; ++d)
           G[3 * c + d] = qz < NSG ? slot[gslot(c, d, qz)] : g[c][d][qz - NSG];
-#if HXG_EXPERIMENT == 2
-      // timing experiment: trivial q-function (state still loaded)
-#pragma unroll
-      for (int q9 = 0; q9 < 9; ++q9) H[q9] = G[q9] * st[q9] + st[q9 + 8];
-#else
       jacobian_qf(prm.mu, prm.lambda, G, st, H);
-#endif
       if (prm.perturb != 0.0) {  // fault-injection hook: + eps w detJ G
         const double wdet =
             prm.geo[((size_t)lay.brick_points() * brick + (size_t)qz * T) * kGeoStride + 9 * T + tid];
@@ -610,12 +570,6 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
   }
   __syncthreads(); HXG_PHASE(4);
 
-#if HXG_EXPERIMENT == 3
-  // timing experiment: no overlap-add / stores of y
-  if (tid == 0 && brick < 0) prm.y[0] = Ebase[0];
-  __syncthreads(); HXG_PHASE(5);
-  continue;
-#endif
   // ---- overlap-add fused with the stores: node-centric ------------------
   // Node (ix, iy, iz) of the block sums the outputs of the elements sharing
   // it, lower element first in x, then y, then z: a fixed order (the
