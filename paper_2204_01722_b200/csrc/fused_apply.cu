@@ -38,10 +38,10 @@
 #define HXG_SLOTS_Q2 1
 #endif
 #ifndef HXG_MINB_Q4
-#define HXG_MINB_Q4 2
+#define HXG_MINB_Q4 3
 #endif
 #ifndef HXG_SLOTS_Q4
-#define HXG_SLOTS_Q4 0
+#define HXG_SLOTS_Q4 1
 #endif
 #ifndef HXG_SLOTS_HIGHP
 #define HXG_SLOTS_HIGHP 0
