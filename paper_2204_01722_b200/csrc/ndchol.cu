@@ -78,10 +78,16 @@ __global__ void permute_scatter(const double* __restrict__ w, const int* __restr
     x[perm[i]] = w[i];
 }
 
-constexpr int kFR = 256;    // forward GEMV tile: rows (threads)
-constexpr int kFC = 1024;   //                    columns (y1 chunk in smem)
-constexpr int kBC = 64;     // backward GEMV tile: columns (8 warps x 8)
-constexpr int kBR = 2048;   //                     rows (v chunk in smem)
+#ifndef HXG_ND_FC
+#define HXG_ND_FC 128
+#endif
+#ifndef HXG_ND_BR
+#define HXG_ND_BR 512
+#endif
+constexpr int kFR = 256;        // forward GEMV tile: rows (threads)
+constexpr int kFC = HXG_ND_FC;  //                    columns (vector chunk in smem)
+constexpr int kBC = 64;         // backward GEMV tile: columns (8 warps x 8)
+constexpr int kBR = HXG_ND_BR;  //                     rows (vector chunk in smem)
 
 // The panel of a front is [W; L21] (W = L11^-1): part 0 = the np x np top
 // block (lower triangular), part 1 = the ns x np bottom block.
