@@ -567,19 +567,31 @@ void NdCholesky::plan_lanes() {
     }
   }
   lanes_.clear();
-  lanes_.resize(roots.size() + 1);  // lane 0 = top fronts on the caller's stream
+  lanes_.resize(roots.size() + 1);  // lane 0 = the caller's stream
   for (auto& l : lanes_) l = std::make_unique<Lane>();
   lane_of_.assign((size_t)nf, 0);
-  for (int t = 0; t < nf; ++t) {
-    const int l = sub[(size_t)t] + 1;
-    lane_of_[(size_t)t] = l;
-    lanes_[(size_t)l]->fronts.push_back(t);
+  top_.clear();
+  for (int t = 0; t < nf; ++t) {  // postorder: children before parents
+    const Front& f = fronts_[(size_t)t];
+    if (sub[(size_t)t] >= 0) {
+      lane_of_[(size_t)t] = sub[(size_t)t] + 1;
+      lanes_[(size_t)lane_of_[(size_t)t]]->fronts.push_back(t);
+    } else {
+      // a front above the lane depth runs on its first child's lane, after
+      // the other child's lane has finished that child
+      lane_of_[(size_t)t] = depth > 0 && f.child[0] >= 0 ? lane_of_[(size_t)f.child[0]] : 0;
+      if (depth > 0)
+        top_.push_back(t);
+      else
+        lanes_[0]->fronts.push_back(t);
+    }
   }
   handoff_off_.assign((size_t)nf, (size_t)-1);
   size_t hsize = 0;
-  for (int r : roots) {
-    handoff_off_[(size_t)r] = hsize;
-    hsize += (size_t)fronts_[(size_t)r].ns * fronts_[(size_t)r].ns;
+  for (int t = 0; t < nf; ++t) {
+    if (depth == 0 || fronts_[(size_t)t].level > depth) continue;
+    handoff_off_[(size_t)t] = hsize;  // subtree roots and the fronts above them
+    hsize += (size_t)fronts_[(size_t)t].ns * fronts_[(size_t)t].ns;
   }
   handoff_.alloc(std::max<size_t>(hsize, 1));
   for (size_t li = 0; li < lanes_.size(); ++li) {
@@ -594,7 +606,10 @@ void NdCholesky::plan_lanes() {
       throw Error(HXG_ERR_CUDA, "cusolverDnCreate failed");
     size_t mw = 1, mi = 1, mt = 1, mp = 1, mtd = 1, mth = 1, cur = 0, peak = 1;
     std::vector<size_t> st;
-    for (int t : L.fronts) {
+    std::vector<int> mine = L.fronts;
+    for (int t : top_)
+      if (lane_of_[(size_t)t] == (int)li) mine.push_back(t);
+    for (int t : mine) {
       const Front& f = fronts_[(size_t)t];
       const size_t m = (size_t)f.np + f.ns;
       mw = std::max(mw, m * m);
@@ -792,20 +807,33 @@ void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s)
       }
     }
   }
+  static const bool prof = std::getenv("HXG_PROFILE") != nullptr;
+  std::chrono::steady_clock::time_point t0;
+  if (prof) {
+    for (auto& l : lanes_) HXG_CUDA(cudaStreamSynchronize(l->stream));
+    t0 = std::chrono::steady_clock::now();
+  }
+  // Fronts above the lane depth, in postorder, each on its first child's
+  // lane once the other child's lane has finished (up to 2^level fronts of a
+  // level run concurrently).
+  for (int t : top_) {
+    Lane& L = *lanes_[(size_t)lane_of_[(size_t)t]];
+    for (int c : fronts_[(size_t)t].child) {
+      if (c < 0 || lane_of_[(size_t)c] == lane_of_[(size_t)t]) continue;
+      Lane& C = *lanes_[(size_t)lane_of_[(size_t)c]];
+      HXG_CUDA(cudaEventRecord(C.done, C.stream));
+      HXG_CUDA(cudaStreamWaitEvent(L.stream, C.done, 0));
+    }
+    factor_front(t, L, a, stacks[(size_t)lane_of_[(size_t)t]]);
+  }
+  for (int t : top.fronts) factor_front(t, top, a, stacks[0]);  // depth-0 trees
   for (size_t li = 1; li < lanes_.size(); ++li) {
     HXG_CUDA(cudaEventRecord(lanes_[li]->done, lanes_[li]->stream));
     HXG_CUDA(cudaStreamWaitEvent(s, lanes_[li]->done, 0));
   }
-  static const bool prof = std::getenv("HXG_PROFILE") != nullptr;
-  std::chrono::steady_clock::time_point t0;
   if (prof) {
     HXG_CUDA(cudaStreamSynchronize(s));
-    t0 = std::chrono::steady_clock::now();
-  }
-  for (int t : top.fronts) factor_front(t, top, a, stacks[0]);
-  if (prof) {
-    HXG_CUDA(cudaStreamSynchronize(s));
-    std::fprintf(stderr, "[hxg]   top fronts (%zu) %.2f ms\n", top.fronts.size(),
+    std::fprintf(stderr, "[hxg]   fronts above the lanes (%zu) %.2f ms\n", top_.size(),
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
                      .count());
   }

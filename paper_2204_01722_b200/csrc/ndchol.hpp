@@ -69,6 +69,7 @@ class NdCholesky {
                     std::vector<std::pair<size_t, int>>& stack);
   std::vector<std::unique_ptr<Lane>> lanes_;
   std::vector<int> lane_of_;
+  std::vector<int> top_;  // fronts above the lane depth (postorder)
   std::vector<size_t> handoff_off_;  // subtree roots: offset of the handed-over update
   DevBuf<double> handoff_;
   DevBuf<double> wvec_;      // solve work vector (new numbering)
