@@ -33,7 +33,10 @@ namespace {
 
 constexpr int kLeafNodes = 128;
 constexpr int kLaneDepth = 4;
-constexpr int kCholBase = 256;  // cuSOLVER potrf / trtri below this block size  // 16 concurrent subtree lanes in the factorization
+#ifndef HXG_CHOL_BASE
+#define HXG_CHOL_BASE 512
+#endif
+constexpr int kCholBase = HXG_CHOL_BASE;  // cuSOLVER potrf / trtri below this block size
 
 __global__ void assemble_kernel(const long long* __restrict__ dst, const int* __restrict__ src,
                                 long long n, const double* __restrict__ vals, double* front) {
