@@ -369,43 +369,43 @@ void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
     const size_t m = (size_t)f.np + f.ns;
     lsize_ += m * (size_t)f.np;
   }
-  // Position of a new index within front t's rows (pivots then shell).
-  auto pos_in = [&](int t, int ni) -> int {
-    const Front& f = fronts_[(size_t)t];
-    if (ni >= f.piv0 && ni < f.piv0 + f.np) return ni - f.piv0;
-    const auto& sh = shell[(size_t)t];
-    auto it = std::lower_bound(sh.begin(), sh.end(), ni);
-    if (it == sh.end() || *it != ni) return -1;
-    return f.np + (int)(it - sh.begin());
-  };
   std::vector<int> maps;
+  std::vector<int> spos((size_t)n_, -1);  // dense front-row lookup (filled per front)
   for (int t = 0; t < nf; ++t) {
     Front& f = fronts_[(size_t)t];
+    const auto& sh = shell[(size_t)t];
+    for (size_t i = 0; i < sh.size(); ++i) spos[(size_t)sh[i]] = f.np + (int)i;
     for (int q = 0; q < 2; ++q) {
       int c = f.child[q];
       f.map_off[q] = maps.size();
       if (c < 0) continue;
       for (int ni : shell[(size_t)c]) {
-        int p = pos_in(t, ni);
+        const int p = ni >= f.piv0 && ni < f.piv0 + f.np ? ni - f.piv0 : spos[(size_t)ni];
         if (p < 0) throw Error(HXG_ERR_GENERIC, "child update row missing from parent front");
         maps.push_back(p);
       }
     }
+    for (int r : sh) spos[(size_t)r] = -1;
   }
   // Assembly lists: lower-triangle original entries with a pivot column.
   std::vector<long long> adst;
   std::vector<int> asrc, afront;
   asm_begin_.assign((size_t)nf + 1, 0);
+  // front-local row of a new index: a dense scratch map filled with the
+  // front's shell rows (pivots are a contiguous range), O(1) lookups
+  std::vector<int> shell_pos((size_t)n_, -1);
   for (int t = 0; t < nf; ++t) {
     const Front& f = fronts_[(size_t)t];
     const int m = f.np + f.ns;
     asm_begin_[(size_t)t] = adst.size();
+    const auto& sh = shell[(size_t)t];
+    for (size_t i = 0; i < sh.size(); ++i) shell_pos[(size_t)sh[i]] = f.np + (int)i;
     for (int pj = 0; pj < f.np; ++pj) {
       int jold = perm[(size_t)(f.piv0 + pj)];
       for (int k = a.row_ptr_h[(size_t)jold]; k < a.row_ptr_h[(size_t)jold + 1]; ++k) {
         int ni = newidx[(size_t)a.cols_h[(size_t)k]];
         if (ni < f.piv0) continue;  // eliminated in a descendant front
-        int pi = pos_in(t, ni);
+        const int pi = ni < f.piv0 + f.np ? ni - f.piv0 : shell_pos[(size_t)ni];
         if (pi < 0) throw Error(HXG_ERR_GENERIC, "matrix entry outside its front");
         if (pi < pj) continue;      // upper triangle
         adst.push_back((long long)pi + (long long)pj * m);
@@ -413,6 +413,7 @@ void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
         afront.push_back(t);
       }
     }
+    for (int r : sh) shell_pos[(size_t)r] = -1;
   }
   asm_begin_[(size_t)nf] = adst.size();
 
@@ -782,8 +783,16 @@ void NdCholesky::factor_front(int t, Lane& L, const CsrMatrix& a,
 
 void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s) {
   if (!analyzed_) {
+    static const bool prof0 = std::getenv("HXG_PROFILE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
     analyze(a, npd);
+    auto t1 = std::chrono::steady_clock::now();
     plan_lanes();
+    auto t2 = std::chrono::steady_clock::now();
+    if (prof0)
+      std::fprintf(stderr, "[hxg]   symbolic: analyze %.1f ms, lanes %.1f ms\n",
+                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                   std::chrono::duration<double, std::milli>(t2 - t1).count());
   }
   ready_ = false;
   Lane& top = *lanes_[0];
