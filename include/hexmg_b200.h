@@ -176,6 +176,9 @@ int hxg_mg_vcycle(hxg_mg_t mg, const double* b, double* x);
 int hxg_mg_smooth(hxg_mg_t mg, int level, const double* b, double* x);
 /* Assembled coarse operator (CSR, sorted columns) — copy to host. */
 int hxg_mg_coarse_nnz(hxg_mg_t mg, int64_t* nnz);
+/* Device copy of the assembled coarse values (CSR order of
+ * hxg_mg_coarse_csr_host), no host round trip. */
+int hxg_mg_coarse_vals_device(hxg_mg_t mg, double* vals_dev);
 int hxg_mg_coarse_csr_host(hxg_mg_t mg, int* row_ptr, int* cols, double* vals);
 /* Coarse Cholesky solve (coarse_solver.hpp:35-40). */
 int hxg_mg_coarse_solve(hxg_mg_t mg, const double* b, double* x);
@@ -189,6 +192,8 @@ int hxg_mg_coarse_solve(hxg_mg_t mg, const double* b, double* x);
 int hxg_chol_create(int n, const int* row_ptr, const int* cols, const int npd[3], int mode,
                     hxg_chol_t* out);
 int hxg_chol_factorize(hxg_chol_t h, const double* vals_host);
+/* Same with the values already on the device. */
+int hxg_chol_factorize_device(hxg_chol_t h, const double* vals_dev);
 int hxg_chol_solve(hxg_chol_t h, const double* b, double* x);
 int hxg_chol_destroy(hxg_chol_t h);
 

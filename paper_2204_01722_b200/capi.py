@@ -156,6 +156,8 @@ SIGNATURES = {
     "hxg_mg_assemble_coarse": [_vp],
     "hxg_chol_create": [_i, _vp, _vp, _vp, _i, _vp],
     "hxg_chol_factorize": [_vp, _vp],
+    "hxg_chol_factorize_device": [_vp, _vp],
+    "hxg_mg_coarse_vals_device": [_vp, _vp],
     "hxg_chol_solve": [_vp, _vp, _vp],
     "hxg_chol_destroy": [_vp],
     "hxg_cg_solve": [_vp, _vp, _i, _vp, _vp, _d, _i, _vp, _vp, _i],

@@ -288,6 +288,13 @@ int hxg_mg_smooth(hxg_mg_t mg, int level, const double* b, double* x) {
     lv.smoother.apply(*lv.op, b, x, false);
   });
 }
+int hxg_mg_coarse_vals_device(hxg_mg_t mg, double* vals_dev) {
+  return guarded([&] {
+    const auto& a = MG(mg).coarse_matrix();
+    HXG_CUDA(cudaMemcpy(vals_dev, a.vals.p, sizeof(double) * a.cols_h.size(),
+                        cudaMemcpyDeviceToDevice));
+  });
+}
 int hxg_mg_coarse_nnz(hxg_mg_t mg, int64_t* nnz) {
   return guarded([&] { *nnz = MG(mg).coarse_matrix().nnz(); });
 }
@@ -456,6 +463,14 @@ int hxg_chol_factorize(hxg_chol_t h, const double* vals_host) {
     if (!h) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "null Cholesky handle");
     HXG_CUDA(cudaMemcpy(h->a.vals.p, vals_host, sizeof(double) * h->a.cols_h.size(),
                         cudaMemcpyHostToDevice));
+    h->solver.factorize(h->a, h->npd, h->stream);
+  });
+}
+int hxg_chol_factorize_device(hxg_chol_t h, const double* vals_dev) {
+  return guarded([&] {
+    if (!h) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "null Cholesky handle");
+    HXG_CUDA(cudaMemcpy(h->a.vals.p, vals_dev, sizeof(double) * h->a.cols_h.size(),
+                        cudaMemcpyDeviceToDevice));
     h->solver.factorize(h->a, h->npd, h->stream);
   });
 }

@@ -280,14 +280,21 @@ class DistributedHierarchy:
             self.lambda_max[k] = self._estimate_lambda_max(k)
         if self._coarse is None:
             self._coarse_symbolic()
-        _, _, lvals = self.b.coarse_csr()
+        if hasattr(self.b, "coarse_vals"):  # device-resident values (GPU backend)
+            lvals = self.b.coarse_vals()
+        else:
+            lvals = torch.as_tensor(np.asarray(self.b.coarse_csr()[2]), dtype=torch.float64,
+                                    device=self.b.device)
+        if not hasattr(self, "_slots_t"):
+            dev = self.b.device
+            self._slots_t = torch.as_tensor(self._slots, device=dev)
+            self._lsel_t = torch.as_tensor(self._lsel, device=dev)
+            self._diag_t = torch.as_tensor(self._diag_slots, device=dev)
         gv = torch.zeros(self._nnz, dtype=torch.float64, device=self.b.device)
-        gv[torch.as_tensor(self._slots, device=self.b.device)] = torch.as_tensor(
-            np.asarray(lvals)[self._lsel], dtype=torch.float64, device=self.b.device)
+        gv[self._slots_t] = lvals[self._lsel_t]
         self.comm.all_reduce_(gv)
-        gv = gv.cpu().numpy()
-        gv[self._diag_slots] = 1.0
-        self._coarse.factorize(gv)
+        gv[self._diag_t] = 1.0
+        self._coarse.factorize(gv if gv.is_cuda else gv.numpy())
 
     # -- cycle ------------------------------------------------------------------
     def coarse_solve(self, b):
@@ -588,6 +595,11 @@ class SlabBackend:
     def coarse_csr(self):
         self.mg.assemble_coarse()
         return self.mg.coarse_csr()
+
+    def coarse_vals(self):
+        """Re-assembled coarse values, left on the device."""
+        self.mg.assemble_coarse()
+        return self.mg.coarse_vals_device()
 
     def coarse_solver(self, row_ptr, cols, npd):
         from .hexmg import CoarseCholesky

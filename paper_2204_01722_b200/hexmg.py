@@ -329,6 +329,14 @@ class MultigridHierarchy:
         check(lib().hxg_mg_coarse_csr_host(self.h, _ptr(rp), _ptr(cols), _ptr(vals)))
         return rp, cols, vals
 
+    def coarse_vals_device(self):
+        """The assembled coarse values as a CUDA tensor (CSR order of coarse_csr)."""
+        nnz = ctypes.c_int64()
+        check(lib().hxg_mg_coarse_nnz(self.h, ctypes.byref(nnz)))
+        v = torch.empty(nnz.value, dtype=torch.float64, device="cuda")
+        check(lib().hxg_mg_coarse_vals_device(self.h, _ptr(v)))
+        return v
+
     def coarse_solve(self, b):
         b = _dev(b, self.level_size(0))
         x = torch.empty_like(b)
@@ -360,6 +368,11 @@ class CoarseCholesky:
             self.h = None
 
     def factorize(self, vals):
+        if isinstance(vals, torch.Tensor) and vals.is_cuda:
+            if vals.numel() != self._cols.size:
+                raise ValueError("value array does not match the pattern")
+            check(lib().hxg_chol_factorize_device(self.h, _ptr(vals.contiguous())))
+            return
         vals = np.ascontiguousarray(vals, np.float64)
         if vals.size != self._cols.size:
             raise ValueError("value array does not match the pattern")
