@@ -51,6 +51,10 @@ namespace hxg {
 
 namespace {
 
+#ifndef HXG_FIXUP_ITEMS
+#define HXG_FIXUP_ITEMS 2
+#endif
+
 struct FusedParams {
   BoxDev box;
   QLayout lay;
@@ -65,7 +69,16 @@ struct FusedParams {
   int brick0;   // first brick of this launch (pipelined host path)
   int nbricks;  // bricks in this launch
   int face_bits;  // >= 0: constraints are these whole faces (analytic), -1: mask array
-  int gz0;     // first node plane of this fix-up launch
+  // Fix-up launch: node planes [zs, ze) and the compact enumeration of the
+  // brick-boundary rows in them (fixup_rows()).
+  struct Rows {
+    int zs, ze;
+    int nzm;            // brick-plane multiples of PB2 in [zs, min(ze, npz - 1))
+    int nzp, nzn;       // z brick planes / other planes in range
+    int nyp, nyn, nxp;  // y planes / other y, x planes (whole box)
+    int threadsA;       // rows with gz or gy on a brick plane x 3 npx
+    int threadsB;       // remaining rows x 3 nxp (x brick planes only)
+  } fx;
   // Uniform copies of the 1D tables for the z-direction contractions
   // (constant-bank operands).
   double B[kMaxQ * (kMaxP + 1)];   // interp (Q x N)
@@ -632,78 +645,146 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
 #endif
 }
 
+// One boundary (node, component): the partials of its up-to-8 sharing
+// bricks, q = i0 + 2 i1 + 4 i2 = (c0, c1, c2) offsets from (lo0, lo1, lo2).
+// gather() issues the loads, finish() sums them in increasing q = increasing
+// brick order, so several entries' loads can be in flight together.
 template <int P, int Q>
-__device__ __forceinline__ void fixup_entry(const FusedParams& prm, int gx, int gy, int gz, int c) {
+struct FixupEntry {
   using D = FDims<P, Q>;
-  constexpr int PB0 = P * D::BX, PB1 = P * D::BY, PB2 = P * D::BZ;
-  const BoxDev& box = prm.box;
-  const QLayout& lay = prm.lay;
-  const int npx = box.npd[0], npy = box.npd[1];
-  const int b1 = gy / PB1, b2 = gz / PB2, b0 = gx / PB0;
-  const int lo1 = (gy % PB1 == 0 && b1 > 0) ? b1 - 1 : b1, hi1 = min(b1, lay.nb[1] - 1);
-  const int lo2 = (gz % PB2 == 0 && b2 > 0) ? b2 - 1 : b2, hi2 = min(b2, lay.nb[2] - 1);
-  const int lo0 = (gx % PB0 == 0 && b0 > 0) ? b0 - 1 : b0, hi0 = min(b0, lay.nb[0] - 1);
-  const unsigned long long pol = policy_evict_first();
-  // Up to 8 sharing bricks, q = i0 + 2 i1 + 4 i2 = (c0, c1, c2) offsets from
-  // (lo0, lo1, lo2): all loads issued together, then summed in increasing q
-  // = increasing brick order.
-  const int n0 = hi0 - lo0, n1 = hi1 - lo1, n2 = hi2 - lo2;  // 0 or 1
-  const double* p0 = prm.partial +
-                     (lo0 + (size_t)lay.nb[0] * (lo1 + (size_t)lay.nb[1] * lo2)) * (D::NB * 3) +
-                     (((gz - PB2 * lo2) * D::NBY + (gy - PB1 * lo1)) * D::NBX + (gx - PB0 * lo0)) * 3 + c;
+  static constexpr int PB0 = P * D::BX, PB1 = P * D::BY, PB2 = P * D::BZ;
+  int gx, gy, gz, c;
+  unsigned valid = 0;  // bit q: brick q shares the node
   double v[8];
+
+  __device__ __forceinline__ void gather(const FusedParams& prm) {
+    const QLayout& lay = prm.lay;
+    const int b1 = gy / PB1, b2 = gz / PB2, b0 = gx / PB0;
+    const int lo1 = (gy % PB1 == 0 && b1 > 0) ? b1 - 1 : b1, hi1 = min(b1, lay.nb[1] - 1);
+    const int lo2 = (gz % PB2 == 0 && b2 > 0) ? b2 - 1 : b2, hi2 = min(b2, lay.nb[2] - 1);
+    const int lo0 = (gx % PB0 == 0 && b0 > 0) ? b0 - 1 : b0, hi0 = min(b0, lay.nb[0] - 1);
+    const unsigned long long pol = policy_evict_first();
+    const int n0 = hi0 - lo0, n1 = hi1 - lo1, n2 = hi2 - lo2;  // 0 or 1
+    const double* p0 = prm.partial +
+                       (lo0 + (size_t)lay.nb[0] * (lo1 + (size_t)lay.nb[1] * lo2)) * (D::NB * 3) +
+                       (((gz - PB2 * lo2) * D::NBY + (gy - PB1 * lo1)) * D::NBX + (gx - PB0 * lo0)) * 3 + c;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int i0 = q & 1, i1 = (q >> 1) & 1, i2 = q >> 2;
-    v[q] = 0.0;
-    if (i0 <= n0 && i1 <= n1 && i2 <= n2) {
-      // neighbour brick +i_d: brick index +i_d stride, local coordinate -i_d P B_d
-      const long long off = (i0 + (long long)lay.nb[0] * (i1 + (long long)lay.nb[1] * i2)) * (D::NB * 3) -
-                            3LL * ((i2 * PB2 * D::NBY + i1 * PB1) * D::NBX + i0 * PB0);
-      v[q] = ld_once(p0 + off, pol);
+    for (int q = 0; q < 8; ++q) {
+      const int i0 = q & 1, i1 = (q >> 1) & 1, i2 = q >> 2;
+      v[q] = 0.0;
+      if (i0 <= n0 && i1 <= n1 && i2 <= n2) {
+        // neighbour brick +i_d: brick index +i_d stride, local coordinate -i_d P B_d
+        const long long off = (i0 + (long long)lay.nb[0] * (i1 + (long long)lay.nb[1] * i2)) * (D::NB * 3) -
+                              3LL * ((i2 * PB2 * D::NBY + i1 * PB1) * D::NBX + i0 * PB0);
+        v[q] = ld_once(p0 + off, pol);
+        valid |= 1u << q;
+      }
     }
   }
-  double s = 0.0;
+
+  __device__ __forceinline__ void finish(const FusedParams& prm) const {
+    const int npx = prm.box.npd[0], npy = prm.box.npd[1];
+    double s = 0.0;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int i0 = q & 1, i1 = (q >> 1) & 1, i2 = q >> 2;
-    if (i0 <= n0 && i1 <= n1 && i2 <= n2) s += v[q];
+    for (int q = 0; q < 8; ++q)
+      if (valid & (1u << q)) s += v[q];
+    const size_t dof = 3 * ((size_t)gx + (size_t)npx * (gy + (size_t)npy * gz)) + c;
+    const int b = prm.face_bits;
+    const bool fixed =
+        b >= 0 ? ((b & 1) && gx == 0) || ((b & 2) && gx == npx - 1) || ((b & 4) && gy == 0) ||
+                     ((b & 8) && gy == npy - 1) || ((b & 16) && gz == 0) ||
+                     ((b & 32) && gz == prm.box.npd[2] - 1)
+               : prm.mask && prm.mask[dof];
+    prm.y[dof] = fixed ? prm.x[dof] : s;  // pass x through (operator.hpp:212-214)
   }
-  const size_t dof = 3 * ((size_t)gx + (size_t)npx * (gy + (size_t)npy * gz)) + c;
-  if (prm.mask && prm.mask[dof]) s = prm.x[dof];
-  prm.y[dof] = s;
-}
+};
 
 // Sums brick-boundary partials: nodes on planes g_d = k P B_d (or the domain's
-// far face) in increasing brick order.  One thread per (node, component) of
-// a (gy, gz) node row (blockDim 128, grid (ceil(3 npx / 128), npy, npz)):
-// rows on a y or z brick plane are boundary along their whole length, and
-// consecutive lanes read consecutive doubles of a brick's partial row
-// (coalesced); other rows only hold the x brick-plane nodes, which the
-// first block of the row covers.
+// far face) in increasing brick order.  One index per boundary (node,
+// component), enumerated compactly (no idle blocks): first the rows with gz or
+// gy on a brick plane, boundary along their whole length (consecutive threads
+// read consecutive doubles of a brick's partial row), then the other rows,
+// which only hold the x brick-plane nodes.  Each thread takes kFixupItems
+// indices a grid-stride apart, all their loads in flight at once.
+constexpr int kFixupItems = HXG_FIXUP_ITEMS;
+__device__ __forceinline__ int plane_at(int k, int nmult, int s, int pb, int far) {
+  return k < nmult ? s + k * pb : far;
+}
+__device__ __forceinline__ int between_at(int j, int s, int pb) {  // j-th non-plane >= s
+  const int w = pb > 1 ? pb - 1 : 1;
+  return s + pb * (j / w) + 1 + j % w;
+}
+
+template <int P, int Q>
+__device__ __forceinline__ bool fixup_decode(const FusedParams& prm, int t, FixupEntry<P, Q>& e) {
+  using E = FixupEntry<P, Q>;
+  const auto& fx = prm.fx;
+  const int npx = prm.box.npd[0], npy = prm.box.npd[1], npz = prm.box.npd[2];
+  if (t < fx.threadsA) {
+    const int W = 3 * npx, r = t / W, k = t - r * W;
+    e.gx = k / 3;
+    e.c = k - 3 * e.gx;
+    const int rz = fx.nzp * npy;
+    if (r < rz) {
+      e.gz = plane_at(r / npy, fx.nzm, fx.zs, E::PB2, npz - 1);
+      e.gy = r % npy;
+    } else {
+      const int q = r - rz;
+      e.gz = between_at(q / fx.nyp, fx.zs, E::PB2);
+      e.gy = plane_at(q % fx.nyp, fx.nyp - 1, 0, E::PB1, npy - 1);
+    }
+    return true;
+  }
+  const int u = t - fx.threadsA;
+  if (u >= fx.threadsB) return false;
+  const int W = 3 * fx.nxp, r = u / W, k = u - r * W;
+  const int kx = k / 3;
+  e.c = k - 3 * kx;
+  e.gx = plane_at(kx, fx.nxp - 1, 0, E::PB0, npx - 1);
+  e.gz = between_at(r / fx.nyn, fx.zs, E::PB2);
+  e.gy = between_at(r % fx.nyn, 0, E::PB1);
+  return true;
+}
+
 template <int P, int Q>
 __global__ void __launch_bounds__(128) fused_fixup_kernel(const __grid_constant__ FusedParams prm) {
+  const int stride = gridDim.x * 128;
+  const int t = blockIdx.x * 128 + threadIdx.x;
+  FixupEntry<P, Q> e[kFixupItems];
+  bool ok[kFixupItems];
+#pragma unroll
+  for (int k = 0; k < kFixupItems; ++k) {
+    ok[k] = fixup_decode<P, Q>(prm, t + k * stride, e[k]);
+    if (ok[k]) e[k].gather(prm);
+  }
+#pragma unroll
+  for (int k = 0; k < kFixupItems; ++k)
+    if (ok[k]) e[k].finish(prm);
+}
+
+// Boundary-row enumeration of a fix-up launch over node planes [zs, ze)
+// (zs a multiple of P B_z).
+template <int P, int Q>
+unsigned fixup_rows(FusedParams& prm, int zs, int ze) {
   using D = FDims<P, Q>;
   constexpr int PB0 = P * D::BX, PB1 = P * D::BY, PB2 = P * D::BZ;
-  const BoxDev& box = prm.box;
-  const int gy = blockIdx.y, gz = blockIdx.z + prm.gz0;
-  const int npx = box.npd[0], npy = box.npd[1];
-  const bool yb = gy % PB1 == 0 || gy == npy - 1;
-  const bool zb = gz % PB2 == 0 || gz == box.npd[2] - 1;
-  int gx, c;
-  if (yb || zb) {
-    const int e = blockIdx.x * 128 + threadIdx.x;
-    if (e >= 3 * npx) return;
-    gx = e / 3;
-    c = e - 3 * gx;
-  } else {
-    const int nx_planes = (npx - 1 + PB0 - 1) / PB0 + 1;  // x brick planes incl. far face
-    if (blockIdx.x != 0 || threadIdx.x >= 3 * nx_planes) return;
-    const int t = threadIdx.x / 3;
-    c = threadIdx.x - 3 * t;
-    gx = min(t * PB0, npx - 1);
-  }
-  fixup_entry<P, Q>(prm, gx, gy, gz, c);
+  const int npx = prm.box.npd[0], npy = prm.box.npd[1], npz = prm.box.npd[2];
+  auto& fx = prm.fx;
+  fx.zs = zs;
+  fx.ze = ze;
+  const int top = ze < npz - 1 ? ze : npz - 1;
+  fx.nzm = top > zs ? (top - zs + PB2 - 1) / PB2 : 0;
+  fx.nzp = fx.nzm + (ze == npz ? 1 : 0);
+  fx.nzn = (ze - zs) - fx.nzp;
+  fx.nyp = (npy - 1 + PB1 - 1) / PB1 + 1;
+  fx.nyn = npy - fx.nyp;
+  fx.nxp = (npx - 1 + PB0 - 1) / PB0 + 1;
+  const long long a = (long long)(fx.nzp * (long long)npy + (long long)fx.nzn * fx.nyp) * 3 * npx;
+  const long long b = (long long)fx.nzn * fx.nyn * 3 * fx.nxp;
+  if (a + b > 0x7fffffffLL) throw Error(HXG_ERR_INVALID_ARGUMENT, "fix-up index space exceeds int32");
+  fx.threadsA = (int)a;
+  fx.threadsB = (int)b;
+  return (unsigned)((a + b + 128LL * kFixupItems - 1) / (128LL * kFixupItems));
 }
 
 // Persistent grid: every resident CTA slot of the device, capped by the work.
@@ -777,8 +858,8 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
     prm.nbricks = (int)op.lay_.num_bricks();
     k<<<persistent_grid(k, D::T, smem, prm.nbricks), D::T, smem, op.stream_>>>(prm);
     HXG_CUDA(cudaGetLastError());
-    dim3 fg((3 * op.box_.npd[0] + 127) / 128, op.box_.npd[1], op.box_.npd[2]);
-    fused_fixup_kernel<P, Q><<<fg, 128, 0, op.stream_>>>(prm);
+    const unsigned fg = fixup_rows<P, Q>(prm, 0, op.box_.npd[2]);
+    if (fg) fused_fixup_kernel<P, Q><<<fg, 128, 0, op.stream_>>>(prm);
     HXG_CUDA(cudaGetLastError());
   });
 }
@@ -852,9 +933,8 @@ void fused_jacobian_host(Operator& op, const double* xh, double* yh) {
       HXG_CUDA(cudaGetLastError());
       const int zs = i == 0 ? 0 : pb2 * lb;
       const int ze = i == C - 1 ? npz : pb2 * le;
-      pc.gz0 = zs;
-      dim3 fg((3 * op.box_.npd[0] + 127) / 128, op.box_.npd[1], ze - zs);
-      fused_fixup_kernel<P, Q><<<fg, 128, 0, pp.comp>>>(pc);
+      const unsigned fg = fixup_rows<P, Q>(pc, zs, ze);
+      if (fg) fused_fixup_kernel<P, Q><<<fg, 128, 0, pp.comp>>>(pc);
       HXG_CUDA(cudaGetLastError());
       HXG_CUDA(cudaEventRecord(pp.out_ready[i], pp.comp));
       HXG_CUDA(cudaStreamWaitEvent(pp.d2h, pp.out_ready[i], 0));
