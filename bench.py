@@ -357,6 +357,38 @@ def run_ours(args, rank, world, local_rank):
         del prob5, x5, y5
         torch.cuda.empty_cache()
 
+    # JacobianStorage variants (paper Table III, material.hpp:66-78) on the
+    # headline Q2 64^3 problem: bytes per DoF from each variant's state and
+    # the measured apply (Current: fused brick kernel; initial variants: the
+    # two-pass element path).  Rank 0, N = 1 only.
+    storage_table = None
+    if world == 1 and not args.no_newton:
+        storage_table = []
+        for sname in ("current", "initial-native", "initial-tuned", "initial-ad"):
+            ps = FemProblem(extents=(1.0, 1.0, 1.0), cells=(CELLS,) * 3, order=ORDER,
+                            fixed_faces=fixed, geometry="box", storage=sname)
+            ns = ps.size()
+            ps.op.apply_residual(torch.zeros(ns, dtype=torch.float64, device="cuda"))
+            xs = 1e-3 * torch.sin(0.7 * torch.arange(ns, dtype=torch.float64, device="cuda"))
+            ys = torch.empty_like(xs)
+            for _ in range(3):
+                ps.op.apply_jacobian(xs, ys)
+            es = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            torch.cuda.synchronize()
+            es[0].record(stream)
+            for _ in range(20):
+                ps.op.apply_jacobian(xs, ys)
+            es[1].record(stream)
+            torch.cuda.synchronize()
+            mss = es[0].elapsed_time(es[1]) / 20
+            bpd = ps.op.stored_bytes_per_dof()
+            storage_table.append({"storage": sname, "bytes_per_dof": bpd, "ms_per_apply": mss,
+                                  "GDoF_s": ns / (mss * 1e-3) / 1e9,
+                                  "roofline_frac": bpd * ns / (mss * 1e-3) / 1e9 / peak_gbs(),
+                                  "path": "fused" if sname == "current" else "two-pass"})
+            del ps, xs, ys
+            torch.cuda.empty_cache()
+
     # End-to-end through the C-ABI host-buffer entry point (pinned host x/y).
     xh = x.cpu().pin_memory()
     yh = torch.empty_like(xh).pin_memory()
@@ -519,6 +551,7 @@ def run_ours(args, rank, world, local_rank):
             "pmg_distributed": pmg_dist,
             "newton_solve": newton_full,
             "apply_cfg5": cfg5,
+            "storage_variants": storage_table,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -422,6 +422,150 @@ def jacobian_qfunction(mu, lam, G, state):
 
 
 # --------------------------------------------------------------------------
+# Initial-configuration JacobianStorage variants (material.hpp:66-78,
+# :152-175, :196-239): state [w, dxi/dX (9), grad_X u (9), +C^-1 sym + lambda
+# log J (Tuned) | +S sym (AD)].  Strides 19 / 26 / 25.
+# --------------------------------------------------------------------------
+STATE_SCALARS = {0: 17, 1: 19, 2: 26, 3: 25}
+
+
+class _Dual:
+    """Forward-mode dual arrays (dual.hpp:9-40): value + directional derivative."""
+
+    def __init__(self, v, d):
+        self.v, self.d = v, d
+
+    def __getitem__(self, k):
+        return _Dual(self.v[k], self.d[k])
+
+    def __add__(self, o):
+        o = _lift(o)
+        return _Dual(self.v + o.v, self.d + o.d)
+
+    __radd__ = __add__
+
+    def __sub__(self, o):
+        o = _lift(o)
+        return _Dual(self.v - o.v, self.d - o.d)
+
+    def __rsub__(self, o):
+        return _lift(o) - self
+
+    def __mul__(self, o):
+        o = _lift(o)
+        return _Dual(self.v * o.v, self.v * o.d + self.d * o.v)
+
+    __rmul__ = __mul__
+
+    def __truediv__(self, o):
+        o = _lift(o)
+        inv = 1.0 / o.v
+        return _Dual(self.v * inv, (self.d - self.v * o.d * inv) * inv)
+
+    def __rtruediv__(self, o):
+        return _lift(o) / self
+
+
+def _lift(o):
+    return o if isinstance(o, _Dual) else _Dual(o, np.zeros_like(o) if np.ndim(o) else 0.0)
+
+
+def _dual_inv3(m):
+    """Adjugate inverse (tensor3.hpp:94-110) of a dual (..., 3, 3)."""
+    adj = [[m[..., 1, 1] * m[..., 2, 2] - m[..., 1, 2] * m[..., 2, 1],
+            m[..., 0, 2] * m[..., 2, 1] - m[..., 0, 1] * m[..., 2, 2],
+            m[..., 0, 1] * m[..., 1, 2] - m[..., 0, 2] * m[..., 1, 1]],
+           [m[..., 1, 2] * m[..., 2, 0] - m[..., 1, 0] * m[..., 2, 2],
+            m[..., 0, 0] * m[..., 2, 2] - m[..., 0, 2] * m[..., 2, 0],
+            m[..., 0, 2] * m[..., 1, 0] - m[..., 0, 0] * m[..., 1, 2]],
+           [m[..., 1, 0] * m[..., 2, 1] - m[..., 1, 1] * m[..., 2, 0],
+            m[..., 0, 1] * m[..., 2, 0] - m[..., 0, 0] * m[..., 2, 1],
+            m[..., 0, 0] * m[..., 1, 1] - m[..., 0, 1] * m[..., 1, 0]]]
+    inv_det = 1.0 / _det3(m)
+    ent = [[a * inv_det for a in row] for row in adj]
+    v = np.stack([np.stack([a.v for a in row], -1) for row in ent], -2)
+    d = np.stack([np.stack([a.d for a in row], -1) for row in ent], -2)
+    return _Dual(v, d)
+
+
+def _dual_second_piola(mu, lam, e):
+    """S(E) = mu I + (lambda log J - mu) C^-1, C = I + 2E (material.hpp:110-121), dual E."""
+    c = _Dual(np.eye(3) + 2.0 * e.v, 2.0 * e.d)
+    dj = _det3(c)
+    log_j = 0.5 * _Dual(np.log(dj.v), dj.d / dj.v)
+    ci = _dual_inv3(c)
+    coeff = lam * log_j - mu
+    return _Dual(mu * np.eye(3) + coeff.v[..., None, None] * ci.v,
+                 coeff.v[..., None, None] * ci.d + coeff.d[..., None, None] * ci.v)
+
+
+def _sym(m):
+    return 0.5 * (m + np.swapaxes(m, -1, -2))
+
+
+def _unpack_sym(v):
+    m = np.empty(v.shape[:-1] + (3, 3))
+    for k, (i, j) in enumerate(SYM_IDX):
+        m[..., i, j] = v[..., k]
+        m[..., j, i] = v[..., k]
+    return m
+
+
+def residual_qfunction_initial(storage, mu, lam, G, dxidX, wdet):
+    """residual_qpoint, initial-configuration storages (material.hpp:152-175)."""
+    grad_u = G @ dxidX
+    F = np.eye(3) + grad_u
+    J = _det3(F)
+    bad = ~(J > 0)
+    if np.any(bad):
+        first = np.flatnonzero(bad.ravel())[0]
+        raise InvertedElementError(J.ravel()[first], *np.unravel_index(first, J.shape))
+    log_j = np.log(J)
+    C = np.swapaxes(F, -1, -2) @ F
+    Ci = _inv3(C)
+    coeff = lam * log_j - mu
+    S = mu * np.eye(3) + coeff[..., None, None] * Ci
+    st = np.zeros(G.shape[:-2] + (STATE_SCALARS[storage],))
+    st[..., 0] = wdet
+    st[..., 1:10] = np.broadcast_to(dxidX, G.shape).reshape(G.shape[:-2] + (9,))
+    st[..., 10:19] = grad_u.reshape(G.shape[:-2] + (9,))
+    for k, (i, j) in enumerate(SYM_IDX):
+        if storage == 2:
+            st[..., 19 + k] = Ci[..., i, j]
+        elif storage == 3:
+            st[..., 19 + k] = S[..., i, j]
+    if storage == 2:
+        st[..., 25] = lam * log_j
+    H = wdet[..., None, None] * ((F @ S) @ np.swapaxes(dxidX, -1, -2))
+    return H, st
+
+
+def jacobian_qfunction_initial(storage, mu, lam, G, st):
+    """jacobian_qpoint, initial-configuration storages (material.hpp:196-239)."""
+    wdet = st[..., 0]
+    dxidX = st[..., 1:10].reshape(st.shape[:-1] + (3, 3))
+    grad_u = st[..., 10:19].reshape(st.shape[:-1] + (3, 3))
+    F = np.eye(3) + grad_u
+    dF = G @ dxidX
+    dE = _sym(np.swapaxes(F, -1, -2) @ dF)
+    if storage == 3:
+        S = _unpack_sym(st[..., 19:25])
+        E = _sym(grad_u) + 0.5 * (np.swapaxes(grad_u, -1, -2) @ grad_u)
+        dS = _dual_second_piola(mu, lam, _Dual(E, dE)).d
+    else:
+        if storage == 2:
+            Ci, llj = _unpack_sym(st[..., 19:25]), st[..., 25]
+        else:
+            C = np.swapaxes(F, -1, -2) @ F
+            Ci, llj = _inv3(C), 0.5 * lam * np.log(_det3(C))
+        coeff = llj - mu
+        S = mu * np.eye(3) + coeff[..., None, None] * Ci
+        cde = np.einsum("...ij,...ij->...", Ci, dE)
+        dS = (lam * cde)[..., None, None] * Ci - (2.0 * coeff)[..., None, None] * ((Ci @ dE) @ Ci)
+    return wdet[..., None, None] * ((dF @ S + F @ dS) @ np.swapaxes(dxidX, -1, -2))
+
+
+# --------------------------------------------------------------------------
 # Composed operator (operator.hpp:70-354)
 # --------------------------------------------------------------------------
 
@@ -438,9 +582,11 @@ def _pts_to_qgrad(H, q):
 
 
 class Operator:
-    """MatrixFreeOperator (operator.hpp:70-373), Current storage only."""
+    """MatrixFreeOperator (operator.hpp:70-373); storage = JacobianStorage id."""
 
-    def __init__(self, mesh: BoxMesh, basis: Basis1D, dxidX, weight, mu, lam, mask, state_ref=None):
+    def __init__(self, mesh: BoxMesh, basis: Basis1D, dxidX, weight, mu, lam, mask, state_ref=None,
+                 storage=0):
+        self.storage = storage
         self.mesh, self.basis = mesh, basis
         self.idx, self.mult = build_restriction(mesh)
         self.dxidX, self.weight = dxidX, weight
@@ -463,7 +609,11 @@ class Operator:
         ev = gather(self.idx, u, b.n)
         G = _qgrad_to_pts(grad_ref(b, ev))
         try:
-            H, st = residual_qfunction(self.mu, self.lam, G, self.dxidX, self.weight)
+            if self.storage:
+                H, st = residual_qfunction_initial(self.storage, self.mu, self.lam, G, self.dxidX,
+                                                   self.weight)
+            else:
+                H, st = residual_qfunction(self.mu, self.lam, G, self.dxidX, self.weight)
         except InvertedElementError as err:
             raise InvertedElementError(err.jacobian, err.element, err.point) from None
         self.state_ref["state"] = st
@@ -483,11 +633,16 @@ class Operator:
             x[self.mask != 0] = 0.0
         ev = gather(self.idx, x, b.n)
         G = _qgrad_to_pts(grad_ref(b, ev))
-        H = jacobian_qfunction(self.mu, self.lam, G, self.state)
+        H = self._jacobian_qf(G, self.state)
         out = scatter_add(self.idx, grad_transpose_ref(b, _pts_to_qgrad(H, b.q)), self.mesh.num_nodes)
         if self.mask is not None:
             out[self.mask != 0] = du[self.mask != 0]
         return out
+
+    def _jacobian_qf(self, G, st):
+        if self.storage:
+            return jacobian_qfunction_initial(self.storage, self.mu, self.lam, G, st)
+        return jacobian_qfunction(self.mu, self.lam, G, st)
 
     def pointwise_tensor(self):
         """D[e,q,(c1,d1),(c2,d2)] by probing (operator.hpp:233-243)."""
@@ -498,7 +653,7 @@ class Operator:
             for d2 in range(3):
                 unit = np.zeros((E, nq, 3, 3))
                 unit[..., c2, d2] = 1.0
-                h = jacobian_qfunction(self.mu, self.lam, unit, st)
+                h = self._jacobian_qf(unit, st)
                 D[..., :, c2 * 3 + d2] = h.reshape(E, nq, 9)
         return D
 
@@ -841,14 +996,14 @@ class Problem:
 
 
 def make_problem(extents, counts, order, q=0, fixed_faces=(0,), traction_face=-1,
-                 traction=(0.0, 0.0, 0.0), young=1.0, poisson=0.3) -> Problem:
+                 traction=(0.0, 0.0, 0.0), young=1.0, poisson=0.3, storage=0) -> Problem:
     q = q or order + 1
     mesh = build_box_mesh(extents, counts, order)
     basis = build_lagrange_basis(order, q)
     dxidX, weight = compute_geometric_factors(mesh, basis)
     mu, lam = lame_from_young_poisson(young, poisson)
     mask = build_constraints(mesh, fixed_faces)
-    op = Operator(mesh, basis, dxidX, weight, mu, lam, mask)
+    op = Operator(mesh, basis, dxidX, weight, mu, lam, mask, storage=storage)
     load = np.zeros(op.size)
     if traction_face >= 0:
         load = traction_load(mesh, basis, traction_face, traction)

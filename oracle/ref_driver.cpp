@@ -36,6 +36,7 @@ using namespace hexmg;
 namespace {
 
 thread_local std::string g_err;
+int g_storage = 0;  // JacobianStorage for the next ref_create (ProblemConfig::storage)
 
 struct RefProblem {
   ProblemConfig cfg;
@@ -105,6 +106,7 @@ void* ref_create(const double* extents, const int* cells, int order, int qpts, i
     cfg.youngs_modulus = young;
     cfg.poisson_ratio = poisson;
     cfg.threads = threads;
+    cfg.storage = static_cast<JacobianStorage>(g_storage);
     h->problem = std::make_unique<FemProblem>(cfg);
   });
   if (rc != 0) {
@@ -112,6 +114,11 @@ void* ref_create(const double* extents, const int* cells, int order, int qpts, i
     return nullptr;
   }
   return h;
+}
+
+void ref_set_storage(int s) { g_storage = s; }
+int ref_state_stride(void* p) {
+  return quadrature_state_stride(static_cast<RefProblem*>(p)->problem->op().storage());
 }
 
 void ref_destroy(void* p) { delete static_cast<RefProblem*>(p); }

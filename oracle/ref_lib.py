@@ -47,6 +47,8 @@ def lib():
         L.ref_apply_jacobian.argtypes = [vp, i, vp, vp]
         L.ref_extract_diagonal.argtypes = [vp, i, vp]
         L.ref_state.argtypes = [vp, vp]
+        L.ref_set_storage.argtypes = [i]
+        L.ref_state_stride.argtypes = [vp]
         L.ref_energy.argtypes = [vp, vp, vp]
         L.ref_stored_bytes_per_dof.argtypes = [vp]
         L.ref_stored_bytes_per_dof.restype = d
@@ -103,8 +105,10 @@ class RefProblem:
     """FemProblem (problem.hpp:19-58) built by the reference itself."""
 
     def __init__(self, extents=(1.0, 1.0, 1.0), cells=(2, 2, 2), order=2, q=0, fixed=("-x",),
-                 traction_face=None, traction=(0.0, 0.0, 0.0), young=1.0, poisson=0.3, threads=1):
+                 traction_face=None, traction=(0.0, 0.0, 0.0), young=1.0, poisson=0.3, threads=1,
+                 storage=0):
         L = lib()
+        L.ref_set_storage(storage)
         ext = np.asarray(extents, dtype=np.float64)
         cl = np.asarray(cells, dtype=np.int32)
         tr = np.asarray(traction, dtype=np.float64)
@@ -113,6 +117,7 @@ class RefProblem:
             mask |= 1 << FACES[f]
         tf = -1 if traction_face is None else FACES[traction_face]
         h = L.ref_create(_p(ext), _p(cl), order, q, mask, tf, _p(tr), young, poisson, threads)
+        L.ref_set_storage(0)
         if not h:
             raise RefError(-1, L.ref_last_error().decode())
         self.h = ctypes.c_void_p(h)
@@ -198,7 +203,7 @@ class RefProblem:
         return d
 
     def state(self):
-        out = np.zeros((self.E, self.nq, 17))
+        out = np.zeros((self.E, self.nq, lib().ref_state_stride(self.h)))
         lib().ref_state(self.h, _p(out))
         return out
 

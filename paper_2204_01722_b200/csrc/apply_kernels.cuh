@@ -8,6 +8,7 @@
 #include "common.hpp"
 #include "element.cuh"
 #include "qfunction.cuh"
+#include "qfunction_initial.cuh"
 
 namespace hxg {
 
@@ -24,6 +25,7 @@ struct ElemParams {
   double* state_out;       // residual: written state
   const double* geo;       // residual/energy: geometry (blocked, 10 per qpt)
   double mu, lambda, perturb;
+  int storage;               // JacobianStorage (the kernel's ST template argument)
   unsigned long long* fail;  // residual: min over e*Q^3+q of inverted points
   double* energy_part;       // energy: per-element partial sums
 };
@@ -88,8 +90,10 @@ __device__ __forceinline__ void load_tables(const double* tab, double* sTab) {
 }
 
 // Two-pass element kernel: gather -> grad -> q-function -> grad^T -> E-vector.
-template <int P, int Q, int MODE>
+// ST = JacobianStorage: the state stride and the q-function pair.
+template <int P, int Q, int MODE, int ST = kStorageCurrent>
 __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams prm) {
+  constexpr int S = device_state_stride(ST);
   using D = Dims<P, Q>;
   constexpr int N = D::N, N3 = D::N3;
   extern __shared__ double smem[];
@@ -116,16 +120,19 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams
   if (MODE == kJacobian) {
 #pragma unroll
     for (int qz = 0; qz < Q; ++qz) {
-      double st[kStateStride];
-      const double* sp = prm.state + (base + (long long)qz * T) * kStateStride + threadIdx.x;
+      double st[S];
+      const double* sp = prm.state + (base + (long long)qz * T) * S + threadIdx.x;
 #pragma unroll
-      for (int s = 0; s < kStateStride; ++s) st[s] = __ldg(sp + s * T);
+      for (int s = 0; s < S; ++s) st[s] = __ldg(sp + s * T);
       double G[9], H[9];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int d = 0; d < 3; ++d) G[3 * c + d] = g[c][d][qz];
-      jacobian_qf(prm.mu, prm.lambda, G, st, H);
+      if constexpr (ST == kStorageCurrent)
+        jacobian_qf(prm.mu, prm.lambda, G, st, H);
+      else
+        jacobian_qf_initial<ST>(prm.mu, prm.lambda, G, st, H);
       if (prm.perturb != 0.0) {  // fault-injection hook: + eps w detJ G
         const double wdet = prm.geo[(base + (long long)qz * T) * kGeoStride + 9 * T + threadIdx.x];
 #pragma unroll
@@ -143,13 +150,17 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams
       const double* gp = prm.geo + (base + (long long)qz * T) * kGeoStride + threadIdx.x;
 #pragma unroll
       for (int s = 0; s < kGeoStride; ++s) geo[s] = __ldg(gp + s * T);
-      double G[9], H[9], st[kRefStateScalars];
+      double G[9], H[9], st[ref_state_stride(ST)];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int d = 0; d < 3; ++d) G[3 * c + d] = g[c][d][qz];
-      double J = residual_qf(prm.mu, prm.lambda, G, geo, geo[9], H, st);
-      double* so = prm.state_out + (base + (long long)qz * T) * kStateStride + threadIdx.x;
+      double J;
+      if constexpr (ST == kStorageCurrent)
+        J = residual_qf(prm.mu, prm.lambda, G, geo, geo[9], H, st);
+      else
+        J = residual_qf_initial<ST>(prm.mu, prm.lambda, G, geo, geo[9], H, st);
+      double* so = prm.state_out + (base + (long long)qz * T) * S + threadIdx.x;
       if (!(J > 0.0)) {
         if (tp.e >= 0) {
           unsigned long long idx =
@@ -160,10 +171,15 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams
 #pragma unroll
         for (int k = 0; k < 9; ++k) H[k] = 0.0;
       } else if (tp.e >= 0) {
-        double sp[kStateStride];
-        pack_state(prm.mu, st, sp);
+        if constexpr (ST == kStorageCurrent) {
+          double sp[kStateStride];
+          pack_state(prm.mu, st, sp);
 #pragma unroll
-        for (int s = 0; s < kStateStride; ++s) so[s * T] = sp[s];
+          for (int s = 0; s < kStateStride; ++s) so[s * T] = sp[s];
+        } else {
+#pragma unroll
+          for (int s = 0; s < S; ++s) so[s * T] = st[s];
+        }
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c)

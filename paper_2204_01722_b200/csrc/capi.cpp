@@ -99,8 +99,6 @@ int hxg_state_release(hxg_state_t s) {
 int hxg_op_create(const hxg_op_desc* d, hxg_state_t state, hxg_op_t* out) {
   return guarded([&] {
     if (!d) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "null descriptor");
-    if (d->storage != 0)
-      throw hxg::Error(HXG_ERR_UNSUPPORTED, "only JacobianStorage::Current is implemented");
     int n = d->order + 1, q = d->qpts;
     std::vector<double> interp(d->interp, d->interp + q * n);
     std::vector<double> deriv(d->deriv, d->deriv + q * n);
@@ -112,7 +110,8 @@ int hxg_op_create(const hxg_op_desc* d, hxg_state_t state, hxg_op_t* out) {
       geo = hxg::Operator::make_box_geometry(d->cells, q, d->extents, d->qweights);
     auto* h = new hxg_op_s();
     h->owned = std::make_unique<hxg::Operator>(d->order, q, d->cells, interp, deriv, colloc, d->mu,
-                                               d->lambda, d->mask, state ? state->s : nullptr, geo);
+                                               d->lambda, d->mask, state ? state->s : nullptr, geo,
+                                               d->storage);
     h->op = h->owned.get();
     *out = h;
   });

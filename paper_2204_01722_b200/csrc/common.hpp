@@ -42,6 +42,21 @@ constexpr int kRefStateScalars = 17;
 // one scalar less to stream and ~20 fewer flops per point.  w detJ itself is
 // the geometry's (undeformed) weight, kept in the geometric factors.
 constexpr int kStateStride = 16;
+// JacobianStorage (material.hpp:66-78) and its per-point scalars: the
+// reference's strides; on the device Current uses kStateStride, the initial
+// variants their reference layout.
+constexpr int kStorageCurrent = 0, kStorageInitialNative = 1, kStorageInitialTuned = 2,
+              kStorageInitialAD = 3;
+__host__ __device__ constexpr int ref_state_stride(int storage) {
+  return storage == kStorageInitialNative ? 19
+         : storage == kStorageInitialTuned ? 26
+         : storage == kStorageInitialAD    ? 25
+                                           : kRefStateScalars;
+}
+__host__ __device__ constexpr int device_state_stride(int storage) {
+  return storage == kStorageCurrent ? kStateStride : ref_state_stride(storage);
+}
+constexpr int kMaxStateStride = 26;
 // Geometry per qpt: dxi/dX (9, row-major) then w * detJ (mesh.hpp:169-189).
 constexpr int kGeoStride = 10;
 

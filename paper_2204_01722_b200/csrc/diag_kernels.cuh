@@ -10,6 +10,7 @@
 #include "common.hpp"
 #include "element.cuh"
 #include "qfunction.cuh"
+#include "qfunction_initial.cuh"
 
 namespace hxg {
 
@@ -21,10 +22,11 @@ struct DiagParams {
   const double* state;
   const double* geo;  // geometric factors (w detJ for the perturbation hook)
   double mu, lambda, perturb;
+  int storage;  // JacobianStorage of the state
   double* out;  // diag: E-vector (e, c, a); assembly: (e, 3N^3, 3N^3)
 };
 
-__device__ __forceinline__ long long state_offset(const QLayout& lay, long long e, int qpt) {
+__device__ __forceinline__ long long state_offset(const QLayout& lay, long long e, int qpt, int S) {
   long long ex = e % lay.cells[0], ey = (e / lay.cells[0]) % lay.cells[1],
             ez = e / ((long long)lay.cells[0] * lay.cells[1]);
   long long bx = ex / lay.B[0], by = ey / lay.B[1], bz = ez / lay.B[2];
@@ -34,22 +36,27 @@ __device__ __forceinline__ long long state_offset(const QLayout& lay, long long 
   int Q = lay.Q;
   int qx = qpt % Q, qy = (qpt / Q) % Q, qz = qpt / (Q * Q);
   int t = (qy * Q + qx) * (lay.B[0] * lay.B[1] * lay.B[2]) + le;
-  return ((brick * Q + qz) * kStateStride) * (long long)lay.T + t;
+  return ((brick * Q + qz) * S) * (long long)lay.T + t;
 }
 
 // D[(c1,d1),(c2,d2)] at one point: 9 probes of the Jacobian q-function.
 __device__ __forceinline__ void point_tensor(const DiagParams& prm, long long e, int qpt,
                                              double* d81) {
-  long long off = state_offset(prm.lay, e, qpt);
-  double st[kStateStride];
-#pragma unroll
-  for (int s = 0; s < kStateStride; ++s) st[s] = prm.state[off + (long long)s * prm.lay.T];
+  const int S = device_state_stride(prm.storage);
+  long long off = state_offset(prm.lay, e, qpt, S);
+  double st[kMaxStateStride];
+  for (int s = 0; s < S; ++s) st[s] = prm.state[off + (long long)s * prm.lay.T];
   for (int u = 0; u < 9; ++u) {
     double G[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, H[9];
     G[u] = 1.0;
-    jacobian_qf(prm.mu, prm.lambda, G, st, H);
+    switch (prm.storage) {
+      case kStorageInitialNative: jacobian_qf_initial<kStorageInitialNative>(prm.mu, prm.lambda, G, st, H); break;
+      case kStorageInitialTuned: jacobian_qf_initial<kStorageInitialTuned>(prm.mu, prm.lambda, G, st, H); break;
+      case kStorageInitialAD: jacobian_qf_initial<kStorageInitialAD>(prm.mu, prm.lambda, G, st, H); break;
+      default: jacobian_qf(prm.mu, prm.lambda, G, st, H);
+    }
     if (prm.perturb != 0.0) {  // + eps w detJ G (w detJ = geometry scalar 9, same point)
-      const long long T = prm.lay.T, row = off / T / kStateStride, t = off % T;
+      const long long T = prm.lay.T, row = off / T / S, t = off % T;
       H[u] += prm.perturb * prm.geo[(row * kGeoStride + 9) * T + t];
     }
 #pragma unroll

@@ -93,9 +93,11 @@ std::shared_ptr<Geometry> Operator::make_box_geometry(const int cells[3], int q,
 Operator::Operator(int p, int q, const int cells[3], const std::vector<double>& interp,
                    const std::vector<double>& deriv, const std::vector<double>& colloc, double mu,
                    double lambda, const uint8_t* mask_host, std::shared_ptr<State> state,
-                   std::shared_ptr<Geometry> geometry)
-    : p_(p), q_(q), mu_(mu), lambda_(lambda), interp_(interp), deriv_(deriv), colloc_(colloc),
-      state_(std::move(state)), geometry_(std::move(geometry)) {
+                   std::shared_ptr<Geometry> geometry, int storage)
+    : p_(p), q_(q), mu_(mu), lambda_(lambda), storage_(storage), interp_(interp), deriv_(deriv),
+      colloc_(colloc), state_(std::move(state)), geometry_(std::move(geometry)) {
+  if (storage < kStorageCurrent || storage > kStorageInitialAD)
+    throw Error(HXG_ERR_INVALID_ARGUMENT, "unknown JacobianStorage " + std::to_string(storage));
   dispatch_pq(p, q, [](auto, auto) {});  // validates the pair
   for (int d = 0; d < 3; ++d) {
     if (cells[d] < 1) throw Error(HXG_ERR_INVALID_ARGUMENT, "element counts must be >= 1");
@@ -130,13 +132,16 @@ Operator::Operator(int p, int q, const int cells[3], const std::vector<double>& 
     face_bits_ = gen == mask_host_ ? bits : -1;
   }
   if (!state_) state_ = std::make_shared<State>();
-  size_t need = (size_t)lay_.total_points() * kStateStride;
+  if (state_->storage >= 0 && state_->storage != storage_)
+    throw Error(HXG_ERR_INVALID_ARGUMENT, "quadrature state shared between different JacobianStorage");
+  size_t need = (size_t)lay_.total_points() * device_state_stride(storage_);
   if (state_->data.n != need) {
     state_->data.alloc(need);
     HXG_CUDA(cudaMemset(state_->data.p, 0, need * sizeof(double)));
     state_->lay = lay_;
     state_->valid = false;
   }
+  state_->storage = storage_;
   if (geometry_ && (geometry_->lay.Q != q || geometry_->lay.cells[0] != cells[0] ||
                     geometry_->lay.cells[1] != cells[1] || geometry_->lay.cells[2] != cells[2]))
     throw Error(HXG_ERR_INVALID_ARGUMENT, "geometric factors do not match basis quadrature");
@@ -154,7 +159,8 @@ void Operator::set_external_load(const double* host) {
 double Operator::stored_bytes_per_dof() const {
   // operator.hpp:137-141 — the reference's byte model (state in its own
   // layout: E * q^3 * 17 doubles, plus input and output vectors).
-  double state_bytes = (double)num_elements() * q_ * q_ * q_ * kRefStateScalars * sizeof(double);
+  double state_bytes =
+      (double)num_elements() * q_ * q_ * q_ * ref_state_stride(storage_) * sizeof(double);
   double vec_bytes = 2.0 * (double)size() * sizeof(double);
   return (state_bytes + vec_bytes) / (double)size();
 }
@@ -172,6 +178,7 @@ void Operator::launch_element(int mode, const double* x, bool mask_input) {
   prm.mu = mu_;
   prm.lambda = lambda_;
   prm.perturb = perturb_;
+  prm.storage = storage_;
   if (perturb_ != 0.0 && !prm.geo)
     throw Error(HXG_ERR_INVALID_ARGUMENT, "the perturbation hook needs geometric factors");
   prm.fail = fail_.p;
@@ -183,15 +190,23 @@ void Operator::launch_element(int mode, const double* x, bool mask_input) {
     using D = Dims<P, Q>;
     size_t smem = sizeof(double) * (D::TAB + D::NE * D::ELEM_SMEM);
     int grid = (int)lay_.num_bricks();
-    if (mode == kJacobian) {
-      auto k = element_apply_kernel<P, Q, kJacobian>;
+    auto launch = [&](auto k) {
       HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       k<<<grid, D::T, smem, stream_>>>(prm);
-    } else {
-      auto k = element_apply_kernel<P, Q, kResidual>;
-      HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k<<<grid, D::T, smem, stream_>>>(prm);
-    }
+    };
+    auto by_storage = [&](auto Mc) {
+      constexpr int M = decltype(Mc)::value;
+      switch (storage_) {
+        case kStorageInitialNative: launch(element_apply_kernel<P, Q, M, kStorageInitialNative>); break;
+        case kStorageInitialTuned: launch(element_apply_kernel<P, Q, M, kStorageInitialTuned>); break;
+        case kStorageInitialAD: launch(element_apply_kernel<P, Q, M, kStorageInitialAD>); break;
+        default: launch(element_apply_kernel<P, Q, M, kStorageCurrent>);
+      }
+    };
+    if (mode == kJacobian)
+      by_storage(std::integral_constant<int, kJacobian>{});
+    else
+      by_storage(std::integral_constant<int, kResidual>{});
   });
   HXG_CUDA(cudaGetLastError());
 }
@@ -230,7 +245,7 @@ void Operator::apply_residual(const double* u, double* f) {
     int qz, t;
     lay_.locate(e, qp, brick, qz, t);
     double J = 0.0;
-    size_t off = (size_t)(((brick * lay_.Q + qz) * kStateStride) * lay_.T + t);
+    size_t off = (size_t)(((brick * lay_.Q + qz) * device_state_stride(storage_)) * lay_.T + t);
     HXG_CUDA(cudaMemcpy(&J, state_->data.p + off, sizeof(double), cudaMemcpyDeviceToHost));
     Error err(HXG_ERR_INVERTED_ELEMENT, "non-positive deformation jacobian " + std::to_string(J) +
                                             " in element " + std::to_string(e) +
@@ -248,7 +263,7 @@ void Operator::apply_jacobian_host(const double* xh, double* yh) {
   if (!state_->valid) throw Error(HXG_ERR_STATE_NOT_INITIALIZED,
                                   "quadrature state not initialized: evaluate the residual at the "
                                   "linearization point first");
-  if (variant_ == 0 && fused_supported(p_, q_)) {
+  if (fused()) {
     ++jacobian_applies_;
     fused_jacobian_host(*this, xh, yh);
     return;
@@ -265,16 +280,18 @@ void Operator::apply_jacobian_host(const double* xh, double* yh) {
   HXG_CUDA(cudaStreamSynchronize(stream_));
 }
 
-int Operator::kernel_launches() const {
-  return (variant_ == 0 && fused_supported(p_, q_)) ? fused_launches(p_, q_) : 2;
+bool Operator::fused() const {
+  return variant_ == 0 && storage_ == kStorageCurrent && fused_supported(p_, q_);
 }
+
+int Operator::kernel_launches() const { return fused() ? fused_launches(p_, q_) : 2; }
 
 void Operator::apply_jacobian(const double* du, double* y) {
   if (!state_->valid) throw Error(HXG_ERR_STATE_NOT_INITIALIZED,
                                   "quadrature state not initialized: evaluate the residual at the "
                                   "linearization point first");
   ++jacobian_applies_;
-  if (variant_ == 0 && fused_supported(p_, q_)) {
+  if (fused()) {
     fused_jacobian(*this, du, y);
     return;
   }
@@ -298,6 +315,7 @@ void Operator::extract_diagonal(double* d) {
   prm.mu = mu_;
   prm.lambda = lambda_;
   prm.perturb = perturb_;
+  prm.storage = storage_;
   if (perturb_ != 0.0 && !prm.geo)
     throw Error(HXG_ERR_INVALID_ARGUMENT, "the perturbation hook needs geometric factors");
   prm.out = evec_.p;
@@ -326,6 +344,7 @@ void Operator::element_matrices(double* out) {
   prm.mu = mu_;
   prm.lambda = lambda_;
   prm.perturb = perturb_;
+  prm.storage = storage_;
   if (perturb_ != 0.0 && !prm.geo)
     throw Error(HXG_ERR_INVALID_ARGUMENT, "the perturbation hook needs geometric factors");
   prm.out = out;
@@ -387,6 +406,23 @@ double Operator::total_strain_energy(const double* u) {
 void Operator::export_state(double* host) const {
   // Stored [sqrt(w detJ) xi (9), tau (6), mu - lambda log J] back to the
   // reference's (e, q, 17) Current layout; w detJ from the geometry.
+  if (storage_ != kStorageCurrent) {  // stored in the reference layout already
+    const int S = device_state_stride(storage_);
+    std::vector<double> blocked((size_t)lay_.total_points() * S);
+    HXG_CUDA(cudaMemcpy(blocked.data(), state_->data.p, blocked.size() * sizeof(double),
+                        cudaMemcpyDeviceToHost));
+    const int nq = q_ * q_ * q_;
+    for (long long e = 0; e < num_elements(); ++e)
+      for (int qp = 0; qp < nq; ++qp) {
+        long long brick;
+        int qz, t;
+        lay_.locate(e, qp, brick, qz, t);
+        const size_t base = (size_t)(brick * lay_.Q + qz) * S * lay_.T + t;
+        double* out = host + ((size_t)e * nq + qp) * S;
+        for (int k = 0; k < S; ++k) out[k] = blocked[base + (size_t)k * lay_.T];
+      }
+    return;
+  }
   if (!geometry_) throw Error(HXG_ERR_INVALID_ARGUMENT, "state export needs geometric factors");
   size_t tot = (size_t)lay_.total_points() * kStateStride;
   std::vector<double> blocked(tot), geo((size_t)lay_.total_points() * kGeoStride);

@@ -43,6 +43,7 @@ struct State {
   DevBuf<double> data;
   QLayout lay;
   bool valid = false;
+  int storage = -1;  // JacobianStorage the data is laid out for (-1: unallocated)
 };
 
 // Geometry shared between levels (multigrid.hpp:229-230): blocked layout,
@@ -88,7 +89,7 @@ class Operator {
   Operator(int p, int q, const int cells[3], const std::vector<double>& interp,
            const std::vector<double>& deriv, const std::vector<double>& colloc, double mu,
            double lambda, const uint8_t* mask_host, std::shared_ptr<State> state,
-           std::shared_ptr<Geometry> geometry);
+           std::shared_ptr<Geometry> geometry, int storage = kStorageCurrent);
 
   // Builds a Geometry from reference-layout host arrays (e, q, 9) / (e, q).
   // Affine box geometry computed on the device (no host arrays).
@@ -100,6 +101,10 @@ class Operator {
 
   int p() const { return p_; }
   int q() const { return q_; }
+  int storage() const { return storage_; }
+  // The fused brick kernel serves Current storage; the initial-configuration
+  // variants run the two-pass element path.
+  bool fused() const;
   long long size() const { return 3 * box_.num_nodes(); }
   long long num_elements() const { return box_.num_elements(); }
   const BoxDev& box() const { return box_; }
@@ -160,6 +165,7 @@ class Operator {
   double mu_, lambda_;
   double load_scale_ = 1.0, perturb_ = 0.0;
   int variant_ = 0;
+  int storage_ = kStorageCurrent;
   int face_bits_ = 0;
   std::vector<double> interp_, deriv_, colloc_;
   std::vector<uint8_t> mask_host_;

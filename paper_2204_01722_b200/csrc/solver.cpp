@@ -278,7 +278,7 @@ Hierarchy::Hierarchy(Operator* fine, int fixed_face_mask, std::vector<int> sched
     face_mask(fine->cells(), schedule[s], fixed_face_mask, mask);
     lv.owned = std::make_unique<Operator>(schedule[s], fine->q(), fine->cells(), b.interp, b.deriv,
                                           b.colloc, fine->mu(), fine->lambda(), mask.data(),
-                                          fine->state(), fine->geometry());
+                                          fine->state(), fine->geometry(), fine->storage());
     lv.owned->set_stream(fine->stream());
     lv.op = lv.owned.get();
   }

@@ -115,12 +115,27 @@ def traction_load(extents, cells, order, q, face, traction):
     return load
 
 
+# JacobianStorage (material.hpp:66-78) by its config name (config.hpp:193-198)
+# and the reference's per-point state scalars.
+STORAGES = {"current": 0, "initial-native": 1, "initial-tuned": 2, "initial-ad": 3}
+STATE_SCALARS = {0: 17, 1: 19, 2: 26, 3: 25}
+
+
+def storage_id(storage):
+    if isinstance(storage, str):
+        if storage not in STORAGES:
+            raise ValueError(f"unknown jacobian storage '{storage}'")
+        return STORAGES[storage]
+    return int(storage)
+
+
 class MatrixFreeOperator:
     """MatrixFreeOperator (operator.hpp:70-373) on the GPU."""
 
     def __init__(self, cells, basis: Basis1D, dxidX, weight, mu, lam, mask=None, state=None,
-                 _handle=None, extents=None):
+                 _handle=None, extents=None, storage=0):
         self._owner = _handle is None
+        self.storage = storage_id(storage)
         if _handle is not None:
             self.h = _handle
         else:
@@ -140,7 +155,7 @@ class MatrixFreeOperator:
                 qw = np.ascontiguousarray(basis.weights, np.float64)
                 self._keep += [ext, qw]
                 desc.extents, desc.qweights = _ptr(ext).value, _ptr(qw).value
-            desc.mu, desc.lam, desc.storage = mu, lam, 0
+            desc.mu, desc.lam, desc.storage = mu, lam, self.storage
             if mask is not None:
                 m = np.ascontiguousarray(mask, np.uint8)
                 self._keep.append(m)
@@ -221,7 +236,7 @@ class MatrixFreeOperator:
         return e.value
 
     def export_state(self, num_elements, nq):
-        out = np.zeros((num_elements, nq, 17))
+        out = np.zeros((num_elements, nq, STATE_SCALARS[self.storage]))
         check(lib().hxg_op_export_state(self.h, _ptr(out)))
         return out
 
@@ -276,7 +291,7 @@ class MultigridHierarchy:
     def level_operator(self, k) -> MatrixFreeOperator:
         h = ctypes.c_void_p()
         check(lib().hxg_mg_level_op(self.h, k, ctypes.byref(h)))
-        op = MatrixFreeOperator(None, None, None, None, 0, 0, _handle=h)
+        op = MatrixFreeOperator(None, None, None, None, 0, 0, _handle=h, storage=self.fine.storage)
         op._hier = self  # keep the hierarchy alive
         return op
 
@@ -443,7 +458,7 @@ class FemProblem:
 
     def __init__(self, extents=(1.0, 1.0, 1.0), cells=(2, 2, 2), order=2, q=0,
                  fixed_faces=("-x",), traction_face=None, traction=(0.0, 0.0, 0.0), young=1.0,
-                 poisson=0.3, geometry=True):
+                 poisson=0.3, geometry=True, storage="current"):
         self.extents, self.cells, self.order = tuple(extents), tuple(cells), order
         self.q = q or order + 1
         self.basis = build_lagrange_basis(order, self.q)
@@ -453,7 +468,8 @@ class FemProblem:
         if geometry is True:  # host restatement of compute_geometric_factors
             dx, w = geometric_factors(extents, cells, order, self.q)
         self.op = MatrixFreeOperator(cells, self.basis, dx, w, self.mu, self.lam, self.mask,
-                                     extents=extents if geometry == "box" else None)
+                                     extents=extents if geometry == "box" else None,
+                                     storage=storage)
         self.load = None
         if traction_face is not None:  # assemble_traction_load (operator.hpp:381-443)
             self.load = traction_load(extents, cells, order, self.q, traction_face, traction)

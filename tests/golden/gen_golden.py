@@ -88,6 +88,36 @@ def gen_operator(order, cells, extents, scale, name):
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
 
 
+STORAGES = {1: "initial-native", 2: "initial-tuned", 3: "initial-ad"}
+
+
+def gen_storage():
+    """JacobianStorage variants (material.hpp:66-78, paper Table III):
+    residual, state, Jacobian apply, diagonal and the p-MG PCG of the
+    reference with each initial-configuration storage."""
+    out = {}
+    for order, cells, ext, name in ((2, (4, 2, 2), (2.0, 1.0, 1.0), "q2"),
+                                    (3, (2, 2, 2), (1.0, 1.0, 1.0), "q3")):
+        for st in STORAGES:
+            rp = R.RefProblem(extents=ext, cells=cells, order=order, fixed=("-x",),
+                              traction_face="+x", traction=(0, 0, -0.02), storage=st)
+            u = parity_state(rp, 0.2)
+            k = f"{name}_s{st}_"
+            out[k + "u"], out[k + "f"] = u, rp.apply_residual(u)
+            out[k + "state"] = rp.state()
+            x = 1e-3 * np.sin(0.7 * np.arange(rp.n))
+            out[k + "x"], out[k + "jx"] = x, rp.apply_jacobian(x)
+            out[k + "diag"] = rp.extract_diagonal()
+            out[k + "bytes_per_dof"] = np.array(rp.stored_bytes_per_dof())
+            rp.mg_setup()
+            b = -out[k + "f"]
+            out[k + "vcycle_x"] = rp.vcycle(b)
+            r = rp.cg(b, "mg", 1e-8, 500)
+            out[k + "mgcg_x"], out[k + "mgcg_its"] = r["x"], np.array(r["iterations"])
+            out[k + "meta"] = np.array([order, *cells, *ext])
+    np.savez_compressed(os.path.join(HERE, "storage.npz"), **out)
+
+
 def gen_verify():
     res = R.verify(threads=1)
     bad = R.verify(threads=1, perturbation=1e-3)
@@ -105,4 +135,5 @@ if __name__ == "__main__":
     gen_operator(4, (2, 2, 1), (1.0, 1.0, 1.0), 0.2, "q4_cube")
     gen_operator(1, (4, 2, 2), (2.0, 1.0, 1.0), 0.2, "q1_bar")
     gen_verify()
+    gen_storage()
     print("ok")

@@ -382,3 +382,49 @@ def test_lbfgs_solver():
     good = FemProblem(**kw).solve(load_steps=1, solver=1, lbfgs_memory=5, precond_refresh=10)
     assert good["converged"] and good["final_fnorm"] < 1e-9
     assert rel(good["u"], G["compress1_ls0_u"]) < 1e-7
+
+
+@pytest.mark.parametrize("name", ["q2", "q3"])
+@pytest.mark.parametrize("storage", [1, 2, 3])
+def test_storage_variant_parity(name, storage):
+    """Initial-configuration JacobianStorage variants (material.hpp:66-78,
+    paper Table III) against the reference run with the same storage
+    (tests/golden/storage.npz): residual, stored state, Jacobian apply,
+    diagonal (1e-12), V-cycle and p-MG PCG (iterations +-1)."""
+    from paper_2204_01722_b200.hexmg import FemProblem, cg_solve
+    g = np.load(os.path.join(GOLD, "storage.npz"))
+    k = f"{name}_s{storage}_"
+    meta = g[k + "meta"]
+    order, cells, ext = int(meta[0]), tuple(int(c) for c in meta[1:4]), tuple(meta[4:7])
+    prob = FemProblem(extents=ext, cells=cells, order=order, fixed_faces=("-x",),
+                      traction_face="+x", traction=(0.0, 0.0, -0.02), storage=storage)
+    f = prob.op.apply_residual(cuda(g[k + "u"]))
+    assert rel(f, g[k + "f"]) < 1e-12
+    st = prob.op.export_state(prob.num_elements, prob.nq)
+    assert st.shape == g[k + "state"].shape
+    assert np.abs(st - g[k + "state"]).max() < 1e-12
+    assert rel(prob.op.apply_jacobian(cuda(g[k + "x"])), g[k + "jx"]) < 1e-12
+    assert rel(prob.op.extract_diagonal(), g[k + "diag"]) < 1e-12
+    assert abs(prob.op.stored_bytes_per_dof() - float(g[k + "bytes_per_dof"])) < 1e-9
+    mg = prob.hierarchy
+    mg.setup_numeric()
+    b = -f
+    assert rel(mg.v_cycle(b), g[k + "vcycle_x"]) < 1e-10
+    rep = cg_solve(prob.op, b, rtol=1e-8, precond="mg", mg=mg)
+    assert abs(rep["iterations"] - int(g[k + "mgcg_its"])) <= 1
+    assert rel(rep["x"], g[k + "mgcg_x"]) < 1e-7
+
+
+def test_storage_variants_agree_on_full_size_apply():
+    """Q2 16^3: the four storages linearise the same residual, so their
+    Jacobian applies agree to rounding."""
+    from paper_2204_01722_b200.hexmg import FemProblem
+    ys = []
+    for storage in ("current", "initial-native", "initial-tuned", "initial-ad"):
+        prob = FemProblem(cells=(16, 16, 16), order=2, fixed_faces=("-x",), storage=storage)
+        n = prob.size()
+        s = torch.arange(n, dtype=torch.float64, device="cuda")
+        prob.op.apply_residual(1e-3 * torch.sin(1e-3 * s))
+        ys.append(prob.op.apply_jacobian(1e-3 * torch.sin(0.7 * s)).cpu().numpy())
+    for y in ys[1:]:
+        assert rel(y, ys[0]) < 1e-11

@@ -126,3 +126,24 @@ def test_oracle_against_compiled_reference():
     x = np.sin(np.arange(rp.n))
     assert rel(P.op.apply_jacobian(x), rp.apply_jacobian(x)) < 1e-12
     assert np.array_equal(H.rough_seed(50, None), R.rough_seed(50))
+
+
+@pytest.mark.parametrize("name", ["q2", "q3"])
+@pytest.mark.parametrize("storage", [1, 2, 3])
+def test_storage_variants_match_golden(name, storage):
+    """numpy restatement of the initial-configuration storages (Native,
+    Tuned, forward-mode AD) against the reference run with the same
+    JacobianStorage (tests/golden/storage.npz)."""
+    g = np.load(os.path.join(GOLD, "storage.npz"))
+    k = f"{name}_s{storage}_"
+    meta = g[k + "meta"]
+    order, cells, ext = int(meta[0]), tuple(int(c) for c in meta[1:4]), tuple(meta[4:7])
+    P = H.make_problem(ext, cells, order, fixed_faces=(0,), traction_face=1,
+                       traction=(0.0, 0.0, -0.02), storage=storage)
+    f = P.op.apply_residual(g[k + "u"])
+    assert np.linalg.norm(f - g[k + "f"]) < 1e-12 * np.linalg.norm(g[k + "f"])
+    assert np.abs(P.op.state - g[k + "state"]).max() < 1e-12
+    jx = P.op.apply_jacobian(g[k + "x"])
+    assert np.linalg.norm(jx - g[k + "jx"]) < 1e-12 * np.linalg.norm(g[k + "jx"])
+    d = P.op.extract_diagonal()
+    assert np.linalg.norm(d - g[k + "diag"]) < 1e-12 * np.linalg.norm(g[k + "diag"])
