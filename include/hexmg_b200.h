@@ -60,6 +60,7 @@ typedef struct hxg_state_s* hxg_state_t; /* QuadratureStateStore   operator.hpp:
 typedef struct hxg_op_s* hxg_op_t;       /* MatrixFreeOperator     operator.hpp:70    */
 typedef struct hxg_mg_s* hxg_mg_t;       /* MultigridHierarchy     multigrid.hpp:88   */
 typedef struct hxg_chol_s* hxg_chol_t;   /* CholeskyCoarseSolver   coarse_solver.hpp:16 */
+typedef struct hxg_asm_s* hxg_asm_t;     /* CooAssembly            assembly.hpp:134   */
 
 /*
  * Operator descriptor = the arguments of the MatrixFreeOperator constructor
@@ -196,6 +197,20 @@ int hxg_chol_factorize(hxg_chol_t h, const double* vals_host);
 int hxg_chol_factorize_device(hxg_chol_t h, const double* vals_dev);
 int hxg_chol_solve(hxg_chol_t h, const double* b, double* x);
 int hxg_chol_destroy(hxg_chol_t h);
+
+/* Assembled representation of an operator of any order (CooAssembly:
+ * coo_symbolic / coo_numeric / CsrMatrix::matvec, assembly.hpp:134-230):
+ * CSR over all DoFs, constrained rows and columns reduced to the identity,
+ * slot values summed over elements in increasing element order.  create =
+ * symbolic; numeric needs the operator's state (StateNotInitialized
+ * otherwise); matvec on device vectors.  The "assembled" rows of the
+ * performance study (study.hpp:191-232). */
+int hxg_asm_create(hxg_op_t op, hxg_asm_t* out);
+int hxg_asm_numeric(hxg_asm_t a);
+int hxg_asm_nnz(hxg_asm_t a, int64_t* nnz);
+int hxg_asm_matvec(hxg_asm_t a, const double* x, double* y);
+int hxg_asm_csr_host(hxg_asm_t a, int* row_ptr, int* cols, double* vals);
+int hxg_asm_destroy(hxg_asm_t a);
 
 /* CgReport (cg.hpp:42-50). */
 typedef struct {

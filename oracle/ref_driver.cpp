@@ -16,10 +16,14 @@
 //   ref_vcycle          -> MultigridHierarchy::v_cycle          multigrid.hpp:137
 //   ref_cg              -> cg_solve                             cg.hpp:81
 //   ref_verify          -> run_verification                     verify.hpp:63
+//   ref_parse_config    -> parse_problem_config                 config.hpp:164
+//   ref_accuracy_study  -> run_accuracy_study                   study.hpp:114
+//   ref_performance_study -> run_performance_study              study.hpp:170
 #include <chrono>
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -441,6 +445,71 @@ int ref_verify(int threads, double perturbation, char* out, int cap) {
       s += r.name + ":" + (r.passed ? "1" : "0") + ":" + r.detail + "\n";
   });
   std::snprintf(out, (size_t)cap, "%s", s.c_str());
+  return rc;
+}
+
+// Config parser (config.hpp:164-262): canonical "key=value" dump of the
+// parsed ProblemConfig, or the ConfigError message via ref_last_error.
+int ref_parse_config(const char* text, char* out, int cap) {
+  std::string s;
+  int rc = guarded([&] {
+    std::istringstream in(text);
+    ProblemConfig c = parse_problem_config(in);
+    auto d = [](double v) { return format_double(v); };
+    s += "case_id=" + c.case_id + "\n";
+    s += "extents=" + d(c.extents[0]) + " " + d(c.extents[1]) + " " + d(c.extents[2]) + "\n";
+    s += "cells=" + std::to_string(c.cells[0]) + " " + std::to_string(c.cells[1]) + " " +
+         std::to_string(c.cells[2]) + "\n";
+    s += "order=" + std::to_string(c.order) + "\n";
+    s += "geometry_order=" + std::to_string(c.geometry_order) + "\n";
+    s += "quadrature_points=" + std::to_string(c.quadrature_points) + "\n";
+    NeoHookean m = c.material();
+    s += "material=" + d(m.mu) + " " + d(m.lambda) + "\n";
+    s += "storage=" + std::to_string((int)c.storage) + "\n";
+    s += "fixed_faces=";
+    for (Face f : c.fixed_faces) s += std::to_string((int)f) + " ";
+    s += "\ntraction_face=" + c.traction_face + "\n";
+    s += "traction=" + d(c.traction[0]) + " " + d(c.traction[1]) + " " + d(c.traction[2]) + "\n";
+    s += "body_force=" + d(c.body_force[0]) + " " + d(c.body_force[1]) + " " + d(c.body_force[2]) + "\n";
+    s += "solver=" + std::to_string((int)c.solver) + "\n";
+    s += "newton=" + std::to_string(c.load_steps) + " " + d(c.newton_rtol) + " " + d(c.newton_atol) +
+         " " + std::to_string(c.newton_max_iterations) + " " + d(c.linear_rtol) + " " +
+         std::to_string(c.linear_max_iterations) + " " + std::to_string((int)c.line_search) + " " +
+         std::to_string(c.lbfgs_memory) + " " + std::to_string(c.precond_refresh) + "\n";
+    s += "mg=" + std::to_string(c.mg_pre_smooth) + " " + std::to_string(c.mg_post_smooth) + "\n";
+    s += "flags=" + std::to_string((int)c.deterministic) + " " + std::to_string((int)c.write_vtk) + "\n";
+    s += "study_cases=";
+    for (const auto& k : c.study_cases) s += k.id() + " ";
+    s += "\nstudy_reference=" + c.study_reference.id() + "\n";
+    s += "perf_orders=";
+    for (int o : c.perf_orders) s += std::to_string(o) + " ";
+    s += "\nperf_target_dofs=";
+    for (long t : c.perf_target_dofs) s += std::to_string(t) + " ";
+    s += "\nperf_representations=";
+    for (const auto& r : c.perf_representations) s += r + " ";
+    s += "\nperf_repeats=" + std::to_string(c.perf_repeats) + "\n";
+  });
+  std::snprintf(out, (size_t)cap, "%s", s.c_str());
+  return rc;
+}
+
+// Study harness (study.hpp:114-233) on a config text; CSV into out.
+int ref_accuracy_study(const char* text, char* out, int cap) {
+  std::ostringstream csv;
+  int rc = guarded([&] {
+    std::istringstream in(text);
+    run_accuracy_study(parse_problem_config(in), csv);
+  });
+  std::snprintf(out, (size_t)cap, "%s", csv.str().c_str());
+  return rc;
+}
+int ref_performance_study(const char* text, char* out, int cap) {
+  std::ostringstream csv;
+  int rc = guarded([&] {
+    std::istringstream in(text);
+    run_performance_study(parse_problem_config(in), csv);
+  });
+  std::snprintf(out, (size_t)cap, "%s", csv.str().c_str());
   return rc;
 }
 

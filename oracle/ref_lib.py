@@ -69,6 +69,8 @@ def lib():
         L.ref_newton.argtypes = [vp, i, i, d, vp, vp, vp, vp]
         L.ref_solve.argtypes = [vp, i, i, d, i, i, i, vp, vp, vp, vp]
         L.ref_verify.argtypes = [i, d, vp, i]
+        for name in ("ref_parse_config", "ref_accuracy_study", "ref_performance_study"):
+            getattr(L, name).argtypes = [ctypes.c_char_p, vp, i]
         _lib = L
     return _lib
 
@@ -314,3 +316,26 @@ def verify(threads=1, perturbation=0.0):
         name, ok, detail = line.split(":", 2)
         out[name] = (ok == "1", detail)
     return out
+
+
+def _text_call(name, text, cap=1 << 20):
+    buf = ctypes.create_string_buffer(cap)
+    rc = getattr(lib(), name)(text.encode(), ctypes.cast(buf, ctypes.c_void_p), cap)
+    if rc != 0:
+        raise RefError(rc, lib().ref_last_error().decode())
+    return buf.value.decode()
+
+
+def parse_config(text):
+    """parse_problem_config -> canonical 'key=value' dump (ref_driver.cpp)."""
+    return _text_call("ref_parse_config", text)
+
+
+def accuracy_study(text):
+    """run_accuracy_study CSV for a config text."""
+    return _text_call("ref_accuracy_study", text)
+
+
+def performance_study(text):
+    """run_performance_study CSV for a config text."""
+    return _text_call("ref_performance_study", text)

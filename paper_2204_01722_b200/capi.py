@@ -157,6 +157,12 @@ SIGNATURES = {
     "hxg_chol_create": [_i, _vp, _vp, _vp, _i, _vp],
     "hxg_chol_factorize": [_vp, _vp],
     "hxg_chol_factorize_device": [_vp, _vp],
+    "hxg_asm_create": [_vp, _vp],
+    "hxg_asm_numeric": [_vp],
+    "hxg_asm_nnz": [_vp, _vp],
+    "hxg_asm_matvec": [_vp, _vp, _vp],
+    "hxg_asm_csr_host": [_vp, _vp, _vp, _vp],
+    "hxg_asm_destroy": [_vp],
     "hxg_mg_coarse_vals_device": [_vp, _vp],
     "hxg_chol_solve": [_vp, _vp, _vp],
     "hxg_chol_destroy": [_vp],

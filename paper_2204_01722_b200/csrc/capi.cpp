@@ -483,6 +483,46 @@ int hxg_chol_destroy(hxg_chol_t h) {
   return guarded([&] { delete h; });
 }
 
+struct hxg_asm_s {
+  hxg::Operator* op;
+  std::unique_ptr<hxg::CoarseAssembly> a;
+};
+
+int hxg_asm_create(hxg_op_t op, hxg_asm_t* out) {
+  return guarded([&] {
+    auto* h = new hxg_asm_s();
+    h->op = &OP(op);
+    h->a = std::make_unique<hxg::CoarseAssembly>(OP(op));
+    *out = h;
+  });
+}
+int hxg_asm_numeric(hxg_asm_t a) {
+  return guarded([&] {
+    a->a->numeric(*a->op);
+    HXG_CUDA(cudaStreamSynchronize(a->op->stream()));
+  });
+}
+int hxg_asm_nnz(hxg_asm_t a, int64_t* nnz) {
+  return guarded([&] { *nnz = a->a->matrix().nnz(); });
+}
+int hxg_asm_matvec(hxg_asm_t a, const double* x, double* y) {
+  return guarded([&] { a->a->matvec(x, y, a->op->stream()); });
+}
+int hxg_asm_csr_host(hxg_asm_t a, int* row_ptr, int* cols, double* vals) {
+  return guarded([&] {
+    const auto& m = a->a->matrix();
+    if (row_ptr) std::memcpy(row_ptr, m.row_ptr_h.data(), sizeof(int) * m.row_ptr_h.size());
+    if (cols) std::memcpy(cols, m.cols_h.data(), sizeof(int) * m.cols_h.size());
+    if (vals) {
+      HXG_CUDA(cudaStreamSynchronize(a->op->stream()));
+      HXG_CUDA(cudaMemcpy(vals, m.vals.p, sizeof(double) * m.cols_h.size(), cudaMemcpyDeviceToHost));
+    }
+  });
+}
+int hxg_asm_destroy(hxg_asm_t a) {
+  return guarded([&] { delete a; });
+}
+
 namespace {
 hxg::NewtonConfig to_config(const hxg_newton_config* c) {
   hxg::NewtonConfig nc;

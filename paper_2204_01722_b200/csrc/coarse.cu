@@ -14,12 +14,19 @@ namespace hxg {
 
 namespace {
 
+// Elements containing node coordinate g along one axis (order P, c cells).
+__host__ __device__ inline void node_elems(int g, int P, int c, int& lo, int& hi) {
+  lo = g > 0 ? (g - 1) / P : 0;
+  hi = g / P < c - 1 ? g / P : c - 1;
+}
+
 // Per-slot value: sum over the elements shared by the row and column nodes,
 // ascending element index (the reference COO entry order, assembly.hpp:121-130).
+template <int P>
 __global__ void fill_csr_kernel(BoxDev box, const int* __restrict__ rows,
                                 const int* __restrict__ cols, const uint8_t* __restrict__ mask,
                                 const double* __restrict__ elem, long long nnz, double* vals) {
-  constexpr int N = 2, N3 = 8, M = 24;
+  constexpr int N = P + 1, M = 3 * N * N * N;
   for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < nnz;
        s += (long long)gridDim.x * blockDim.x) {
     int r = rows[s], c = cols[s];
@@ -36,20 +43,38 @@ __global__ void fill_csr_kernel(BoxDev box, const int* __restrict__ rows,
     int lo[3], hi[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      lo[d] = max(max(g[d], h[d]) - 1, 0);
-      hi[d] = min(min(g[d], h[d]), box.cells[d] - 1);
+      int l1, h1, l2, h2;
+      node_elems(g[d], P, box.cells[d], l1, h1);
+      node_elems(h[d], P, box.cells[d], l2, h2);
+      lo[d] = max(l1, l2);
+      hi[d] = min(h1, h2);
     }
     double acc = 0.0;
     for (int ez = lo[2]; ez <= hi[2]; ++ez)
       for (int ey = lo[1]; ey <= hi[1]; ++ey)
         for (int ex = lo[0]; ex <= hi[0]; ++ex) {
           long long e = ex + box.cells[0] * (ey + (long long)box.cells[1] * ez);
-          int a = (g[0] - ex) + N * ((g[1] - ey) + N * (g[2] - ez));
-          int b = (h[0] - ex) + N * ((h[1] - ey) + N * (h[2] - ez));
+          int a = (g[0] - P * ex) + N * ((g[1] - P * ey) + N * (g[2] - P * ez));
+          int b = (h[0] - P * ex) + N * ((h[1] - P * ey) + N * (h[2] - P * ez));
           acc += elem[e * (M * M) + (a * 3 + ca) * M + b * 3 + cb];
         }
-    (void)N3;
     vals[s] = acc;
+  }
+}
+
+// CsrMatrix::matvec (assembly.hpp): one warp per row, lanes over the row's
+// slots, fixed-order shuffle reduction.
+__global__ void csr_matvec_kernel(int n, const int* __restrict__ row_ptr,
+                                  const int* __restrict__ cols, const double* __restrict__ vals,
+                                  const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((long long)gridDim.x * blockDim.x) >> 5) {
+    double acc = 0.0;
+    for (int s = row_ptr[r] + lane; s < row_ptr[r + 1]; s += 32) acc += vals[s] * __ldg(x + cols[s]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[r] = acc;
   }
 }
 
@@ -63,35 +88,40 @@ __global__ void csr_to_dense_kernel(const int* rows, const int* cols, const doub
 }  // namespace
 
 CoarseAssembly::CoarseAssembly(const Operator& op) {
-  if (op.p() != 1) throw Error(HXG_ERR_UNSUPPORTED, "coarse assembly expects the p = 1 level");
   box_ = op.box();
+  const int P = op.p();
   const auto& mask = op.mask_host();
   long long nn = box_.num_nodes();
+  if (3 * nn > 0x7fffffffLL) throw Error(HXG_ERR_UNSUPPORTED, "assembled operator exceeds int32 rows");
   int n = (int)(3 * nn);
   a_.n = n;
   auto fixed = [&](long long dof) { return !mask.empty() && mask[(size_t)dof] != 0; };
+  const long long per_row = 3LL * (2 * P + 1) * (2 * P + 1) * (2 * P + 1);
   a_.row_ptr_h.assign((size_t)n + 1, 0);
   a_.cols_h.clear();
-  a_.cols_h.reserve((size_t)n * 81);
+  a_.cols_h.reserve((size_t)std::min<long long>((long long)n * per_row, 1LL << 31));
   std::vector<int> rows;
-  rows.reserve((size_t)n * 81);
+  rows.reserve(a_.cols_h.capacity());
   for (long long node = 0; node < nn; ++node) {
     int g[3] = {(int)(node % box_.npd[0]), (int)((node / box_.npd[0]) % box_.npd[1]),
                 (int)(node / ((long long)box_.npd[0] * box_.npd[1]))};
+    int lo[3], hi[3];  // node range of the elements containing the node
+    for (int d = 0; d < 3; ++d) {
+      int el, eh;
+      node_elems(g[d], P, box_.cells[d], el, eh);
+      lo[d] = P * el;
+      hi[d] = P * (eh + 1);
+    }
     for (int ca = 0; ca < 3; ++ca) {
       long long r = 3 * node + ca;
       if (fixed(r)) {
         a_.cols_h.push_back((int)r);
         rows.push_back((int)r);
       } else {
-        for (int dz = -1; dz <= 1; ++dz)
-          for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-              int h[3] = {g[0] + dx, g[1] + dy, g[2] + dz};
-              bool ok = true;
-              for (int d = 0; d < 3; ++d) ok = ok && h[d] >= 0 && h[d] < box_.npd[d];
-              if (!ok) continue;
-              long long nb = h[0] + box_.npd[0] * (h[1] + (long long)box_.npd[1] * h[2]);
+        for (int hz = lo[2]; hz <= hi[2]; ++hz)
+          for (int hy = lo[1]; hy <= hi[1]; ++hy)
+            for (int hx = lo[0]; hx <= hi[0]; ++hx) {
+              long long nb = hx + box_.npd[0] * (hy + (long long)box_.npd[1] * hz);
               for (int cb = 0; cb < 3; ++cb) {
                 long long c = 3 * nb + cb;
                 if (fixed(c)) continue;
@@ -100,6 +130,8 @@ CoarseAssembly::CoarseAssembly(const Operator& op) {
               }
             }
       }
+      if (a_.cols_h.size() > 0x7fffffffULL)
+        throw Error(HXG_ERR_UNSUPPORTED, "assembled operator exceeds int32 nonzeros");
       a_.row_ptr_h[(size_t)r + 1] = (int)a_.cols_h.size();
     }
   }
@@ -116,12 +148,21 @@ CoarseAssembly::CoarseAssembly(const Operator& op) {
 }
 
 void CoarseAssembly::numeric(Operator& op) {
-  size_t need = (size_t)op.num_elements() * 24 * 24;
-  if (elem_.n != need) elem_.alloc(need);
-  op.element_matrices(elem_.p);
-  long long nnz = a_.nnz();
-  fill_csr_kernel<<<grid_for(nnz, 256), 256, 0, op.stream()>>>(box_, a_.rows.p, a_.cols.p, mask_.p,
-                                                                 elem_.p, nnz, a_.vals.p);
+  dispatch_p(op.p(), [&](auto Pc) {
+    constexpr int P = decltype(Pc)::value, M = 3 * (P + 1) * (P + 1) * (P + 1);
+    size_t need = (size_t)op.num_elements() * M * M;
+    if (elem_.n != need) elem_.alloc(need);
+    op.element_matrices(elem_.p);
+    long long nnz = a_.nnz();
+    fill_csr_kernel<P><<<grid_for(nnz, 256), 256, 0, op.stream()>>>(box_, a_.rows.p, a_.cols.p,
+                                                                     mask_.p, elem_.p, nnz, a_.vals.p);
+  });
+  HXG_CUDA(cudaGetLastError());
+}
+
+void CoarseAssembly::matvec(const double* x, double* y, cudaStream_t s) const {
+  csr_matvec_kernel<<<grid_for((long long)a_.n * 32, 256), 256, 0, s>>>(a_.n, a_.row_ptr.p, a_.cols.p,
+                                                                        a_.vals.p, x, y);
   HXG_CUDA(cudaGetLastError());
 }
 

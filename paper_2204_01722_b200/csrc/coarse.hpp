@@ -20,13 +20,18 @@ struct CsrMatrix {
 
 class CoarseAssembly {
  public:
-  // Symbolic phase (coo_symbolic): the CSR pattern of the box Q1 operator
-  // with constrained rows/columns reduced to the identity.
+  // Symbolic phase (coo_symbolic): the CSR pattern of the box operator of
+  // any order (every node pair sharing an element) with constrained
+  // rows/columns reduced to the identity.  The p = 1 level is the coarse
+  // operator; higher orders serve the "assembled" representation of the
+  // performance study (study.hpp:191-232).
   explicit CoarseAssembly(const Operator& op);
   // Numeric phase (coo_numeric + fill_from_coo): element matrices, then a
   // per-slot sum over elements in increasing element order.
   void numeric(Operator& op);
   const CsrMatrix& matrix() const { return a_; }
+  // y = A x (CsrMatrix::matvec), device vectors.
+  void matvec(const double* x, double* y, cudaStream_t s) const;
 
  private:
   CsrMatrix a_;

@@ -348,11 +348,10 @@ void Operator::element_matrices(double* out) {
   if (perturb_ != 0.0 && !prm.geo)
     throw Error(HXG_ERR_INVALID_ARGUMENT, "the perturbation hook needs geometric factors");
   prm.out = out;
-  if (p_ != 1) throw Error(HXG_ERR_UNSUPPORTED, "assembly is implemented for the p = 1 coarse level");
-  dispatch_q(q_, [&](auto Qc) {
-    constexpr int Q = decltype(Qc)::value;
-    size_t smem = sizeof(double) * (2 * Q * 2 + Q * Q * Q * 81);
-    auto k = assemble_element_kernel<1, Q>;
+  dispatch_pq(p_, q_, [&](auto Pc, auto Qc) {
+    constexpr int P = decltype(Pc)::value, Q = decltype(Qc)::value;
+    size_t smem = sizeof(double) * (2 * Q * (P + 1) + Q * Q * Q * 81);
+    auto k = assemble_element_kernel<P, Q>;
     HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<(unsigned)num_elements(), 256, smem, stream_>>>(prm);
   });

@@ -129,6 +129,25 @@ def storage_id(storage):
     return int(storage)
 
 
+def body_force_load(extents, cells, basis: Basis1D, force):
+    """assemble_body_force_load (operator.hpp:440-456) for the box mesh:
+    load[node, c] = f_c sum_e sum_q w detJ N_a(q).  The box map is affine and
+    tensor-product, so the assembled vector is f_c detJ (m_x x m_y x m_z) with
+    m_d the assembled 1D vectors sum_i w_i B[i, a] (host setup, once)."""
+    p, q = basis.order, basis.q
+    B = np.asarray(basis.interp).reshape(q, p + 1)
+    s = np.asarray(basis.weights) @ B  # (p+1,) 1D element integrals
+    ms = []
+    for d in range(3):
+        m = np.zeros(p * cells[d] + 1)
+        for e in range(cells[d]):
+            m[p * e:p * e + p + 1] += s
+        ms.append(m)
+    detj = np.prod([extents[d] / (2.0 * cells[d]) for d in range(3)])
+    nodal = detj * np.einsum("k,j,i->kji", ms[2], ms[1], ms[0]).ravel()
+    return np.ascontiguousarray((nodal[:, None] * np.asarray(force, np.float64)[None, :]).ravel())
+
+
 class MatrixFreeOperator:
     """MatrixFreeOperator (operator.hpp:70-373) on the GPU."""
 
@@ -359,6 +378,47 @@ class MultigridHierarchy:
         return x
 
 
+class AssembledOperator:
+    """CooAssembly (assembly.hpp:134-230) of a MatrixFreeOperator of any
+    order on the device: CSR symbolic at construction, numeric() from the
+    operator's current state, matvec = CsrMatrix::matvec."""
+
+    def __init__(self, op: MatrixFreeOperator):
+        self.op = op
+        h = ctypes.c_void_p()
+        check(lib().hxg_asm_create(op.h, ctypes.byref(h)))
+        self.h = h
+        nnz = ctypes.c_int64()
+        check(lib().hxg_asm_nnz(self.h, ctypes.byref(nnz)))
+        self.nnz = nnz.value
+        self.n = op.size()
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib().hxg_asm_destroy(self.h)
+            except Exception:  # interpreter shutdown
+                pass
+            self.h = None
+
+    def numeric(self):
+        check(lib().hxg_asm_numeric(self.h))
+
+    def matvec(self, x, y=None):
+        x = _dev(x, self.n)
+        if y is None:
+            y = torch.empty_like(x)
+        check(lib().hxg_asm_matvec(self.h, _ptr(x), _ptr(y)))
+        return y
+
+    def csr(self):
+        rp = np.zeros(self.n + 1, np.int32)
+        cols = np.zeros(self.nnz, np.int32)
+        vals = np.zeros(self.nnz, np.float64)
+        check(lib().hxg_asm_csr_host(self.h, _ptr(rp), _ptr(cols), _ptr(vals)))
+        return rp, cols, vals
+
+
 class CoarseCholesky:
     """CholeskyCoarseSolver (coarse_solver.hpp:16-47) on a caller-assembled
     Q1 lattice matrix: analyzePattern at construction, factorize(vals),
@@ -458,11 +518,16 @@ class FemProblem:
 
     def __init__(self, extents=(1.0, 1.0, 1.0), cells=(2, 2, 2), order=2, q=0,
                  fixed_faces=("-x",), traction_face=None, traction=(0.0, 0.0, 0.0), young=1.0,
-                 poisson=0.3, geometry=True, storage="current"):
+                 poisson=0.3, geometry=True, storage="current", body_force=(0.0, 0.0, 0.0),
+                 mu=None, lam=None, mg_smoothing=(1, 1)):
         self.extents, self.cells, self.order = tuple(extents), tuple(cells), order
         self.q = q or order + 1
         self.basis = build_lagrange_basis(order, self.q)
-        self.mu, self.lam = lame_from_young_poisson(young, poisson)
+        if mu is not None:  # explicit Lame parameters (config.hpp:82-85)
+            self.mu, self.lam = mu, lam
+        else:
+            self.mu, self.lam = lame_from_young_poisson(young, poisson)
+        self.mg_smoothing = tuple(mg_smoothing)
         self.mask, self.fixed_face_mask = constraint_mask(cells, order, fixed_faces)
         dx = w = None
         if geometry is True:  # host restatement of compute_geometric_factors
@@ -473,6 +538,9 @@ class FemProblem:
         self.load = None
         if traction_face is not None:  # assemble_traction_load (operator.hpp:381-443)
             self.load = traction_load(extents, cells, order, self.q, traction_face, traction)
+        if any(b != 0.0 for b in body_force):  # assemble_body_force_load (operator.hpp:440-456)
+            bf = body_force_load(extents, cells, self.basis, body_force)
+            self.load = bf if self.load is None else self.load + bf
         self.op.set_external_load(self.load)
         self.num_elements = cells[0] * cells[1] * cells[2]
         self.nq = self.q**3
@@ -498,5 +566,7 @@ class FemProblem:
     @property
     def hierarchy(self) -> MultigridHierarchy:
         if self._mg is None:
-            self._mg = MultigridHierarchy(self.op, self.fixed_face_mask)
+            self._mg = MultigridHierarchy(self.op, self.fixed_face_mask,
+                                          pre_smooth=self.mg_smoothing[0],
+                                          post_smooth=self.mg_smoothing[1])
         return self._mg

@@ -428,3 +428,69 @@ def test_storage_variants_agree_on_full_size_apply():
         ys.append(prob.op.apply_jacobian(1e-3 * torch.sin(0.7 * s)).cpu().numpy())
     for y in ys[1:]:
         assert rel(y, ys[0]) < 1e-11
+
+
+def _csv(text):
+    rows = [r.split(",") for r in text.strip().splitlines()]
+    return rows[0], rows[1:]
+
+
+def test_accuracy_study_matches_reference_csv():
+    """run_accuracy_study (study.hpp:114-141) on a small body-force +
+    traction config: every deterministic CSV column against the reference's
+    own CSV (tests/golden/harness.json).  The reference's post-line-search
+    residual quirk is reproduced so Newton stops where the reference's does."""
+    import io
+    import json
+    from paper_2204_01722_b200.config import parse_problem_config
+    from paper_2204_01722_b200.study import run_accuracy_study
+    G = json.load(open(os.path.join(GOLD, "harness.json")))
+    out = io.StringIO()
+    run_accuracy_study(parse_problem_config(G["accuracy_config"]), out,
+                       reference_line_search_quirk=True)
+    h1, ours = _csv(out.getvalue())
+    h2, ref = _csv(G["accuracy_csv"])
+    assert h1 == h2 and len(ours) == len(ref)
+    for a, b in zip(ours, ref):
+        assert a[:4] == b[:4]  # case_id, order, refinement, dofs
+        assert abs(float(a[4]) - float(b[4])) <= 1e-10 * abs(float(b[4]))  # strain energy
+        assert abs(float(a[5]) - float(b[5])) <= 1e-8 * max(abs(float(b[5])), 1e-12)
+        assert a[6] == b[6]  # newton iterations
+        assert abs(int(a[7]) - int(b[7])) <= int(a[6])  # cg iterations (+-1 per solve)
+        assert abs(float(a[8]) - float(b[8])) <= 1e-6 * float(b[8])  # condition estimate
+        assert float(a[9]) == float(b[9])  # bytes per dof
+
+
+def test_performance_study_matches_reference_csv():
+    """run_performance_study (study.hpp:170-233): case sizes, DoFs, assembled
+    nonzeros, bytes per DoF and status against the reference's CSV; the
+    assembled matvec equals the matrix-free apply."""
+    import io
+    import json
+    from paper_2204_01722_b200.config import parse_problem_config
+    from paper_2204_01722_b200.study import run_performance_study
+    G = json.load(open(os.path.join(GOLD, "harness.json")))
+    out = io.StringIO()
+    recs = run_performance_study(parse_problem_config(G["performance_config"]), out)
+    h1, ours = _csv(out.getvalue())
+    h2, ref = _csv(G["performance_csv"])
+    assert h1 == h2 and len(ours) == len(ref)
+    for a, b in zip(ours, ref):
+        assert a[:6] == b[:6]  # case_id, representation, order, cells, dofs, nnz
+        assert abs(float(a[6]) - float(b[6])) <= 1e-12 * float(b[6])
+        assert a[7:9] == b[7:9]  # applies, status
+    assert all(r["dofs_per_second"] > 0 for r in recs)
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_assembled_matvec_equals_matrix_free(order):
+    from paper_2204_01722_b200.hexmg import AssembledOperator, FemProblem
+    prob = FemProblem(extents=(2.0, 1.0, 1.0), cells=(4, 2, 2), order=order, fixed_faces=("-x",),
+                      traction_face="+x", traction=(0.0, 0.0, -0.02), body_force=(0.0, 0.01, 0.0))
+    n = prob.size()
+    s = torch.arange(n, dtype=torch.float64, device="cuda")
+    prob.op.apply_residual(1e-2 * torch.sin(1e-2 * s))
+    A = AssembledOperator(prob.op)
+    A.numeric()
+    x = torch.cos(0.3 * s)
+    assert rel(A.matvec(x), prob.op.apply_jacobian(x).cpu().numpy()) < 1e-12
