@@ -34,6 +34,7 @@
 #include "hexmg/problem.hpp"
 #include "hexmg/multigrid.hpp"
 #include "hexmg/nonlinear.hpp"
+#include "hexmg/vtk.hpp"
 
 using namespace hexmg;
 
@@ -490,6 +491,18 @@ int ref_parse_config(const char* text, char* out, int cap) {
     s += "\nperf_repeats=" + std::to_string(c.perf_repeats) + "\n";
   });
   std::snprintf(out, (size_t)cap, "%s", s.c_str());
+  return rc;
+}
+
+// Legacy VTK of a displacement field on the problem's mesh (vtk.hpp:15-55).
+int ref_write_vtk(void* p, const double* u, char* out, int cap) {
+  std::ostringstream os;
+  int rc = guarded([&] {
+    auto* h = static_cast<RefProblem*>(p);
+    const BoxMesh& m = h->problem->mesh();
+    write_vtk(os, m, std::span<const double>(u, (size_t)m.num_dofs()));
+  });
+  std::snprintf(out, (size_t)cap, "%s", os.str().c_str());
   return rc;
 }
 

@@ -69,6 +69,7 @@ def lib():
         L.ref_newton.argtypes = [vp, i, i, d, vp, vp, vp, vp]
         L.ref_solve.argtypes = [vp, i, i, d, i, i, i, vp, vp, vp, vp]
         L.ref_verify.argtypes = [i, d, vp, i]
+        L.ref_write_vtk.argtypes = [vp, vp, vp, i]
         for name in ("ref_parse_config", "ref_accuracy_study", "ref_performance_study"):
             getattr(L, name).argtypes = [ctypes.c_char_p, vp, i]
         _lib = L
@@ -149,6 +150,13 @@ class RefProblem:
 
     def set_time(self, t):
         lib().ref_set_time(self.h, t)
+
+    def write_vtk(self, u, cap=1 << 24):
+        """write_vtk (vtk.hpp:15-55) of u on this problem's mesh, as text."""
+        buf = ctypes.create_string_buffer(cap)
+        u = np.ascontiguousarray(u, np.float64)
+        _check(lib().ref_write_vtk(self.h, _p(u), ctypes.cast(buf, ctypes.c_void_p), cap))
+        return buf.value.decode()
 
     def coords(self):
         out = np.zeros(self.n)

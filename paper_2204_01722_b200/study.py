@@ -182,3 +182,13 @@ def run_performance_study(base: ProblemConfig, csv, log=None):
                 csv.write(performance_csv_row(rec) + "\n")
                 records.append(rec)
     return records
+
+
+if __name__ == "__main__":
+    import sys
+    from .config import load_problem_config
+    if len(sys.argv) != 3 or sys.argv[2] not in ("accuracy", "performance"):
+        sys.exit("usage: python -m paper_2204_01722_b200.study <config> accuracy|performance")
+    cfg = load_problem_config(sys.argv[1])
+    run = run_accuracy_study if sys.argv[2] == "accuracy" else run_performance_study
+    run(cfg, sys.stdout, sys.stderr)

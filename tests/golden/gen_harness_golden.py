@@ -55,6 +55,37 @@ perf_repeats = 3
 """
 
 
+VTK_CASES = [(2, (2, 1, 1), (2.0, 1.0, 1.0)), (3, (1, 2, 1), (1.0, 1.5, 0.7)),
+             (1, (2, 2, 2), (1.0, 1.0, 1.0))]
+
+# The reference's write_vtk formats doubles through std::ostream, which
+# crashes once numpy's bundled libraries are in the process; run it in a
+# ctypes-only child.
+_VTK_CHILD = r"""
+import ctypes, json, math, sys
+order, cells, ext = json.loads(sys.argv[1])
+L = ctypes.CDLL(sys.argv[2])
+L.ref_create.restype = ctypes.c_void_p
+h = L.ref_create((ctypes.c_double * 3)(*ext), (ctypes.c_int * 3)(*cells), order, 0, 1, -1,
+                 (ctypes.c_double * 3)(0, 0, 0), ctypes.c_double(1.0), ctypes.c_double(0.3), 1)
+n = L.ref_size(ctypes.c_void_p(h))
+u = (ctypes.c_double * n)(*[1.2345678912345e-3 * math.sin(0.37 * i) for i in range(n)])
+buf = ctypes.create_string_buffer(1 << 22)
+assert L.ref_write_vtk(ctypes.c_void_p(h), u, buf, 1 << 22) == 0
+sys.stdout.write(buf.value.decode())
+"""
+
+
+def gen_vtk():
+    import subprocess
+    out = []
+    for order, cells, ext in VTK_CASES:
+        text = subprocess.run([sys.executable, "-c", _VTK_CHILD, json.dumps([order, cells, ext]),
+                               R.LIB_PATH], check=True, capture_output=True, text=True).stdout
+        out.append({"order": order, "cells": cells, "extents": ext, "vtk": text})
+    return out
+
+
 def main():
     parse = []
     for text in PARSE_CASES:
@@ -63,7 +94,8 @@ def main():
         except R.RefError as e:
             parse.append({"text": text, "error": str(e).split("] ", 1)[-1]})
     out = {"parse": parse, "accuracy_config": ACCURACY, "accuracy_csv": R.accuracy_study(ACCURACY),
-           "performance_config": PERFORMANCE, "performance_csv": R.performance_study(PERFORMANCE)}
+           "performance_config": PERFORMANCE, "performance_csv": R.performance_study(PERFORMANCE),
+           "vtk": gen_vtk()}
     with open(os.path.join(HERE, "harness.json"), "w") as f:
         json.dump(out, f, indent=1)
     print("ok")
