@@ -494,3 +494,16 @@ def test_assembled_matvec_equals_matrix_free(order):
     A.numeric()
     x = torch.cos(0.3 * s)
     assert rel(A.matvec(x), prob.op.apply_jacobian(x).cpu().numpy()) < 1e-12
+
+
+@pytest.mark.parametrize("perturbation", [0.0, 1e-3])
+def test_verify_suite_matches_reference(perturbation):
+    """run_verification (verify.hpp:63-285) through this framework: the same
+    named checks pass / fail as in the reference (tests/golden/verify.npz),
+    with and without the Jacobian perturbation hook."""
+    from paper_2204_01722_b200.verify import run_verification
+    g = np.load(os.path.join(GOLD, "verify.npz"))
+    expect = dict(zip(g["names"].tolist(), (g["passed"] if perturbation == 0.0
+                                             else g["passed_perturbed"]).tolist()))
+    got = {name: ok for name, ok, _ in run_verification(perturbation)}
+    assert got == expect, {k: (got.get(k), v) for k, v in expect.items() if got.get(k) != v}
