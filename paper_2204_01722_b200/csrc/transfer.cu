@@ -4,6 +4,8 @@
 // contraction order; the node-ordered sum (node_kernels.cuh) scatters.
 #include "transfer.hpp"
 
+#include <cstdlib>
+
 #include "dispatch.hpp"
 #include "node_kernels.cuh"
 
@@ -58,6 +60,68 @@ __global__ void prolong_element_kernel(TransferParams prm) {
       out += prm.ctof[k * NC + kc] * t2;
     }
     prm.evec[(e * 3 + c) * NF3 + a] = out;
+  }
+}
+
+// Prolong fused with the node-ordered average: one thread per fine node
+// evaluates, for each element containing it (ascending element index, the
+// order of node_sum_kernel), the per-entry interpolation above with the same
+// operation sequence, sums them from 0 and scales by 1/m -- bitwise the
+// element kernel + node_sum_kernel(kEpiInvMult) pair, without the E-vector
+// round trip (Q2 64^3: 170 MB written and re-read).  The coarse values are
+// L1/L2-resident (neighbouring fine nodes share them).
+template <int NF, int NC>
+__global__ void __launch_bounds__(256) prolong_node_kernel(TransferParams prm) {
+  constexpr int PF = NF - 1, PC = NC - 1;
+  const BoxDev& f = prm.fine;
+  const BoxDev& cb = prm.coarse;
+  const long long nn = f.num_nodes();
+  for (long long node = blockIdx.x * (long long)blockDim.x + threadIdx.x; node < nn;
+       node += (long long)gridDim.x * blockDim.x) {
+    const int g[3] = {(int)(node % f.npd[0]), (int)((node / f.npd[0]) % f.npd[1]),
+                      (int)(node / ((long long)f.npd[0] * f.npd[1]))};
+    int lo[3], hi[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int e = g[d] / PF;
+      if (g[d] % PF == 0) {
+        lo[d] = e > 0 ? e - 1 : 0;
+        hi[d] = e < f.cells[d] ? e : f.cells[d] - 1;
+      } else {
+        lo[d] = hi[d] = e;
+      }
+    }
+    double s[3] = {0.0, 0.0, 0.0};
+    int mult = 0;
+    for (int ez = lo[2]; ez <= hi[2]; ++ez)
+      for (int ey = lo[1]; ey <= hi[1]; ++ey)
+        for (int ex = lo[0]; ex <= hi[0]; ++ex) {
+          const int i = g[0] - PF * ex, j = g[1] - PF * ey, k = g[2] - PF * ez;
+          const double* xb = prm.in + 3 * ((PC * ex) + cb.npd[0] * ((long long)(PC * ey) +
+                                                                  (long long)cb.npd[1] * (PC * ez)));
+          const long long sy = 3LL * cb.npd[0], sz = 3LL * cb.npd[0] * cb.npd[1];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            double out = 0.0;
+#pragma unroll
+            for (int kc = 0; kc < NC; ++kc) {
+              double t2 = 0.0;
+#pragma unroll
+              for (int jc = 0; jc < NC; ++jc) {
+                double t1 = 0.0;
+#pragma unroll
+                for (int ic = 0; ic < NC; ++ic)
+                  t1 += prm.ctof[i * NC + ic] * __ldg(xb + 3 * ic + sy * jc + sz * kc + c);
+                t2 += prm.ctof[j * NC + jc] * t1;
+              }
+              out += prm.ctof[k * NC + kc] * t2;
+            }
+            s[c] += out;
+          }
+          ++mult;
+        }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) prm.evec[3 * node + c] = s[c] * (1.0 / (double)mult);
   }
 }
 
@@ -150,6 +214,15 @@ Transfer::Transfer(const int cells[3], int fine_order, int coarse_order)
 }
 
 void Transfer::prolong(const double* xc, double* xf, cudaStream_t s) {
+  if (!getenv("HXG_PROLONG_TWO_PASS")) {
+    TransferParams prm{fine_, coarse_, ctof_.p, xc, xf, {}};
+    dispatch_transfer(pf_, pc_, [&](auto NFc, auto NCc) {
+      constexpr int NF = decltype(NFc)::value, NC = decltype(NCc)::value;
+      prolong_node_kernel<NF, NC><<<grid_for(fine_.num_nodes(), 256), 256, 0, s>>>(prm);
+    });
+    HXG_CUDA(cudaGetLastError());
+    return;
+  }
   int nf = pf_ + 1;
   size_t need = (size_t)fine_.num_elements() * 3 * nf * nf * nf;
   if (evf_.n != need) evf_.alloc(need);

@@ -507,3 +507,22 @@ def test_verify_suite_matches_reference(perturbation):
                                              else g["passed_perturbed"]).tolist()))
     got = {name: ok for name, ok, _ in run_verification(perturbation)}
     assert got == expect, {k: (got.get(k), v) for k, v in expect.items() if got.get(k) != v}
+
+
+@pytest.mark.parametrize("order,cells", [(2, (5, 3, 4)), (3, (3, 2, 2)), (4, (2, 2, 3))])
+def test_node_prolong_bitwise_equals_two_pass(order, cells):
+    """The fused node-centric prolongation is bitwise the element kernel +
+    node-ordered average pair it replaces, on every transfer of the
+    hierarchy."""
+    from paper_2204_01722_b200.hexmg import FemProblem
+    prob = FemProblem(cells=cells, order=order, fixed_faces=("-x",))
+    mg = prob.hierarchy
+    for k in range(mg.num_levels() - 1):
+        xc = torch.sin(0.37 * torch.arange(mg.level_size(k), dtype=torch.float64, device="cuda"))
+        fused = mg.prolong(k, xc).clone()
+        os.environ["HXG_PROLONG_TWO_PASS"] = "1"
+        try:
+            ref = mg.prolong(k, xc).clone()
+        finally:
+            del os.environ["HXG_PROLONG_TWO_PASS"]
+        assert torch.equal(fused, ref)
