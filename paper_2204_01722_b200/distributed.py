@@ -41,7 +41,7 @@ import math
 import numpy as np
 import torch
 
-from .partition import exchange_faces
+from .partition import Block, exchange_block, exchange_faces
 
 
 # --------------------------------------------------------------------------
@@ -95,14 +95,66 @@ class SlabComm:
         return t
 
 
-def global_rough_seed_slice(global_npd, node_x0, local_npd, mask=None):
+class BlockComm(SlabComm):
+    """The same primitives for a px x py x pz block partition
+    (``partition.block_partition``): interface sums one direction after the
+    other, interface scaling per shared direction (a node on k partition
+    planes has 2^k times the local multiplicity), ownership by the lower
+    block in every direction."""
+
+    def __init__(self, block: Block, dist=None):
+        super().__init__(block.rank, block.world, dist)
+        self.block = block
+
+    def _planes(self, v, d, npd):
+        n = npd[d]
+        out = []
+        if self.block.neighbour(d, -1) is not None:
+            out.append(0)
+        if self.block.neighbour(d, +1) is not None:
+            out.append(n - 1)
+        sl = [(lambda i: v[:, :, i, :]), (lambda i: v[:, i, :, :]), (lambda i: v[i, :, :, :])][d]
+        return [sl(i) for i in out]
+
+    def exchange(self, y, npd):
+        if self.dist is not None:
+            exchange_block(y, npd, self.block, self.dist)
+        return y
+
+    def scale_interfaces(self, y, npd, factor):
+        if self.world == 1:
+            return y
+        v = y.view(npd[2], npd[1], npd[0], 3)
+        for d in range(3):
+            for pl in self._planes(v, d, npd):
+                pl *= factor
+        return y
+
+    def owned(self, npd, device):
+        key = (tuple(npd), str(device))
+        if key not in self._owned:
+            m = torch.ones(npd[2], npd[1], npd[0], 3, dtype=torch.bool, device=device)
+            if self.block.neighbour(0, -1) is not None:
+                m[:, :, 0, :] = False
+            if self.block.neighbour(1, -1) is not None:
+                m[:, 0, :, :] = False
+            if self.block.neighbour(2, -1) is not None:
+                m[0, :, :, :] = False
+            self._owned[key] = m.reshape(-1)
+        return self._owned[key]
+
+
+def global_rough_seed_slice(global_npd, node0, local_npd, mask=None):
     """rough_seed (cg.hpp:138-147, mt19937(0x9e3779b9)) of the GLOBAL vector,
-    restricted to this slab's nodes; constrained entries zeroed."""
+    restricted to this block's nodes (node0: first global node per direction,
+    or the x offset alone for a slab); constrained entries zeroed."""
     n = 3 * global_npd[0] * global_npd[1] * global_npd[2]
     raw = np.random.RandomState(0x9E3779B9).randint(0, 2**32, size=n, dtype=np.uint64)
     v = 2.0 * (raw.astype(np.float64) * (1.0 / 4294967296.0)) - 1.0
     v = v.reshape(global_npd[2], global_npd[1], global_npd[0], 3)
-    v = np.ascontiguousarray(v[:, :, node_x0:node_x0 + local_npd[0], :]).ravel()
+    x0, y0, z0 = (node0, 0, 0) if np.isscalar(node0) else node0
+    v = np.ascontiguousarray(v[z0:z0 + local_npd[2], y0:y0 + local_npd[1],
+                               x0:x0 + local_npd[0], :]).ravel()
     if mask is not None:
         v[np.asarray(mask, bool)] = 0.0
     return v
@@ -166,13 +218,15 @@ def q1_lattice_pattern(npd, mask):
 class DistributedHierarchy:
     """MultigridHierarchy (multigrid.hpp:88-194) over slab-partitioned
     levels; ``global_cells`` is the whole box, ``x0`` this slab's first
-    element along x, ``global_mask_fn(order)`` the global constraint mask of
-    a level (for the coarse pattern)."""
+    element along x (or a block's first element per direction, a 3-tuple),
+    ``global_mask_fn(order)`` the global constraint mask of a level (for the
+    coarse pattern)."""
 
     def __init__(self, backend, comm: SlabComm, global_cells, x0, global_mask_fn, degree=2,
                  pre_smooth=1, post_smooth=1):
         self.b, self.comm = backend, comm
         self.global_cells, self.x0 = tuple(global_cells), x0
+        self.e0 = (x0, 0, 0) if np.isscalar(x0) else tuple(x0)
         self.global_mask_fn = global_mask_fn
         self.degree, self.pre, self.post = degree, pre_smooth, post_smooth
         self.L = len(backend.levels)
@@ -207,7 +261,7 @@ class DistributedHierarchy:
     def _estimate_lambda_max(self, k, iterations=10):
         """estimate_lambda_max (cg.hpp:152-184) on the distributed D^-1 A."""
         p = self.b.levels[k]
-        seed = global_rough_seed_slice(self.global_npd(k), p * self.x0, self.npd(k),
+        seed = global_rough_seed_slice(self.global_npd(k), tuple(p * e for e in self.e0), self.npd(k),
                                        self.b.mask(k).cpu().numpy())
         r = torch.as_tensor(seed, dtype=torch.float64, device=self.b.device)
         inv = self.inv_diag[k]
@@ -251,7 +305,8 @@ class DistributedHierarchy:
         def to_global(d):
             node, c = d // 3, d % 3
             ix, iy, iz = node % lnpd[0], (node // lnpd[0]) % lnpd[1], node // (lnpd[0] * lnpd[1])
-            return 3 * ((ix + self.x0) + gnpd[0] * (iy + gnpd[1] * iz)) + c
+            ex, ey, ez = self.e0  # p = 1: node offset = element offset
+            return 3 * ((ix + ex) + gnpd[0] * ((iy + ey) + gnpd[1] * (iz + ez))) + c
 
         rg, cg = to_global(lrows), to_global(np.asarray(lcols, np.int64))
         lkeys = rg * n + cg

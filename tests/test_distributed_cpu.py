@@ -244,3 +244,69 @@ def test_distributed_newton_matches_reference(case, traction, steps):
         assert fnorm < 1e-9
         ur = _slice(G[f"{case}_u"], npd_g, x0, nx)
         assert np.linalg.norm(u - ur) < 1e-9 * np.linalg.norm(ur)
+
+
+def _block_worker(rank, world, port, cells, order, dims, out):
+    from paper_2204_01722_b200.distributed import BlockComm
+    from paper_2204_01722_b200.partition import block_partition
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.set_default_dtype(torch.float64)
+        blk = block_partition(cells, dims, rank, order)
+        h = [EXT[d] / cells[d] for d in range(3)]
+        ext = tuple(h[d] * blk.cells[d] for d in range(3))
+        fixed = (0,) if blk.coords[0] == 0 else ()
+        tface = 1 if blk.coords[0] == dims[0] - 1 else -1
+        P = H.make_problem(ext, blk.cells, order, fixed_faces=fixed, traction_face=tface,
+                           traction=TRACTION)
+        comm = BlockComm(blk, dist)
+        f = torch.from_numpy(P.op.apply_residual(np.zeros(P.op.size)))
+        comm.exchange(f, blk.npd)
+        be = OracleSlabBackend(P, fixed)
+
+        def gmask(p):
+            return H.build_constraints(H.build_box_mesh(EXT, cells, p), (0,))
+
+        hier = DistributedHierarchy(be, comm, cells, blk.e0, gmask)
+        hier.setup_numeric()
+        rep = distributed_pcg(hier, -f, rtol=1e-8)
+        out[rank] = (rep["iterations"], rep["x"].numpy(), hier.lambda_max[1:], blk.node0, blk.npd)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dims", [(2, 2, 1), (1, 2, 2)])
+def test_block_partitioned_pmg_matches_single_process(dims):
+    """px x py x pz block partition (SURVEY.md §8(e), 2 x 2 x 2 for cfg5):
+    interface sums through edges and corners, per-direction interface
+    scaling of the transfers, ownership by the lower block; same lambda_max,
+    PCG iterations and solution as the single-process reference."""
+    cells, order = (6, 4, 4), 2
+    world = dims[0] * dims[1] * dims[2]
+    Pg, xg, its_g, lams_g = _global_reference(cells, order)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_block_worker, args=(world, _free_port(), cells, order, dims, out), nprocs=world,
+             join=True)
+    g = xg.reshape(Pg.mesh.npd[2], Pg.mesh.npd[1], Pg.mesh.npd[0], 3)
+    for r in range(world):
+        its, x, lams, n0, npd = out[r]
+        assert abs(its - its_g) <= 1, (its, its_g)
+        for a, b in zip(lams, lams_g):
+            assert abs(a - b) < 1e-10 * abs(b), (lams, lams_g)
+        xr = np.ascontiguousarray(g[n0[2]:n0[2] + npd[2], n0[1]:n0[1] + npd[1],
+                                    n0[0]:n0[0] + npd[0]]).ravel()
+        assert np.linalg.norm(x - xr) < 1e-6 * np.linalg.norm(xr)
+
+
+def test_block_partition_shapes():
+    from paper_2204_01722_b200.partition import block_partition
+    bs = [block_partition((160, 160, 160), (2, 2, 2), r, 2) for r in range(8)]
+    assert all(b.cells == (80, 80, 80) for b in bs)
+    assert sorted(b.e0 for b in bs) == sorted((x, y, z) for x in (0, 80) for y in (0, 80)
+                                              for z in (0, 80))
+    b = block_partition((7, 5, 3), (3, 2, 1), 4, 1)
+    assert b.coords == (1, 1, 0) and b.cells == (2, 2, 3) and b.e0 == (3, 3, 0)
+    assert b.neighbour(0, -1) == 3 and b.neighbour(0, 1) == 5 and b.neighbour(1, 1) is None
