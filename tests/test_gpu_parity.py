@@ -526,3 +526,52 @@ def test_node_prolong_bitwise_equals_two_pass(order, cells):
         finally:
             del os.environ["HXG_PROLONG_TWO_PASS"]
         assert torch.equal(fused, ref)
+
+
+def _edge_case_problem(order, cells, maskkind):
+    """Device operator + numpy oracle on the same box, mask and state."""
+    from paper_2204_01722_b200.hexmg import MatrixFreeOperator, build_lagrange_basis, \
+        geometric_factors, lame_from_young_poisson
+    ext = (1.3, 0.8, 1.1)
+    P = H.make_problem(ext, cells, order, fixed_faces=(0,))
+    n = P.op.size
+    if maskkind == "faces":  # several whole faces (analytic face-bit path)
+        mask = H.build_constraints(P.mesh, (0, 3, 4)).astype(np.uint8)
+    elif maskkind == "general":  # one component of a face + scattered DoFs (mask-array path)
+        mask = np.zeros(n, np.uint8)
+        m0 = H.build_constraints(P.mesh, (0,))
+        mask[(m0 != 0) & (np.arange(n) % 3 == 2)] = 1
+        mask[np.random.RandomState(3).choice(n, max(1, n // 17), replace=False)] = 1
+    else:
+        mask = None
+    P.op.mask = mask
+    basis = build_lagrange_basis(order)
+    dx, w = geometric_factors(ext, cells, order, order + 1)
+    mu, lam = lame_from_young_poisson(1.0, 0.3)
+    op = MatrixFreeOperator(cells, basis, dx, w, mu, lam, mask)
+    X = P.mesh.coords if hasattr(P.mesh, "coords") else None
+    s = np.arange(n)
+    u = 0.02 * np.sin(0.01 * s) * np.cos(0.003 * s)
+    if mask is not None:
+        u[mask != 0] = 0.0
+    return P, op, u, X
+
+
+@pytest.mark.parametrize("order,cells", [(1, (1, 1, 1)), (2, (1, 1, 1)), (3, (1, 1, 1)), (4, (1, 1, 1)),
+                                         (2, (5, 3, 7)), (3, (3, 5, 3)), (4, (3, 1, 2)), (1, (9, 2, 5))])
+@pytest.mark.parametrize("maskkind", ["none", "faces", "general"])
+def test_edge_cases_against_oracle(order, cells, maskkind):
+    """Single-element meshes, ragged bricks (cells not multiples of the brick),
+    no constraints, several whole faces (analytic mask) and a general mask
+    (one component + scattered DoFs): residual, Jacobian apply (fused and
+    two-pass) and diagonal against the numpy oracle to 1e-12."""
+    P, op, u, _ = _edge_case_problem(order, cells, maskkind)
+    f = op.apply_residual(cuda(u))
+    assert rel(f, P.op.apply_residual(u)) < 1e-12
+    x = np.cos(0.37 * np.arange(P.op.size))
+    jref = P.op.apply_jacobian(x)
+    for variant in (0, 1):
+        op.set_variant(variant)
+        assert rel(op.apply_jacobian(cuda(x)), jref) < 1e-12
+    op.set_variant(0)
+    assert rel(op.extract_diagonal(), P.op.extract_diagonal()) < 1e-12
