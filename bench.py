@@ -366,8 +366,8 @@ def run_ours(args, rank, world, local_rank):
 
     # JacobianStorage variants (paper Table III, material.hpp:66-78) on the
     # headline Q2 64^3 problem: bytes per DoF from each variant's state and
-    # the measured apply (Current: fused brick kernel; initial variants: the
-    # two-pass element path).  Rank 0, N = 1 only.
+    # the measured apply (fused brick kernel for every storage).  Rank 0,
+    # N = 1 only.
     storage_table = None
     if world == 1 and not args.no_newton:
         storage_table = []
@@ -392,7 +392,7 @@ def run_ours(args, rank, world, local_rank):
             storage_table.append({"storage": sname, "bytes_per_dof": bpd, "ms_per_apply": mss,
                                   "GDoF_s": ns / (mss * 1e-3) / 1e9,
                                   "roofline_frac": bpd * ns / (mss * 1e-3) / 1e9 / peak_gbs(),
-                                  "path": "fused" if sname == "current" else "two-pass"})
+                                  "path": "fused brick kernel"})
             del ps, xs, ys
             torch.cuda.empty_cache()
 

@@ -130,6 +130,12 @@ __host__ __device__ constexpr int pad_plane(int p, int q) {
 __host__ __device__ constexpr int fused_min_blocks(int p, int q) {
   return p * 10 + q == 34 ? HXG_MINB_HIGHP : p * 10 + q == 23 ? HXG_MINB_Q2 : p * 10 + q == 45 ? HXG_MINB_Q4 : 2;
 }
+// Initial-storage variants (measured, Q2 64^3): Native and AD run 2 CTAs/SM
+// in 113 registers (0.525 / 0.667 ms vs 0.547 / 0.770 at 1 CTA); Tuned keeps
+// 1 CTA/SM (0.510 vs 0.695 ms).
+__host__ __device__ constexpr int variant_min_blocks(int storage) {
+  return storage == kStorageInitialTuned ? 1 : 2;
+}
 // Column-private shared slots for the gradients (see P2).
 __host__ __device__ constexpr bool fused_slots(int p, int q) {
   return p * 10 + q == 12 || p * 10 + q == 13 || (HXG_SLOTS_Q2 && p * 10 + q == 23) ||
@@ -196,9 +202,15 @@ __device__ __forceinline__ double ld_once(const double* a, unsigned long long po
   return v;
 }
 
-template <int P, int Q>
-__global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
+// ST = JacobianStorage: Current streams the 16-scalar state through
+// jacobian_qf; the initial-configuration variants (material.hpp:196-239)
+// stream their 19 / 26 / 25-scalar reference layout through
+// jacobian_qf_initial (one CTA per SM: their q-functions need the registers).
+template <int P, int Q, int ST = kStorageCurrent>
+__global__ void __launch_bounds__(Dims<P, Q>::T,
+                                  ST == kStorageCurrent ? fused_min_blocks(P, Q) : variant_min_blocks(ST))
     fused_jacobian_kernel(const __grid_constant__ FusedParams prm) {
+  constexpr int SS = device_state_stride(ST);
   using D = FDims<P, Q>;
   constexpr int N = D::N, T = D::T;
   constexpr int NBX = D::NBX, NBY = D::NBY;
@@ -213,10 +225,10 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
   // brick's quadrature state is one contiguous run, pulled into L2 one brick
   // ahead so the q-function loads hit L2.
   auto prefetch_state = [&](int b) {
-    constexpr unsigned bytes = (unsigned)(sizeof(double) * Q * kStateStride * T);
+    constexpr unsigned bytes = (unsigned)(sizeof(double) * Q * SS * T);
     constexpr unsigned chunk = 32768;
     const char* base = reinterpret_cast<const char*>(
-        prm.state + (size_t)lay.brick_points() * b * kStateStride);
+        prm.state + (size_t)lay.brick_points() * b * SS);
 #pragma unroll
     for (unsigned off = 0; off < bytes; off += chunk)
       prefetch_l2(base + off, off + chunk <= bytes ? chunk : bytes - off);
@@ -309,7 +321,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
   if (tid == 0 && bi + (int)gridDim.x < prm.nbricks) prefetch_state(brick + gridDim.x);
   const int bx = bc.x, by = bc.y, bz = bc.z;
   const BrickXYZ bnext = advance(bc);
-  const double* st_brick = prm.state + (size_t)lay.brick_points() * brick * kStateStride;
+  const double* st_brick = prm.state + (size_t)lay.brick_points() * brick * SS;
   const int ecx = min(BX, box.cells[0] - bx * BX);
   const int ecy = min(BY, box.cells[1] - by * BY);
   const int ecz = min(BZ, box.cells[2] - bz * BZ);
@@ -484,10 +496,10 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
   for (int qz = 0; qz < Q; ++qz) {
     double H[9];
     if (valid) {
-      double st[kStateStride];
-      const double* sp = sp0 + qz * T * kStateStride;
+      double st[SS];
+      const double* sp = sp0 + qz * T * SS;
 #pragma unroll
-      for (int s = 0; s < kStateStride; ++s) {
+      for (int s = 0; s < SS; ++s) {
         st[s] = ld_stream(sp + s * T, pol_stream);
       }
       double G[9];
@@ -496,7 +508,10 @@ __global__ void __launch_bounds__(Dims<P, Q>::T, fused_min_blocks(P, Q))
 #pragma unroll
         for (int d = 0; d < 3; ++d)
           G[3 * c + d] = qz < NSG ? slot[gslot(c, d, qz)] : g[c][d][qz - NSG];
-      jacobian_qf(prm.mu, prm.lambda, G, st, H);
+      if constexpr (ST == kStorageCurrent)
+        jacobian_qf(prm.mu, prm.lambda, G, st, H);
+      else
+        jacobian_qf_initial<ST>(prm.mu, prm.lambda, G, st, H);
       if (prm.perturb != 0.0) {  // fault-injection hook: + eps w detJ G
         const double wdet =
             prm.geo[((size_t)lay.brick_points() * brick + (size_t)qz * T) * kGeoStride + 9 * T + tid];
@@ -813,6 +828,23 @@ extern "C" int hxg_debug_phase_cycles(unsigned long long* out, int reset) {
 }
 #endif
 
+// The fused kernel for the operator's storage: Current for every (P, Q);
+// the initial variants on the fine-level pairs Q = P + 1.
+template <int P, int Q>
+void (*select_fused(int storage))(FusedParams) {
+  if constexpr (Q == P + 1) {
+    switch (storage) {
+      case kStorageInitialNative: return fused_jacobian_kernel<P, Q, kStorageInitialNative>;
+      case kStorageInitialTuned: return fused_jacobian_kernel<P, Q, kStorageInitialTuned>;
+      case kStorageInitialAD: return fused_jacobian_kernel<P, Q, kStorageInitialAD>;
+      default: break;
+    }
+  }
+  if (storage != kStorageCurrent)
+    throw Error(HXG_ERR_UNSUPPORTED, "fused initial-storage kernels cover q = p + 1");
+  return fused_jacobian_kernel<P, Q, kStorageCurrent>;
+}
+
 bool fused_supported(int p, int q) {
   bool ok = false;
   try {
@@ -850,7 +882,7 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
     if (op.partial_.n != need) op.partial_.alloc(need);
     prm.partial = op.partial_.p;
     size_t smem = sizeof(double) * D::SMEM;
-    auto k = fused_jacobian_kernel<P, Q>;
+    auto k = select_fused<P, Q>(op.storage_);
     HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));
@@ -901,7 +933,7 @@ void fused_jacobian_host(Operator& op, const double* xh, double* yh) {
     if (op.partial_.n != need) op.partial_.alloc(need);
     prm.partial = op.partial_.p;
     size_t smem = sizeof(double) * D::SMEM;
-    auto k = fused_jacobian_kernel<P, Q>;
+    auto k = select_fused<P, Q>(op.storage_);
     HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));

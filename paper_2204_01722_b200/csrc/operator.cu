@@ -281,7 +281,7 @@ void Operator::apply_jacobian_host(const double* xh, double* yh) {
 }
 
 bool Operator::fused() const {
-  return variant_ == 0 && storage_ == kStorageCurrent && fused_supported(p_, q_);
+  return variant_ == 0 && fused_supported(p_, q_) && (storage_ == kStorageCurrent || q_ == p_ + 1);
 }
 
 int Operator::kernel_launches() const { return fused() ? fused_launches(p_, q_) : 2; }
