@@ -575,3 +575,29 @@ def test_edge_cases_against_oracle(order, cells, maskkind):
         assert rel(op.apply_jacobian(cuda(x)), jref) < 1e-12
     op.set_variant(0)
     assert rel(op.extract_diagonal(), P.op.extract_diagonal()) < 1e-12
+
+
+@pytest.mark.parametrize("order", [1, 2, 3, 4])
+def test_known_answers_linear_and_constant_fields(order):
+    """Operator-level counterparts of the reference's sum-factorisation
+    known-answer tests (proj/tests/test_basis.cpp: constant-field gradient
+    zero, linear-field gradient exact): for u = A X the strain energy is
+    volume * psi(I + A) exactly (material.hpp:38-48), and a rigid
+    translation has zero residual and is in the Jacobian's kernel."""
+    from paper_2204_01722_b200.hexmg import FemProblem, build_lagrange_basis
+    from paper_2204_01722_b200.vtk import box_coords
+    ext, cells = (1.3, 0.8, 1.1), (3, 2, 2)
+    prob = FemProblem(extents=ext, cells=cells, order=order, fixed_faces=())
+    X = box_coords(ext, cells, order, build_lagrange_basis(order).nodes)
+    A = np.array([[0.02, -0.01, 0.005], [0.015, -0.03, 0.0], [0.0, 0.01, 0.025]])
+    u = (X @ A.T).ravel()
+    F = np.eye(3) + A
+    J = np.linalg.det(F)
+    psi = 0.5 * prob.lam * np.log(J) ** 2 - prob.mu * np.log(J) + 0.5 * prob.mu * (np.sum(F * F) - 3)
+    vol = ext[0] * ext[1] * ext[2]
+    e = prob.op.total_strain_energy(cuda(u))
+    assert abs(e - vol * psi) < 1e-12 * abs(vol * psi)
+    t = np.tile([0.3, -0.2, 0.1], X.shape[0])
+    f = prob.op.apply_residual(cuda(t))
+    assert f.abs().max().item() < 1e-13
+    assert prob.op.apply_jacobian(cuda(t)).abs().max().item() < 1e-13
