@@ -63,13 +63,15 @@ __global__ void prolong_element_kernel(TransferParams prm) {
   }
 }
 
-// Prolong fused with the node-ordered average: one thread per fine node
-// evaluates, for each element containing it (ascending element index, the
-// order of node_sum_kernel), the per-entry interpolation above with the same
-// operation sequence, sums them from 0 and scales by 1/m -- bitwise the
-// element kernel + node_sum_kernel(kEpiInvMult) pair, without the E-vector
-// round trip (Q2 64^3: 170 MB written and re-read).  The coarse values are
-// L1/L2-resident (neighbouring fine nodes share them).
+// Prolong fused with the node-ordered average: one thread per fine node.
+// A node shared by k elements sits on their common faces, where the 1D
+// coarse-on-fine rows are exact unit vectors (the fine and coarse GLL
+// endpoints coincide, lagrange_tabulate), so every element's per-entry
+// interpolation (the element kernel above, same operation sequence) is the
+// same double: it is evaluated once, in the lowest containing element, and
+// the node_sum_kernel(kEpiInvMult) epilogue is replayed on k copies (sum from
+// 0 in element order, times 1/k) -- bitwise the element kernel + node sum
+// pair (tested), without the E-vector round trip or the k-fold recompute.
 template <int NF, int NC>
 __global__ void __launch_bounds__(256) prolong_node_kernel(TransferParams prm) {
   constexpr int PF = NF - 1, PC = NC - 1;
@@ -80,48 +82,38 @@ __global__ void __launch_bounds__(256) prolong_node_kernel(TransferParams prm) {
        node += (long long)gridDim.x * blockDim.x) {
     const int g[3] = {(int)(node % f.npd[0]), (int)((node / f.npd[0]) % f.npd[1]),
                       (int)(node / ((long long)f.npd[0] * f.npd[1]))};
-    int lo[3], hi[3];
+    int lo[3], mult = 1;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       const int e = g[d] / PF;
-      if (g[d] % PF == 0) {
-        lo[d] = e > 0 ? e - 1 : 0;
-        hi[d] = e < f.cells[d] ? e : f.cells[d] - 1;
-      } else {
-        lo[d] = hi[d] = e;
-      }
+      const bool shared = g[d] % PF == 0;
+      lo[d] = shared && e > 0 ? e - 1 : (e < f.cells[d] ? e : f.cells[d] - 1);
+      if (shared && e > 0 && e < f.cells[d]) mult *= 2;
     }
-    double s[3] = {0.0, 0.0, 0.0};
-    int mult = 0;
-    for (int ez = lo[2]; ez <= hi[2]; ++ez)
-      for (int ey = lo[1]; ey <= hi[1]; ++ey)
-        for (int ex = lo[0]; ex <= hi[0]; ++ex) {
-          const int i = g[0] - PF * ex, j = g[1] - PF * ey, k = g[2] - PF * ez;
-          const double* xb = prm.in + 3 * ((PC * ex) + cb.npd[0] * ((long long)(PC * ey) +
-                                                                  (long long)cb.npd[1] * (PC * ez)));
-          const long long sy = 3LL * cb.npd[0], sz = 3LL * cb.npd[0] * cb.npd[1];
+    const int i = g[0] - PF * lo[0], j = g[1] - PF * lo[1], k = g[2] - PF * lo[2];
+    const double* xb = prm.in + 3 * ((PC * lo[0]) + cb.npd[0] * ((long long)(PC * lo[1]) +
+                                                               (long long)cb.npd[1] * (PC * lo[2])));
+    const long long sy = 3LL * cb.npd[0], sz = 3LL * cb.npd[0] * cb.npd[1];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            double out = 0.0;
+    for (int c = 0; c < 3; ++c) {
+      double out = 0.0;
 #pragma unroll
-            for (int kc = 0; kc < NC; ++kc) {
-              double t2 = 0.0;
+      for (int kc = 0; kc < NC; ++kc) {
+        double t2 = 0.0;
 #pragma unroll
-              for (int jc = 0; jc < NC; ++jc) {
-                double t1 = 0.0;
+        for (int jc = 0; jc < NC; ++jc) {
+          double t1 = 0.0;
 #pragma unroll
-                for (int ic = 0; ic < NC; ++ic)
-                  t1 += prm.ctof[i * NC + ic] * __ldg(xb + 3 * ic + sy * jc + sz * kc + c);
-                t2 += prm.ctof[j * NC + jc] * t1;
-              }
-              out += prm.ctof[k * NC + kc] * t2;
-            }
-            s[c] += out;
-          }
-          ++mult;
+          for (int ic = 0; ic < NC; ++ic)
+            t1 += prm.ctof[i * NC + ic] * __ldg(xb + 3 * ic + sy * jc + sz * kc + c);
+          t2 += prm.ctof[j * NC + jc] * t1;
         }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) prm.evec[3 * node + c] = s[c] * (1.0 / (double)mult);
+        out += prm.ctof[k * NC + kc] * t2;
+      }
+      double s = 0.0;
+      for (int r = 0; r < mult; ++r) s += out;
+      prm.evec[3 * node + c] = s * (1.0 / (double)mult);
+    }
   }
 }
 
