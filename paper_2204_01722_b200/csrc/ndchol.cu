@@ -275,7 +275,12 @@ void cublas_check(cublasStatus_t s, const char* what) {
 }  // namespace
 
 NdCholesky::NdCholesky() = default;
-NdCholesky::~NdCholesky() = default;
+NdCholesky::~NdCholesky() {
+  if (graph_) cudaGraphExecDestroy(graph_);
+  if (gev_in_) cudaEventDestroy(gev_in_);
+  if (gev_out_) cudaEventDestroy(gev_out_);
+  if (gstream_) cudaStreamDestroy(gstream_);
+}
 
 void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
   n_ = a.n;
@@ -782,6 +787,10 @@ void NdCholesky::factor_front(int t, Lane& L, const CsrMatrix& a,
 }
 
 void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s) {
+  if (graph_) {  // the captured solve holds the previous buffers' launch parameters
+    cudaGraphExecDestroy(graph_);
+    graph_ = nullptr;
+  }
   if (!analyzed_) {
     static const bool prof0 = std::getenv("HXG_PROFILE") != nullptr;
     auto t0 = std::chrono::steady_clock::now();
@@ -862,6 +871,36 @@ void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s)
 
 void NdCholesky::solve(const double* b, double* x, cudaStream_t s) {
   if (!ready_) throw Error(HXG_ERR_GENERIC, "coarse solver not factorized");
+  static const bool direct = std::getenv("HXG_NO_GRAPH") != nullptr;
+  if (direct) {
+    solve_launch(b, x, s);
+    return;
+  }
+  if (!gstream_) {
+    HXG_CUDA(cudaStreamCreateWithFlags(&gstream_, cudaStreamNonBlocking));
+    HXG_CUDA(cudaEventCreateWithFlags(&gev_in_, cudaEventDisableTiming));
+    HXG_CUDA(cudaEventCreateWithFlags(&gev_out_, cudaEventDisableTiming));
+  }
+  if (!graph_ || graph_b_ != b || graph_x_ != x) {
+    if (graph_) cudaGraphExecDestroy(graph_);
+    graph_ = nullptr;
+    cudaGraph_t g = nullptr;
+    HXG_CUDA(cudaStreamBeginCapture(gstream_, cudaStreamCaptureModeThreadLocal));
+    solve_launch(b, x, gstream_);
+    HXG_CUDA(cudaStreamEndCapture(gstream_, &g));
+    HXG_CUDA(cudaGraphInstantiate(&graph_, g, 0));
+    cudaGraphDestroy(g);
+    graph_b_ = b;
+    graph_x_ = x;
+  }
+  HXG_CUDA(cudaEventRecord(gev_in_, s));
+  HXG_CUDA(cudaStreamWaitEvent(gstream_, gev_in_, 0));
+  HXG_CUDA(cudaGraphLaunch(graph_, gstream_));
+  HXG_CUDA(cudaEventRecord(gev_out_, gstream_));
+  HXG_CUDA(cudaStreamWaitEvent(s, gev_out_, 0));
+}
+
+void NdCholesky::solve_launch(const double* b, double* x, cudaStream_t s) {
   NdSolve a;
   a.piv0 = dfront_piv0_.p;
   a.np = dfront_np_.p;
