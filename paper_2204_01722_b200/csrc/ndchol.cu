@@ -872,26 +872,33 @@ void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s)
 void NdCholesky::solve(const double* b, double* x, cudaStream_t s) {
   if (!ready_) throw Error(HXG_ERR_GENERIC, "coarse solver not factorized");
   static const bool direct = std::getenv("HXG_NO_GRAPH") != nullptr;
+  // The permutations touch the caller's vectors and run on the caller's
+  // stream; the per-level core (internal buffers only) is the graph, so it
+  // does not depend on b / x and is captured once per factorization.
+  permute_gather<<<grid_for(n_, 256), 256, 0, s>>>(b, perm_.p, n_, wvec_.p);
+  HXG_CUDA(cudaGetLastError());
   if (direct) {
-    solve_launch(b, x, s);
-    return;
+    solve_launch(s);
+  } else {
+    run_graph(s);
   }
+  permute_scatter<<<grid_for(n_, 256), 256, 0, s>>>(wvec_.p, perm_.p, n_, x);
+  HXG_CUDA(cudaGetLastError());
+}
+
+void NdCholesky::run_graph(cudaStream_t s) {
   if (!gstream_) {
     HXG_CUDA(cudaStreamCreateWithFlags(&gstream_, cudaStreamNonBlocking));
     HXG_CUDA(cudaEventCreateWithFlags(&gev_in_, cudaEventDisableTiming));
     HXG_CUDA(cudaEventCreateWithFlags(&gev_out_, cudaEventDisableTiming));
   }
-  if (!graph_ || graph_b_ != b || graph_x_ != x) {
-    if (graph_) cudaGraphExecDestroy(graph_);
-    graph_ = nullptr;
+  if (!graph_) {
     cudaGraph_t g = nullptr;
     HXG_CUDA(cudaStreamBeginCapture(gstream_, cudaStreamCaptureModeThreadLocal));
-    solve_launch(b, x, gstream_);
+    solve_launch(gstream_);
     HXG_CUDA(cudaStreamEndCapture(gstream_, &g));
     HXG_CUDA(cudaGraphInstantiate(&graph_, g, 0));
     cudaGraphDestroy(g);
-    graph_b_ = b;
-    graph_x_ = x;
   }
   HXG_CUDA(cudaEventRecord(gev_in_, s));
   HXG_CUDA(cudaStreamWaitEvent(gstream_, gev_in_, 0));
@@ -900,7 +907,7 @@ void NdCholesky::solve(const double* b, double* x, cudaStream_t s) {
   HXG_CUDA(cudaStreamWaitEvent(s, gev_out_, 0));
 }
 
-void NdCholesky::solve_launch(const double* b, double* x, cudaStream_t s) {
+void NdCholesky::solve_launch(cudaStream_t s) {
   NdSolve a;
   a.piv0 = dfront_piv0_.p;
   a.np = dfront_np_.p;
@@ -933,7 +940,6 @@ void NdCholesky::solve_launch(const double* b, double* x, cudaStream_t s) {
   a.part_f = part_f_.p;
   a.part_b = part_b_.p;
   auto n_of = [](const std::vector<int>& lev, size_t l) { return lev[l + 1] - lev[l]; };
-  permute_gather<<<grid_for(n_, 256), 256, 0, s>>>(b, perm_.p, n_, wvec_.p);
   // Forward, deepest level first: y = [y1; y2] assembled; z1 = W y1;
   // u = y2 - L21 z1 passed up.
   for (int l = (int)levels_.size() - 1; l >= 0; --l) {
@@ -958,7 +964,6 @@ void NdCholesky::solve_launch(const double* b, double* x, cudaStream_t s) {
         nd_bwd_finish<<<n_of(lev_ct_, l), kBC, 0, s>>>(a, part, lev_ct_[l]);
     }
   }
-  permute_scatter<<<grid_for(n_, 256), 256, 0, s>>>(wvec_.p, perm_.p, n_, x);
   HXG_CUDA(cudaGetLastError());
 }
 

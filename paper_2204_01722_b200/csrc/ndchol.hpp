@@ -31,20 +31,19 @@ class NdCholesky {
   // 3 DoFs per node.  Throws NOT_SPD if a pivot block is not SPD.
   void factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s);
   // The ~120 dependent per-level launches of a solve are replayed from a
-  // CUDA graph (captured on an internal stream, re-captured when b / x /
-  // the factorization change); HXG_NO_GRAPH=1 launches them directly.
+  // CUDA graph (captured on an internal stream once per factorization);
+  // HXG_NO_GRAPH=1 launches them directly.
   void solve(const double* b, double* x, cudaStream_t s);
   bool ready() const { return ready_; }
   double factor_bytes() const { return (double)lsize_ * sizeof(double); }
   int num_levels() const { return (int)levels_.size(); }
 
  private:
-  void solve_launch(const double* b, double* x, cudaStream_t s);
+  void solve_launch(cudaStream_t s);  // per-level core on wvec_
+  void run_graph(cudaStream_t s);
   cudaStream_t gstream_ = nullptr;
   cudaEvent_t gev_in_ = nullptr, gev_out_ = nullptr;
   cudaGraphExec_t graph_ = nullptr;
-  const double* graph_b_ = nullptr;
-  double* graph_x_ = nullptr;
   struct Front {
     int parent = -1;
     int child[2] = {-1, -1};
