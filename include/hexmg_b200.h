@@ -204,7 +204,8 @@ int hxg_chol_destroy(hxg_chol_t h);
  * slot values summed over elements in increasing element order.  create =
  * symbolic; numeric needs the operator's state (StateNotInitialized
  * otherwise); matvec on device vectors.  The "assembled" rows of the
- * performance study (study.hpp:191-232). */
+ * performance study (study.hpp:191-232).  The operator must outlive the
+ * handle (it is re-read by numeric). */
 int hxg_asm_create(hxg_op_t op, hxg_asm_t* out);
 int hxg_asm_numeric(hxg_asm_t a);
 int hxg_asm_nnz(hxg_asm_t a, int64_t* nnz);
