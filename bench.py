@@ -103,9 +103,11 @@ class ClockSampler:
 # CPU baseline / reference arm: the unmodified reference compiled into
 # oracle/_ref (kind "reference"), else the numpy port (kind "port").
 # --------------------------------------------------------------------------
-def cpu_reference_time(order, cells, applies, threads, warmup=1):
+def cpu_reference_time(order, cells, applies, threads, warmup=1, one_thread_applies=0):
     """Seconds for `applies` Jacobian applies after `warmup`, reference perf
-    harness method (study.hpp:196-212)."""
+    harness method (study.hpp:196-212); with one_thread_applies > 0 the
+    same operator is also timed on one thread (report
+    1-thread and all-core), returned as a 5th value."""
     import numpy as np
     from oracle import ref_lib as R
     if R.available():
@@ -116,6 +118,10 @@ def cpu_reference_time(order, cells, applies, threads, warmup=1):
         rp.apply_residual(u)
         x = 1e-3 * np.sin(0.7 * np.arange(rp.n))
         sec = rp.time_jacobian(x, warmup=warmup, repeats=applies)
+        if one_thread_applies > 0:
+            rp.set_threads(1)
+            sec1 = rp.time_jacobian(x, warmup=0, repeats=one_thread_applies)
+            return rp.n, sec, "reference", threads, sec1
         return rp.n, sec, "reference", threads
     from oracle import hexmg_np as H
     P = H.make_problem((1.0, 1.0, 1.0), (cells,) * 3, order)
@@ -530,11 +536,15 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         try:
-            ndof_c, sec, kind, cores = cpu_reference_time(ORDER, CELLS, args.cpu_applies, threads)
+            res = cpu_reference_time(ORDER, CELLS, args.cpu_applies, threads, one_thread_applies=2)
+            ndof_c, sec, kind, cores = res[:4]
             cpu = {"value": ndof_c * args.cpu_applies / sec / 1e9, "unit": UNIT, "cores": cores,
                    "kind": kind,
                    "sample": f"{args.cpu_applies} Jacobian applies of the same {CELLS}^3 "
                              f"Q{ORDER} problem after 1 warm-up, {cores} threads"}
+            if len(res) > 4:
+                cpu["one_thread"] = {"value": ndof_c * 2 / res[4] / 1e9, "unit": UNIT,
+                                     "sample": "2 applies of the same operator on 1 thread"}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
                    "sample": f"failed: {exc}"}
