@@ -93,7 +93,7 @@ __device__ __forceinline__ void load_tables(const double* tab, double* sTab) {
 // ST = JacobianStorage: the state stride and the q-function pair.
 template <int P, int Q, int MODE, int ST = kStorageCurrent>
 __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams prm) {
-  constexpr int S = device_state_stride(ST);
+  constexpr int S = device_state_stride(ST), SP = state_row(S, Q);
   using D = Dims<P, Q>;
   constexpr int N = D::N, N3 = D::N3;
   extern __shared__ double smem[];
@@ -121,9 +121,9 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams
 #pragma unroll
     for (int qz = 0; qz < Q; ++qz) {
       double st[S];
-      const double* sp = prm.state + (base + (long long)qz * T) * S + threadIdx.x;
+      const double* sp = prm.state + (base + (long long)qz * T) * SP + state_lane(threadIdx.x, Q);
 #pragma unroll
-      for (int s = 0; s < S; ++s) st[s] = __ldg(sp + s * T);
+      for (int s = 0; s < S; ++s) st[s] = __ldg(sp + state_pair_off(s, (int)T, Q));
       double G[9], H[9];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams
         J = residual_qf(prm.mu, prm.lambda, G, geo, geo[9], H, st);
       else
         J = residual_qf_initial<ST>(prm.mu, prm.lambda, G, geo, geo[9], H, st);
-      double* so = prm.state_out + (base + (long long)qz * T) * S + threadIdx.x;
+      double* so = prm.state_out + (base + (long long)qz * T) * SP + state_lane(threadIdx.x, Q);
       if (!(J > 0.0)) {
         if (tp.e >= 0) {
           unsigned long long idx =
@@ -175,10 +175,10 @@ __global__ void __launch_bounds__(Dims<P, Q>::T) element_apply_kernel(ElemParams
           double sp[kStateStride];
           pack_state(prm.mu, st, sp);
 #pragma unroll
-          for (int s = 0; s < kStateStride; ++s) so[s * T] = sp[s];
+          for (int s = 0; s < kStateStride; ++s) so[state_pair_off(s, (int)T, Q)] = sp[s];
         } else {
 #pragma unroll
-          for (int s = 0; s < S; ++s) so[s * T] = st[s];
+          for (int s = 0; s < S; ++s) so[state_pair_off(s, (int)T, Q)] = st[s];
         }
       }
 #pragma unroll

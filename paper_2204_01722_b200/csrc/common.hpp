@@ -57,6 +57,24 @@ __host__ __device__ constexpr int device_state_stride(int storage) {
   return storage == kStorageCurrent ? kStateStride : ref_state_stride(storage);
 }
 constexpr int kMaxStateStride = 26;
+// In HBM the scalars of a point are paired (q <= 4): row r = brick Q + qz
+// holds ceil(S/2) pair-planes of T points x 2 doubles, so scalar s of point
+// t sits at r SP T + (s/2) 2T + 2t + s%2 (SP = S rounded up to even) and a
+// thread streams its point's state with 16-byte loads (Q2 apply 332.7 ->
+// 318.0 us).  q = 5 (the Q4 hierarchy) keeps one plane per scalar,
+// r S T + s T + t (paired it measured 3.5 % slower there).
+__host__ __device__ constexpr bool state_paired(int q) { return q != 5; }
+__host__ __device__ constexpr int state_pad(int S) { return (S + 1) & ~1; }
+__host__ __device__ constexpr int state_row(int S, int q) {
+  return state_paired(q) ? state_pad(S) : S;
+}
+template <class I>
+__host__ __device__ constexpr I state_lane(I t, int q) {
+  return state_paired(q) ? 2 * t : t;
+}
+__host__ __device__ inline long long state_pair_off(int s, int T, int q) {
+  return state_paired(q) ? (long long)(s >> 1) * 2 * T + (s & 1) : (long long)s * T;
+}
 // Geometry per qpt: dxi/dX (9, row-major) then w * detJ (mesh.hpp:169-189).
 constexpr int kGeoStride = 10;
 

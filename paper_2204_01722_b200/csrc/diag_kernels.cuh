@@ -36,7 +36,7 @@ __device__ __forceinline__ long long state_offset(const QLayout& lay, long long 
   int Q = lay.Q;
   int qx = qpt % Q, qy = (qpt / Q) % Q, qz = qpt / (Q * Q);
   int t = (qy * Q + qx) * (lay.B[0] * lay.B[1] * lay.B[2]) + le;
-  return ((brick * Q + qz) * S) * (long long)lay.T + t;
+  return ((brick * Q + qz) * state_row(S, Q)) * (long long)lay.T + state_lane(t, Q);
 }
 
 // D[(c1,d1),(c2,d2)] at one point: 9 probes of the Jacobian q-function.
@@ -45,7 +45,7 @@ __device__ __forceinline__ void point_tensor(const DiagParams& prm, long long e,
   const int S = device_state_stride(prm.storage);
   long long off = state_offset(prm.lay, e, qpt, S);
   double st[kMaxStateStride];
-  for (int s = 0; s < S; ++s) st[s] = prm.state[off + (long long)s * prm.lay.T];
+  for (int s = 0; s < S; ++s) st[s] = prm.state[off + state_pair_off(s, prm.lay.T, prm.lay.Q)];
   for (int u = 0; u < 9; ++u) {
     double G[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, H[9];
     G[u] = 1.0;
@@ -56,7 +56,8 @@ __device__ __forceinline__ void point_tensor(const DiagParams& prm, long long e,
       default: jacobian_qf(prm.mu, prm.lambda, G, st, H);
     }
     if (prm.perturb != 0.0) {  // + eps w detJ G (w detJ = geometry scalar 9, same point)
-      const long long T = prm.lay.T, row = off / T / S, t = off % T;
+      const long long T = prm.lay.T, row = off / T / state_row(S, prm.lay.Q);
+      const long long t = state_paired(prm.lay.Q) ? (off % (2 * T)) / 2 : off % T;
       H[u] += prm.perturb * prm.geo[(row * kGeoStride + 9) * T + t];
     }
 #pragma unroll

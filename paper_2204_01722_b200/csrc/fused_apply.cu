@@ -191,6 +191,12 @@ __device__ __forceinline__ double ld_stream(const double* a, unsigned long long 
                : "l"(a), "l"(pol));
   return v;
 }
+__device__ __forceinline__ void ld_stream2(const double* a, unsigned long long pol, double& x,
+                                           double& y) {
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+      : "=d"(x), "=d"(y)
+      : "l"(a), "l"(pol));
+}
 __device__ __forceinline__ void st_keep(double* a, double v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }
@@ -210,7 +216,8 @@ template <int P, int Q, int ST = kStorageCurrent>
 __global__ void __launch_bounds__(Dims<P, Q>::T,
                                   ST == kStorageCurrent ? fused_min_blocks(P, Q) : variant_min_blocks(ST))
     fused_jacobian_kernel(const __grid_constant__ FusedParams prm) {
-  constexpr int SS = device_state_stride(ST);
+  constexpr int SS = device_state_stride(ST), SP = state_row(SS, Q);
+  constexpr bool kStateV2 = state_paired(Q);  // 16-byte loads of the paired layout
   using D = FDims<P, Q>;
   constexpr int N = D::N, T = D::T;
   constexpr int NBX = D::NBX, NBY = D::NBY;
@@ -225,10 +232,10 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   // brick's quadrature state is one contiguous run, pulled into L2 one brick
   // ahead so the q-function loads hit L2.
   auto prefetch_state = [&](int b) {
-    constexpr unsigned bytes = (unsigned)(sizeof(double) * Q * SS * T);
+    constexpr unsigned bytes = (unsigned)(sizeof(double) * Q * SP * T);
     constexpr unsigned chunk = 32768;
     const char* base = reinterpret_cast<const char*>(
-        prm.state + (size_t)lay.brick_points() * b * SS);
+        prm.state + (size_t)lay.brick_points() * b * SP);
 #pragma unroll
     for (unsigned off = 0; off < bytes; off += chunk)
       prefetch_l2(base + off, off + chunk <= bytes ? chunk : bytes - off);
@@ -321,7 +328,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   if (tid == 0 && bi + (int)gridDim.x < prm.nbricks) prefetch_state(brick + gridDim.x);
   const int bx = bc.x, by = bc.y, bz = bc.z;
   const BrickXYZ bnext = advance(bc);
-  const double* st_brick = prm.state + (size_t)lay.brick_points() * brick * SS;
+  const double* st_brick = prm.state + (size_t)lay.brick_points() * brick * SP;
   const int ecx = min(BX, box.cells[0] - bx * BX);
   const int ecy = min(BY, box.cells[1] - by * BY);
   const int ecz = min(BZ, box.cells[2] - bz * BZ);
@@ -458,7 +465,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   volatile double* slot = S + te;
   double g[3][3][QR > 0 ? QR : 1];
   double hr[3][3][QH > 0 ? QH : 1];
-  const double* sp0 = st_brick + tid;
+  const double* sp0 = st_brick + state_lane(tid, Q);
   const unsigned long long pol_stream = policy_evict_first();
   auto gslot = [&](int c, int d, int z) { return ((c * 3 + d) * N + z) * Q2; };
 #pragma unroll
@@ -496,11 +503,14 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   for (int qz = 0; qz < Q; ++qz) {
     double H[9];
     if (valid) {
-      double st[SS];
-      const double* sp = sp0 + qz * T * SS;
+      double st[SP];
+      const double* sp = sp0 + qz * T * SP;
 #pragma unroll
-      for (int s = 0; s < SS; ++s) {
-        st[s] = ld_stream(sp + s * T, pol_stream);
+      if constexpr (kStateV2) {
+        for (int s = 0; s < SS; s += 2) ld_stream2(sp + s * T, pol_stream, st[s], st[s + 1]);
+      } else {
+#pragma unroll
+        for (int s = 0; s < SS; ++s) st[s] = ld_stream(sp + s * T, pol_stream);
       }
       double G[9];
 #pragma unroll

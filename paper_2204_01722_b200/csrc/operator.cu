@@ -134,7 +134,7 @@ Operator::Operator(int p, int q, const int cells[3], const std::vector<double>& 
   if (!state_) state_ = std::make_shared<State>();
   if (state_->storage >= 0 && state_->storage != storage_)
     throw Error(HXG_ERR_INVALID_ARGUMENT, "quadrature state shared between different JacobianStorage");
-  size_t need = (size_t)lay_.total_points() * device_state_stride(storage_);
+  size_t need = (size_t)lay_.total_points() * state_row(device_state_stride(storage_), q_);
   if (state_->data.n != need) {
     state_->data.alloc(need);
     HXG_CUDA(cudaMemset(state_->data.p, 0, need * sizeof(double)));
@@ -245,7 +245,8 @@ void Operator::apply_residual(const double* u, double* f) {
     int qz, t;
     lay_.locate(e, qp, brick, qz, t);
     double J = 0.0;
-    size_t off = (size_t)(((brick * lay_.Q + qz) * device_state_stride(storage_)) * lay_.T + t);
+    size_t off = (size_t)(((brick * lay_.Q + qz) * state_row(device_state_stride(storage_), q_)) *
+                              lay_.T + state_lane(t, q_));
     HXG_CUDA(cudaMemcpy(&J, state_->data.p + off, sizeof(double), cudaMemcpyDeviceToHost));
     Error err(HXG_ERR_INVERTED_ELEMENT, "non-positive deformation jacobian " + std::to_string(J) +
                                             " in element " + std::to_string(e) +
@@ -406,8 +407,8 @@ void Operator::export_state(double* host) const {
   // Stored [sqrt(w detJ) xi (9), tau (6), mu - lambda log J] back to the
   // reference's (e, q, 17) Current layout; w detJ from the geometry.
   if (storage_ != kStorageCurrent) {  // stored in the reference layout already
-    const int S = device_state_stride(storage_);
-    std::vector<double> blocked((size_t)lay_.total_points() * S);
+    const int S = device_state_stride(storage_), SP = state_row(S, q_);
+    std::vector<double> blocked((size_t)lay_.total_points() * SP);
     HXG_CUDA(cudaMemcpy(blocked.data(), state_->data.p, blocked.size() * sizeof(double),
                         cudaMemcpyDeviceToHost));
     const int nq = q_ * q_ * q_;
@@ -416,9 +417,9 @@ void Operator::export_state(double* host) const {
         long long brick;
         int qz, t;
         lay_.locate(e, qp, brick, qz, t);
-        const size_t base = (size_t)(brick * lay_.Q + qz) * S * lay_.T + t;
+        const size_t base = (size_t)(brick * lay_.Q + qz) * SP * lay_.T + state_lane(t, q_);
         double* out = host + ((size_t)e * nq + qp) * S;
-        for (int k = 0; k < S; ++k) out[k] = blocked[base + (size_t)k * lay_.T];
+        for (int k = 0; k < S; ++k) out[k] = blocked[base + state_pair_off(k, lay_.T, q_)];
       }
     return;
   }
@@ -435,14 +436,14 @@ void Operator::export_state(double* host) const {
       int qz, t;
       lay_.locate(e, qp, brick, qz, t);
       const size_t row = (size_t)(brick * lay_.Q + qz);
-      const size_t base = row * kStateStride * lay_.T + t;
+      const size_t base = row * kStateStride * lay_.T + state_lane(t, q_);
       const double wdet = geo[(row * kGeoStride + 9) * lay_.T + t];
       const double isw = 1.0 / std::sqrt(wdet);
       double* out = host + ((size_t)e * nq + qp) * kRefStateScalars;
       out[0] = wdet;
-      for (int k = 0; k < 9; ++k) out[1 + k] = blocked[base + (size_t)k * lay_.T] * isw;
-      for (int k = 0; k < 6; ++k) out[10 + k] = blocked[base + (size_t)(9 + k) * lay_.T];
-      out[16] = mu_ - blocked[base + (size_t)15 * lay_.T];
+      for (int k = 0; k < 9; ++k) out[1 + k] = blocked[base + state_pair_off(k, lay_.T, q_)] * isw;
+      for (int k = 0; k < 6; ++k) out[10 + k] = blocked[base + state_pair_off(9 + k, lay_.T, q_)];
+      out[16] = mu_ - blocked[base + state_pair_off(15, lay_.T, q_)];
     }
 }
 
