@@ -96,6 +96,21 @@ CoarseAssembly::CoarseAssembly(const Operator& op) {
   int n = (int)(3 * nn);
   a_.n = n;
   auto fixed = [&](long long dof) { return !mask.empty() && mask[(size_t)dof] != 0; };
+  // Unconstrained pattern size, separable over the axes: 9 prod_d sum_g
+  // (nodes coupled to g along d); refuse int32 overflow before allocating.
+  double bound = 9.0;
+  for (int d = 0; d < 3; ++d) {
+    double sum = 0.0;
+    for (int g = 0; g < box_.npd[d]; ++g) {
+      int el, eh;
+      node_elems(g, P, box_.cells[d], el, eh);
+      sum += P * (eh + 1) - P * el + 1;
+    }
+    bound *= sum;
+  }
+  // (constraints only remove entries: past twice the limit no mask brings it back)
+  if (bound > (mask.empty() ? 1.0 : 2.0) * 2147483647.0)
+    throw Error(HXG_ERR_UNSUPPORTED, "assembled operator exceeds int32 nonzeros");
   const long long per_row = 3LL * (2 * P + 1) * (2 * P + 1) * (2 * P + 1);
   a_.row_ptr_h.assign((size_t)n + 1, 0);
   a_.cols_h.clear();

@@ -176,7 +176,10 @@ def run_performance_study(base: ProblemConfig, csv, log=None):
                 except torch.cuda.OutOfMemoryError:
                     rec["status"] = "out-of-memory"
                 except RuntimeError as exc:
-                    if "out of memory" not in str(exc).lower():
+                    # device allocation failures and CSR index spaces beyond
+                    # int32 (the reference's bad_alloc range) become failed rows
+                    msg = str(exc).lower()
+                    if "out of memory" not in msg and "exceeds int32" not in msg:
                         raise
                     rec["status"] = "out-of-memory"
                 csv.write(performance_csv_row(rec) + "\n")
