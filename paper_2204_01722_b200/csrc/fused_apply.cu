@@ -51,6 +51,9 @@ namespace hxg {
 
 namespace {
 
+#ifndef HXG_PIPE_ALL_Q5
+#define HXG_PIPE_ALL_Q5 0
+#endif
 #ifndef HXG_FIXUP_ITEMS
 #define HXG_FIXUP_ITEMS 2
 #endif
@@ -499,18 +502,36 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   }
 
   // ---- q-function on the streamed state --------------------------------
+  auto load_plane = [&](int qz, double* st) {
+    const double* sp = sp0 + qz * T * SP;
+    if constexpr (kStateV2) {
+#pragma unroll
+      for (int s = 0; s < SS; s += 2) ld_stream2(sp + s * T, pol_stream, st[s], st[s + 1]);
+    } else {
+#pragma unroll
+      for (int s = 0; s < SS; ++s) st[s] = ld_stream(sp + s * T, pol_stream);
+    }
+  };
+  // Software pipeline of the state planes (plane qz + 1 loaded while plane qz
+  // is consumed): measured Q4 394.5 -> 364.4 us; slower for Q2 (+1 %) and
+  // Q3 (+8 %), whose register budgets it squeezes.
+  constexpr bool kPipe =
+      Q == 5 && ST == kStorageCurrent && (P == 4 || HXG_PIPE_ALL_Q5);
+  double stn[kPipe ? SP : 1];
+  if constexpr (kPipe) {
+    if (valid) load_plane(0, stn);
+  }
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
     double H[9];
     if (valid) {
       double st[SP];
-      const double* sp = sp0 + qz * T * SP;
+      if constexpr (kPipe) {
 #pragma unroll
-      if constexpr (kStateV2) {
-        for (int s = 0; s < SS; s += 2) ld_stream2(sp + s * T, pol_stream, st[s], st[s + 1]);
+        for (int s = 0; s < SP; ++s) st[s] = stn[s];
+        if (qz + 1 < Q) load_plane(qz + 1, stn);
       } else {
-#pragma unroll
-        for (int s = 0; s < SS; ++s) st[s] = ld_stream(sp + s * T, pol_stream);
+        load_plane(qz, st);
       }
       double G[9];
 #pragma unroll
