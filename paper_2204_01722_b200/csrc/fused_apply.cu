@@ -51,6 +51,9 @@ namespace hxg {
 
 namespace {
 
+#ifndef HXG_PIPE_Q2
+#define HXG_PIPE_Q2 0
+#endif
 #ifndef HXG_PIPE_ALL_Q5
 #define HXG_PIPE_ALL_Q5 0
 #endif
@@ -502,36 +505,42 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   }
 
   // ---- q-function on the streamed state --------------------------------
-  auto load_plane = [&](int qz, double* st) {
+  // Loads scalars [s0, s1) of plane qz (s0, s1 even on the paired layout).
+  auto load_range = [&](int qz, double* st, int s0, int s1) {
     const double* sp = sp0 + qz * T * SP;
     if constexpr (kStateV2) {
 #pragma unroll
-      for (int s = 0; s < SS; s += 2) ld_stream2(sp + s * T, pol_stream, st[s], st[s + 1]);
+      for (int s = 0; s < SS; s += 2)
+        if (s >= s0 && s < s1) ld_stream2(sp + s * T, pol_stream, st[s], st[s + 1]);
     } else {
 #pragma unroll
-      for (int s = 0; s < SS; ++s) st[s] = ld_stream(sp + s * T, pol_stream);
+      for (int s = 0; s < SS; ++s)
+        if (s >= s0 && s < s1) st[s] = ld_stream(sp + s * T, pol_stream);
     }
   };
-  // Software pipeline of the state planes (plane qz + 1 loaded while plane qz
-  // is consumed): measured Q4 394.5 -> 364.4 us; slower for Q2 (+1 %) and
-  // Q3 (+8 %), whose register budgets it squeezes.
-  constexpr bool kPipe =
-      Q == 5 && ST == kStorageCurrent && (P == 4 || HXG_PIPE_ALL_Q5);
-  double stn[kPipe ? SP : 1];
-  if constexpr (kPipe) {
-    if (valid) load_plane(0, stn);
+  // Software pipeline of the state planes: the first kPipe scalars of plane
+  // qz + 1 are loaded while plane qz is consumed.  Measured: all of them for
+  // Q4 (394.5 -> 364.4 us); Q2 / Q3 have no register room for the full plane
+  // (+1 % / +8 %).
+  constexpr int kPipe = (Q == 5 && ST == kStorageCurrent && (P == 4 || HXG_PIPE_ALL_Q5)) ? SP
+                        : (P == 2 && Q == 3 && ST == kStorageCurrent)                   ? HXG_PIPE_Q2
+                                                                                        : 0;
+  double stn[kPipe > 0 ? kPipe : 1];
+  if constexpr (kPipe > 0) {
+    if (valid) load_range(0, stn, 0, kPipe);
   }
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
     double H[9];
     if (valid) {
       double st[SP];
-      if constexpr (kPipe) {
+      if constexpr (kPipe > 0) {
 #pragma unroll
-        for (int s = 0; s < SP; ++s) st[s] = stn[s];
-        if (qz + 1 < Q) load_plane(qz + 1, stn);
+        for (int s = 0; s < kPipe; ++s) st[s] = stn[s];
+        load_range(qz, st, kPipe, SP);
+        if (qz + 1 < Q) load_range(qz + 1, stn, 0, kPipe);
       } else {
-        load_plane(qz, st);
+        load_range(qz, st, 0, SP);
       }
       double G[9];
 #pragma unroll
