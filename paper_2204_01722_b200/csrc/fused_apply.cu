@@ -57,6 +57,9 @@ namespace {
 #ifndef HXG_PIPE_ALL_Q5
 #define HXG_PIPE_ALL_Q5 0
 #endif
+#ifndef HXG_FIXUP_PDL
+#define HXG_FIXUP_PDL 1
+#endif
 #ifndef HXG_FIXUP_ITEMS
 #define HXG_FIXUP_ITEMS 2
 #endif
@@ -805,6 +808,11 @@ template <int P, int Q>
 __global__ void __launch_bounds__(128) fused_fixup_kernel(const __grid_constant__ FusedParams prm) {
   const int stride = gridDim.x * 128;
   const int t = blockIdx.x * 128 + threadIdx.x;
+#if HXG_FIXUP_PDL
+  // launched as a programmatic dependent of the brick kernel: wait for its
+  // completion (and memory flush) before reading the partials
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   FixupEntry<P, Q> e[kFixupItems];
   bool ok[kFixupItems];
 #pragma unroll
@@ -931,7 +939,22 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
     k<<<persistent_grid(k, D::T, smem, prm.nbricks), D::T, smem, op.stream_>>>(prm);
     HXG_CUDA(cudaGetLastError());
     const unsigned fg = fixup_rows<P, Q>(prm, 0, op.box_.npd[2]);
-    if (fg) fused_fixup_kernel<P, Q><<<fg, 128, 0, op.stream_>>>(prm);
+    if (fg) {
+#if HXG_FIXUP_PDL
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(fg);
+      cfg.blockDim = dim3(128);
+      cfg.stream = op.stream_;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      HXG_CUDA(cudaLaunchKernelEx(&cfg, fused_fixup_kernel<P, Q>, prm));
+#else
+      fused_fixup_kernel<P, Q><<<fg, 128, 0, op.stream_>>>(prm);
+#endif
+    }
     HXG_CUDA(cudaGetLastError());
   });
 }
