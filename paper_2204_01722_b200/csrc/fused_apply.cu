@@ -57,6 +57,9 @@ namespace {
 #ifndef HXG_PIPE_ALL_Q5
 #define HXG_PIPE_ALL_Q5 0
 #endif
+#ifndef HXG_BRICK_PDL
+#define HXG_BRICK_PDL 1
+#endif
 #ifndef HXG_FIXUP_PDL
 #define HXG_FIXUP_PDL 1
 #endif
@@ -249,6 +252,11 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
     for (unsigned off = 0; off < bytes; off += chunk)
       prefetch_l2(base + off, off + chunk <= bytes ? chunk : bytes - off);
   };
+#if HXG_BRICK_PDL
+  // launched as a programmatic dependent of whatever precedes it on the
+  // stream: nothing global is touched before the predecessor has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   if (tid == 0 && (int)blockIdx.x < prm.nbricks) prefetch_state(prm.brick0 + blockIdx.x);
 #if HXG_EXPERIMENT == 4
   long long t_last = clock64();
@@ -936,7 +944,23 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
                                   cudaSharedmemCarveoutMaxShared));
     prm.brick0 = 0;
     prm.nbricks = (int)op.lay_.num_bricks();
+#if HXG_BRICK_PDL
+    {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(persistent_grid(k, D::T, smem, prm.nbricks));
+      cfg.blockDim = dim3(D::T);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = op.stream_;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      HXG_CUDA(cudaLaunchKernelEx(&cfg, k, prm));
+    }
+#else
     k<<<persistent_grid(k, D::T, smem, prm.nbricks), D::T, smem, op.stream_>>>(prm);
+#endif
     HXG_CUDA(cudaGetLastError());
     const unsigned fg = fixup_rows<P, Q>(prm, 0, op.box_.npd[2]);
     if (fg) {
