@@ -58,10 +58,10 @@ namespace {
 #define HXG_PIPE_ALL_Q5 0
 #endif
 #ifndef HXG_BRICK_PDL
-#define HXG_BRICK_PDL 1
+#define HXG_BRICK_PDL 0
 #endif
 #ifndef HXG_FIXUP_PDL
-#define HXG_FIXUP_PDL 1
+#define HXG_FIXUP_PDL 0
 #endif
 #ifndef HXG_FIXUP_ITEMS
 #define HXG_FIXUP_ITEMS 2
