@@ -135,6 +135,36 @@ def cpu_reference_time(order, cells, applies, threads, warmup=1, one_thread_appl
     return P.op.size, time.perf_counter() - t0, "port", 1
 
 
+# SURVEY.md §8(d) "CPU p-MG solve baseline sizes": the reference's simplicial
+# coarse Cholesky (coarse_solver.hpp:44) limits the CPU solve to small cubes
+# (Q2 32^3 alone spends ~5 min in the single-threaded coarse factorisation),
+# so the default sample is Q2 20^3, Q3 21^3, Q4 16^3 (--cpu-pmg-sizes).
+CPU_PMG_SIZES = "2:20,3:21,4:16"
+
+
+def cpu_pmg_baseline(cases, threads):
+    """The compiled reference's p-MG solve on the host cores (study.hpp:83-107
+    timing method: setup_numeric and PCG to 1e-8 timed separately): cube,
+    fixed -x, traction (0,0,-0.02) on +x, linearised at u = 0."""
+    import numpy as np
+    from oracle import ref_lib as R
+    out = []
+    for order, n in cases:
+        ref = R.RefProblem(extents=(1, 1, 1), cells=(n,) * 3, order=order, fixed=("-x",),
+                           traction_face="+x", traction=(0, 0, -0.02), threads=threads)
+        b = -ref.apply_residual(np.zeros(ref.n))
+        t0 = time.perf_counter()
+        ref.mg_setup()
+        t1 = time.perf_counter()
+        r = ref.cg(b, precond="mg", rtol=1e-8)
+        t2 = time.perf_counter()
+        out.append({"order": order, "cells": n, "dofs": ref.n, "setup_numeric_s": t1 - t0,
+                    "pcg_rtol1e-8_s": t2 - t1, "pcg_rtol1e-8_iterations": r["iterations"],
+                    "condition": r["eig_max"] / r["eig_min"]})
+        del ref
+    return out
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
@@ -327,19 +357,21 @@ def run_ours(args, rank, world, local_rank):
     cfg5 = None
     if not args.no_cfg5:
         c5 = 160
-        prob5 = FemProblem(extents=(1.0, 1.0, 1.0), cells=(c5,) * 3, order=ORDER, fixed_faces=fixed,
-                           geometry="box")
-        n5 = prob5.size()
-        prob5.op.apply_residual(torch.zeros(n5, dtype=torch.float64, device="cuda"))
-        x5 = 1e-3 * torch.sin(0.7 * (torch.arange(n5, dtype=torch.float64, device="cuda") + rank * n5))
-        y5 = torch.empty_like(x5)
-        npd5 = (ORDER * c5 + 1,) * 3
         # cfg5 weak scaling: one 160^3 block per GPU in a px x py x pz
         # arrangement (2 x 2 x 2 at 8 GPUs), interface sums
         # through faces, edges and corners
         from paper_2204_01722_b200.partition import block_partition, exchange_block
         dims5 = {2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}.get(world, (world, 1, 1))
         blk5 = block_partition(tuple(c5 * d for d in dims5), dims5, rank, ORDER)
+        # only blocks on the global -x face carry its Dirichlet condition
+        fixed5 = ("-x",) if blk5.coords[0] == 0 else ()
+        prob5 = FemProblem(extents=(1.0, 1.0, 1.0), cells=(c5,) * 3, order=ORDER, fixed_faces=fixed5,
+                           geometry="box")
+        n5 = prob5.size()
+        prob5.op.apply_residual(torch.zeros(n5, dtype=torch.float64, device="cuda"))
+        x5 = 1e-3 * torch.sin(0.7 * (torch.arange(n5, dtype=torch.float64, device="cuda") + rank * n5))
+        y5 = torch.empty_like(x5)
+        npd5 = (ORDER * c5 + 1,) * 3
 
         def step5():
             prob5.op.apply_jacobian(x5, y5)
@@ -559,6 +591,30 @@ def run_ours(args, rank, world, local_rank):
             cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
                    "sample": f"failed: {exc}"}
 
+    # CPU p-MG solve baseline beside the GPU at the same sizes (rank 0, N = 1).
+    cpu_pmg = None
+    if (rank == 0 and world == 1 and not args.no_cpu_baseline and not args.no_newton
+            and args.cpu_pmg_sizes):
+        cases = [tuple(int(v) for v in c.split(":")) for c in args.cpu_pmg_sizes.split(",")]
+        threads = os.cpu_count() or 1
+        try:
+            rows = cpu_pmg_baseline(cases, threads)
+            for row in rows:
+                g = pmg_case(row["order"], row["cells"], False)
+                row["gpu"] = {"setup_numeric_s": g["setup_numeric_ms"] * 1e-3,
+                              "pcg_rtol1e-8_s": g["pcg_rtol1e-8_ms"] * 1e-3,
+                              "pcg_rtol1e-8_iterations": g["pcg_rtol1e-8_iterations"]}
+                row["iterations_within_1"] = abs(g["pcg_rtol1e-8_iterations"]
+                                                 - row["pcg_rtol1e-8_iterations"]) <= 1
+                row["speedup_setup"] = row["setup_numeric_s"] / row["gpu"]["setup_numeric_s"]
+                row["speedup_pcg"] = row["pcg_rtol1e-8_s"] / row["gpu"]["pcg_rtol1e-8_s"]
+            cpu_pmg = {"kind": "reference", "cores": threads, "cases": rows,
+                       "note": "compiled reference (oracle/_ref, Eigen-API shim for the Lanczos "
+                               "eigensolve and SimplicialLLT: a restatement, single-threaded) vs "
+                               "this library on cuda:0; wall seconds (CPU) / device events (GPU)"}
+        except Exception as exc:  # noqa: BLE001
+            cpu_pmg = {"kind": "reference", "cores": threads, "failed": str(exc)}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -581,6 +637,7 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": args.steps * op.kernel_launches(),
             "clocks": sampler.summary(),
             "cpu_baseline": cpu,
+            "cpu_pmg": cpu_pmg,
             "newton_krylov_step": newton,
             "pmg_solves": pmg,
             "pmg_distributed": pmg_dist,
@@ -603,6 +660,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-applies", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-pmg-sizes", default=CPU_PMG_SIZES,
+                    help="order:cells,... of the CPU p-MG solve baseline ('' to skip)")
     ap.add_argument("--no-newton", action="store_true")
     ap.add_argument("--no-cfg5", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],

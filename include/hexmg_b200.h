@@ -68,7 +68,8 @@ typedef struct hxg_asm_s* hxg_asm_t;     /* CooAssembly            assembly.hpp:
  * mesh.hpp:19-33; restriction is analytic, mesh.hpp:119-138), Basis1D
  * (basis.hpp:117-130), GeometricFactors dxidX/weight (mesh.hpp:169-189,
  * reference layout (e, q, 9) and (e, q)), NeoHookean (material.hpp:15-18),
- * JacobianStorage (only Current = 0 is implemented), Constraints mask
+ * JacobianStorage (0 Current, 1 InitialNative, 2 InitialTuned, 3 InitialAD;
+ * material.hpp:66-78), Constraints mask
  * (operator.hpp:29-35; NULL = unconstrained).  Host pointers, copied.
  */
 typedef struct {
@@ -81,7 +82,7 @@ typedef struct {
   const double* dxidX;   /* E*q^3*9   GeometricFactors::dxidX  */
   const double* weight;  /* E*q^3     GeometricFactors::weight */
   double mu, lambda;     /* NeoHookean                         */
-  int storage;           /* JacobianStorage; 0 = Current       */
+  int storage;           /* JacobianStorage 0..3 (see above)   */
   const uint8_t* mask;   /* 3*num_nodes Constraints::mask or NULL */
   /* Device-side geometry: when dxidX/weight are NULL
    * and both of these are given, the geometric factors of the axis-aligned

@@ -282,6 +282,7 @@ int hxg_mg_vcycle(hxg_mg_t mg, const double* b, double* x) {
 }
 int hxg_mg_smooth(hxg_mg_t mg, int level, const double* b, double* x) {
   return guarded([&] {
+    MG(mg).follow_stream();
     auto& lv = MG(mg).level(level);
     if (!lv.smoother.ready) throw hxg::Error(HXG_ERR_GENERIC, "smoother not set up");
     lv.smoother.apply(*lv.op, b, x, false);
@@ -289,9 +290,12 @@ int hxg_mg_smooth(hxg_mg_t mg, int level, const double* b, double* x) {
 }
 int hxg_mg_coarse_vals_device(hxg_mg_t mg, double* vals_dev) {
   return guarded([&] {
+    // ordered after the assembly kernels on the hierarchy's stream
     const auto& a = MG(mg).coarse_matrix();
-    HXG_CUDA(cudaMemcpy(vals_dev, a.vals.p, sizeof(double) * a.cols_h.size(),
-                        cudaMemcpyDeviceToDevice));
+    cudaStream_t s = MG(mg).stream();
+    HXG_CUDA(cudaMemcpyAsync(vals_dev, a.vals.p, sizeof(double) * a.cols_h.size(),
+                             cudaMemcpyDeviceToDevice, s));
+    HXG_CUDA(cudaStreamSynchronize(s));
   });
 }
 int hxg_mg_coarse_nnz(hxg_mg_t mg, int64_t* nnz) {
@@ -302,7 +306,10 @@ int hxg_mg_coarse_csr_host(hxg_mg_t mg, int* row_ptr, int* cols, double* vals) {
     const auto& a = MG(mg).coarse_matrix();
     std::memcpy(row_ptr, a.row_ptr_h.data(), sizeof(int) * a.row_ptr_h.size());
     std::memcpy(cols, a.cols_h.data(), sizeof(int) * a.cols_h.size());
-    HXG_CUDA(cudaMemcpy(vals, a.vals.p, sizeof(double) * a.cols_h.size(), cudaMemcpyDeviceToHost));
+    cudaStream_t s = MG(mg).stream();
+    HXG_CUDA(cudaMemcpyAsync(vals, a.vals.p, sizeof(double) * a.cols_h.size(),
+                             cudaMemcpyDeviceToHost, s));
+    HXG_CUDA(cudaStreamSynchronize(s));
   });
 }
 int hxg_mg_coarse_solve(hxg_mg_t mg, const double* b, double* x) {
@@ -468,8 +475,11 @@ int hxg_chol_factorize(hxg_chol_t h, const double* vals_host) {
 int hxg_chol_factorize_device(hxg_chol_t h, const double* vals_dev) {
   return guarded([&] {
     if (!h) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "null Cholesky handle");
-    HXG_CUDA(cudaMemcpy(h->a.vals.p, vals_dev, sizeof(double) * h->a.cols_h.size(),
-                        cudaMemcpyDeviceToDevice));
+    // The producer of vals_dev may be on any stream: wait for the device
+    // (a setup-time call), then copy on the handle's stream.
+    HXG_CUDA(cudaDeviceSynchronize());
+    HXG_CUDA(cudaMemcpyAsync(h->a.vals.p, vals_dev, sizeof(double) * h->a.cols_h.size(),
+                             cudaMemcpyDeviceToDevice, h->stream));
     h->solver.factorize(h->a, h->npd, h->stream);
   });
 }

@@ -294,6 +294,7 @@ Hierarchy::Hierarchy(Operator* fine, int fixed_face_mask, std::vector<int> sched
 }
 
 void Hierarchy::setup_numeric() {
+  follow_stream();
   PhaseTimer pt(stream());
   for (int k = 1; k < num_levels(); ++k) {
     level(k).smoother.create(*level(k).op, degree_);
@@ -308,21 +309,28 @@ void Hierarchy::setup_numeric() {
 }
 
 void Hierarchy::assemble_coarse() {
+  follow_stream();
   if (!assembly_) assembly_ = std::make_unique<CoarseAssembly>(*level(0).op);
   assembly_->numeric(*level(0).op);
 }
 
 void Hierarchy::prolong(int coarse_level, const double* xc, double* xf) {
+  follow_stream();
   level(coarse_level + 1).from_coarser->prolong(xc, xf, stream());
 }
 
 void Hierarchy::restrict_to(int coarse_level, const double* xf, double* xc) {
+  follow_stream();
   level(coarse_level + 1).from_coarser->restrict_to(xf, xc, stream());
 }
 
-void Hierarchy::coarse_solve(const double* b, double* x) { coarse_.solve(b, x, stream()); }
+void Hierarchy::coarse_solve(const double* b, double* x) {
+  follow_stream();
+  coarse_.solve(b, x, stream());
+}
 
 void Hierarchy::v_cycle(const double* b, double* x, bool x_zero) {
+  follow_stream();
   cycle(num_levels() - 1, b, x, x_zero);
   Operator* op = levels_.back()->op;
   vmask_copy(x, b, op->mask(), op->size(), stream());

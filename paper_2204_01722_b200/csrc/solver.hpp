@@ -81,6 +81,15 @@ class Hierarchy {
   // 0 automatic (dense below kDenseCoarseMax DoFs), 1 dense, 2 sparse ND.
   void set_coarse_mode(int m) { coarse_mode_ = m; }
   cudaStream_t stream() const { return levels_.back()->op->stream(); }
+  // The level operators follow the fine operator's stream: a caller may
+  // hxg_op_set_stream the fine operator after the hierarchy is built, and
+  // every entry point re-points the coarse levels before issuing work, so a
+  // V-cycle never splits across two streams.
+  void follow_stream() {
+    cudaStream_t s = stream();
+    for (auto& lv : levels_)
+      if (lv->op->stream() != s) lv->op->set_stream(s);
+  }
 
  private:
   void cycle(int k, const double* b, double* x, bool x_zero);

@@ -41,6 +41,18 @@ def _dev(t, n=None) -> torch.Tensor:
     return t
 
 
+def _out(t, n) -> torch.Tensor:
+    """Caller-supplied output buffer: the device kernels write n float64
+    entries through its pointer, so anything else is refused up front."""
+    if not isinstance(t, torch.Tensor):
+        raise ValueError("output buffer must be a torch tensor")
+    if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous() or t.numel() != n:
+        raise ValueError(f"output buffer must be a contiguous float64 CUDA tensor of {n} entries "
+                         f"(got {t.dtype}, {t.device}, contiguous={t.is_contiguous()}, "
+                         f"numel={t.numel()})")
+    return t
+
+
 @dataclass
 class Basis1D:
     """basis.hpp:117-130 (host tabulations from the library's setup)."""
@@ -227,24 +239,31 @@ class MatrixFreeOperator:
 
     def apply_residual(self, u, out=None):
         u = _dev(u, self._size)
-        out = torch.empty_like(u) if out is None else out
+        out = torch.empty_like(u) if out is None else _out(out, self._size)
         check(lib().hxg_op_apply_residual(self.h, _ptr(u), _ptr(out)))
         return out
 
     def apply_jacobian(self, du, out=None):
         du = _dev(du, self._size)
-        out = torch.empty_like(du) if out is None else out
+        out = torch.empty_like(du) if out is None else _out(out, self._size)
         check(lib().hxg_op_apply_jacobian(self.h, _ptr(du), _ptr(out)))
         return out
 
     def apply_jacobian_host(self, du: np.ndarray, out: np.ndarray | None = None):
         du = np.ascontiguousarray(du, np.float64)
-        out = np.empty_like(du) if out is None else out
+        if du.size != self._size:
+            raise ValueError("nodal field size mismatch")
+        if out is None:
+            out = np.empty_like(du)
+        elif not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.size == self._size
+                  and out.flags.c_contiguous and out.flags.writeable):
+            raise ValueError("host output must be a writeable contiguous float64 array of op.size()")
         check(lib().hxg_op_apply_jacobian_host(self.h, _ptr(du), _ptr(out)))
         return out
 
     def extract_diagonal(self, out=None):
-        out = torch.empty(self._size, dtype=torch.float64, device="cuda") if out is None else out
+        out = (torch.empty(self._size, dtype=torch.float64, device="cuda") if out is None
+               else _out(out, self._size))
         check(lib().hxg_op_extract_diagonal(self.h, _ptr(out)))
         return out
 
@@ -266,11 +285,12 @@ class MatrixFreeOperator:
         return ev
 
     def scatter_add(self, ev, out):
-        check(lib().hxg_op_scatter_add(self.h, _ptr(_dev(ev)), _ptr(out)))
+        check(lib().hxg_op_scatter_add(self.h, _ptr(_dev(ev)), _ptr(_out(out, self._size))))
         return out
 
     def time_jacobian(self, x, y, warmup=3, repeats=20) -> float:
         ms = ctypes.c_double()
+        x, y = _dev(x, self._size), _out(y, self._size)
         check(lib().hxg_op_time_jacobian(self.h, _ptr(x), _ptr(y), warmup, repeats, ctypes.byref(ms)))
         return ms.value
 
@@ -344,13 +364,14 @@ class MultigridHierarchy:
         return xc
 
     def v_cycle(self, b, x=None):
-        b = _dev(b)
-        x = torch.zeros_like(b) if x is None else x
+        b = _dev(b, self.level_size(self.num_levels() - 1))
+        x = torch.zeros_like(b) if x is None else _out(x, b.numel())
         check(lib().hxg_mg_vcycle(self.h, _ptr(b), _ptr(x)))
         return x
 
     def smooth(self, k, b, x):
-        check(lib().hxg_mg_smooth(self.h, k, _ptr(_dev(b)), _ptr(x)))
+        n = self.level_size(k)
+        check(lib().hxg_mg_smooth(self.h, k, _ptr(_dev(b, n)), _ptr(_out(x, n))))
         return x
 
     def coarse_csr(self):
@@ -406,8 +427,7 @@ class AssembledOperator:
 
     def matvec(self, x, y=None):
         x = _dev(x, self.n)
-        if y is None:
-            y = torch.empty_like(x)
+        y = torch.empty_like(x) if y is None else _out(y, self.n)
         check(lib().hxg_asm_matvec(self.h, _ptr(x), _ptr(y)))
         return y
 
@@ -455,7 +475,7 @@ class CoarseCholesky:
 
     def solve(self, b, x=None):
         b = _dev(b, self.n)
-        x = torch.empty_like(b) if x is None else x
+        x = torch.empty_like(b) if x is None else _out(x, self.n)
         check(lib().hxg_chol_solve(self.h, _ptr(b), _ptr(x)))
         return x
 
@@ -465,7 +485,7 @@ def cg_solve(op: MatrixFreeOperator, b, x=None, rtol=1e-8, max_iterations=500,
     """cg_solve (cg.hpp:81-134); precond in {"none", "jacobi", "mg"}."""
     pc = {"none": 0, "jacobi": 1, "mg": 2}[precond]
     b = _dev(b, op.size())
-    x = torch.zeros_like(b) if x is None else x
+    x = torch.zeros_like(b) if x is None else _out(x, op.size())
     rep = capi.CgReport()
     hist = np.zeros(max_iterations + 2)
     check(lib().hxg_cg_solve(op.h, mg.h if mg is not None else None, pc, _ptr(b), _ptr(x), rtol,

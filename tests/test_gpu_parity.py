@@ -182,9 +182,10 @@ def test_jacobian_perturbation_hook_breaks_fd():
 
 @pytest.mark.parametrize("order,n", [(2, 64), (3, 43), (4, 32)])
 def test_full_size_properties(order, n):
-    """BASELINE sizes: symmetry, linearity, A.0 = 0, run-to-run bitwise
-    determinism, fused == two-pass, and one random element spot-checked
-    against the oracle's dense element action."""
+    """BASELINE sizes, size-independent properties: symmetry, linearity,
+    A.0 = 0, run-to-run bitwise determinism, fused == two-pass.  The direct
+    comparison with the compiled reference at these sizes is
+    tests/test_gpu_reference_sizes.py."""
     from paper_2204_01722_b200.hexmg import FemProblem
     prob = FemProblem(extents=(1, 1, 1), cells=(n, n, n), order=order, geometry=True)
     N = prob.size()

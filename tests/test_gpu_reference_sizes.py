@@ -1,0 +1,125 @@
+"""Parity at the BASELINE sizes and the SURVEY.md §8(c) solver goldens,
+against the compiled reference run live on the GPU box's host cores
+(oracle/_ref/libhexmg_ref.so = the unmodified reference headers,
+oracle/Makefile).
+
+* Q2 64^3, Q3 43^3, Q4 32^3 (BASELINE.json configs[1..2]): residual,
+  exported 17-scalar state, Jacobian apply and extract_diagonal at u = 0
+  (the reference performance harness, study.hpp:198-212) and at the smooth
+  tau != 0 state of SURVEY.md §8(d) (operator.hpp:146-283), through the
+  production path (fused brick kernel + fix-up, multi-brick in every
+  direction) to 1e-12 relative L2 (north_star).
+* p-MG PCG to 1e-8 (cg.hpp:81-134, multigrid.hpp:137-194) on the §8(c)
+  cases Q2 8^3 / 16^3, Q3 16^3, Q4 12^3 with the nested-dissection coarse
+  Cholesky running (auto mode picks it above a few thousand coarse DoFs;
+  Q2 8^3 is also forced onto it): iterations within +-1 of the SURVEY
+  goldens and of the live reference, fine-level lambda_max against the
+  golden / reference, solution against the reference's at 10 rtol.
+"""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import ref_lib as R  # noqa: E402  (checker only)
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not R.available(), reason="oracle/_ref not built")]
+
+THREADS = max(1, os.cpu_count() or 1)
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def smooth_state(coords, mask, scale=1.0):
+    """SURVEY.md §8(d) parity state u(X) = (-0.05 X + 0.02 s, 0.03 s, 0.01 X^2),
+    s = sin(pi X / 2) sin(pi Y) sin(pi Z), constrained entries 0."""
+    X, Y, Z = coords[:, 0], coords[:, 1], coords[:, 2]
+    s = np.sin(np.pi * X / 2) * np.sin(np.pi * Y) * np.sin(np.pi * Z)
+    u = scale * np.stack([-0.05 * X + 0.02 * s, 0.03 * s, 0.01 * X**2], 1).ravel()
+    u[mask != 0] = 0.0
+    return u
+
+
+@pytest.mark.parametrize("order,n,geometry", [(2, 64, True), (3, 43, "box"), (4, 32, "box")])
+def test_baseline_size_operator_matches_reference(order, n, geometry):
+    from paper_2204_01722_b200.hexmg import FemProblem
+    ref = R.RefProblem(extents=(1, 1, 1), cells=(n,) * 3, order=order, fixed=("-x",),
+                       threads=THREADS)
+    prob = FemProblem(extents=(1, 1, 1), cells=(n,) * 3, order=order, fixed_faces=("-x",),
+                      geometry=geometry)
+    N = prob.size()
+    assert ref.n == N
+    mask = prob.mask
+    x = 1e-3 * np.sin(0.7 * np.arange(N))  # study.hpp:198-201 input
+
+    # u = 0 linearisation (the reference performance harness)
+    u0 = np.zeros(N)
+    ref.apply_residual(u0)
+    prob.op.apply_residual(cuda(u0))
+    assert rel(prob.op.apply_jacobian(cuda(x)), ref.apply_jacobian(x)) < 1e-12
+    assert rel(prob.op.extract_diagonal(), ref.extract_diagonal()) < 1e-12
+
+    # smooth tau != 0 state
+    u = smooth_state(ref.coords(), mask)
+    f_ref = ref.apply_residual(u)
+    f = prob.op.apply_residual(cuda(u))
+    assert rel(f, f_ref) < 1e-12
+    st_ref = ref.state()
+    st = prob.op.export_state(prob.num_elements, prob.nq)
+    scale = np.abs(st_ref).max(axis=(0, 1))
+    assert (np.abs(st - st_ref).max(axis=(0, 1)) <= 1e-12 * np.maximum(scale, 1.0)).all()
+    del st, st_ref
+    y_ref = ref.apply_jacobian(x)
+    y = prob.op.apply_jacobian(cuda(x))
+    assert rel(y, y_ref) < 1e-12
+    # constrained entries pass x through bitwise (operator.hpp:212-214)
+    yc = y.cpu().numpy()
+    assert np.array_equal(yc[mask != 0], x[mask != 0])
+    assert rel(prob.op.extract_diagonal(), ref.extract_diagonal()) < 1e-12
+
+
+# SURVEY.md §8(c) "PCG to 1e-8" goldens: (order, n, iterations, fine lambda_max)
+PCG_GOLDENS = [(2, 8, 10, 3.128782), (2, 16, 9, None), (3, 16, 8, None), (4, 12, 11, None)]
+
+
+@pytest.mark.parametrize("order,n,its_golden,lam_golden", PCG_GOLDENS)
+def test_survey_pcg_goldens_nested_dissection(order, n, its_golden, lam_golden):
+    from paper_2204_01722_b200.hexmg import FemProblem, cg_solve
+    kw = dict(extents=(1, 1, 1), cells=(n,) * 3, order=order)
+    ref = R.RefProblem(fixed=("-x",), traction_face="+x", traction=(0, 0, -0.02),
+                       threads=THREADS, **kw)
+    prob = FemProblem(fixed_faces=("-x",), traction_face="+x", traction=(0, 0, -0.02), **kw)
+    N = prob.size()
+    b = -ref.apply_residual(np.zeros(N))  # u = 0, b = -F(0)
+    f = prob.op.apply_residual(torch.zeros(N, dtype=torch.float64, device="cuda"))
+    assert rel(-f, b) < 1e-12
+    ref.mg_setup()
+    r_ref = ref.cg(b, precond="mg", rtol=1e-8)
+    mg = prob.hierarchy
+    L = mg.num_levels()
+    ncoarse = mg.level_size(0)
+    modes = ["auto"] if ncoarse > 6000 else ["auto", "nd"]
+    for mode in modes:
+        mg.set_coarse_mode(mode)
+        mg.setup_numeric()
+        lam = mg.lambda_max(L - 1)
+        assert abs(lam - ref.lambda_max(L - 1)) < 1e-10 * lam
+        if lam_golden is not None:
+            assert abs(lam - lam_golden) < 5e-7 * lam_golden
+        r = cg_solve(prob.op, cuda(b), rtol=1e-8, precond="mg", mg=mg)
+        assert r["converged"]
+        assert abs(r["iterations"] - its_golden) <= 1, (mode, r["iterations"])
+        assert abs(r["iterations"] - r_ref["iterations"]) <= 1, (mode, r["iterations"])
+        assert rel(r["x"], r_ref["x"]) < 1e-7, mode
+        cond, cond_ref = r["eig_max"] / r["eig_min"], r_ref["eig_max"] / r_ref["eig_min"]
+        assert abs(cond - cond_ref) < 1e-3 * cond_ref, mode
