@@ -48,7 +48,8 @@ typedef struct {
   int code;
   int element;     /* InvertedElementError::element(), -1 if n/a */
   int point;       /* InvertedElementError::point(),   -1 if n/a */
-  double jacobian; /* InvertedElementError::jacobian()            */
+  double jacobian; /* InvertedElementError::jacobian(); the curvature
+                      of an IndefiniteOperatorError                 */
   char message[512];
 } hxg_error;
 
@@ -287,6 +288,8 @@ int hxg_dot(const double* x, const double* y, int64_t n, void* stream, double* o
 /* Device memory helpers for callers without their own allocator. */
 int hxg_malloc(void** p, size_t bytes);
 int hxg_free(void* p);
+/* 1 if p is device (or managed) memory, 0 for host memory. */
+int hxg_pointer_is_device(const void* p, int* is_device);
 int hxg_memcpy_h2d(void* dst, const void* src, size_t bytes);
 int hxg_memcpy_d2h(void* dst, const void* src, size_t bytes);
 int hxg_device_synchronize(void);

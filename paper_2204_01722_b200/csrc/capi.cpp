@@ -381,6 +381,13 @@ int hxg_dot(const double* x, const double* y, int64_t n, void* stream, double* o
 
 int hxg_malloc(void** p, size_t bytes) { return guarded([&] { HXG_CUDA(cudaMalloc(p, bytes)); }); }
 int hxg_free(void* p) { return guarded([&] { HXG_CUDA(cudaFree(p)); }); }
+int hxg_pointer_is_device(const void* p, int* is_device) {
+  return guarded([&] {
+    cudaPointerAttributes a{};
+    HXG_CUDA(cudaPointerGetAttributes(&a, p));
+    *is_device = a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+  });
+}
 int hxg_memcpy_h2d(void* dst, const void* src, size_t bytes) {
   return guarded([&] { HXG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice)); });
 }

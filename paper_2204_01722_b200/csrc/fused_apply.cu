@@ -63,6 +63,21 @@ namespace {
 #ifndef HXG_FIXUP_PDL
 #define HXG_FIXUP_PDL 0
 #endif
+// Where the bulk L2 prefetch of a brick's quadrature state is issued:
+// 0 = the next brick, at the start of the current one; 1 = the current
+// brick, at its start (its state is first read after the node-block wait,
+// P1 and P2); 2 = the next brick, after the current P1 pass; 3 = the next
+// brick, after the current q-function phase.  Measured (ab_time, B200, us
+// per apply, modes 0/1/2/3): Q2 64^3 318.1/307.0/308.5/306.5, Q3 43^3
+// 335.9/324.2/332.6/327.4, Q4 32^3 364.3/371.3/379.4/388.1 (no prefetch:
+// 345.7/354.8/397.5).  A whole brick ahead keeps ~2 x 32 MB of state in
+// flight through L2, more than one die's half holds for Q2/Q3.
+#ifndef HXG_PF_MODE
+#define HXG_PF_MODE -1  // -1: per (P, Q) as measured
+#endif
+__host__ __device__ constexpr int pf_mode(int q) {
+  return HXG_PF_MODE >= 0 ? HXG_PF_MODE : (q == 5 ? 0 : 1);
+}
 #ifndef HXG_FIXUP_ITEMS
 #define HXG_FIXUP_ITEMS 2
 #endif
@@ -257,7 +272,8 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   // stream: nothing global is touched before the predecessor has completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-  if (tid == 0 && (int)blockIdx.x < prm.nbricks) prefetch_state(prm.brick0 + blockIdx.x);
+  if (pf_mode(Q) != 1 && tid == 0 && (int)blockIdx.x < prm.nbricks)
+    prefetch_state(prm.brick0 + blockIdx.x);
 #if HXG_EXPERIMENT == 4
   long long t_last = clock64();
   long long ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -342,7 +358,9 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
 #pragma unroll 1
   for (int bi = blockIdx.x; bi < prm.nbricks; bi += gridDim.x, cur ^= 1) {
   const int brick = prm.brick0 + bi;
-  if (tid == 0 && bi + (int)gridDim.x < prm.nbricks) prefetch_state(brick + gridDim.x);
+  const bool pf_next = tid == 0 && bi + (int)gridDim.x < prm.nbricks;
+  if (pf_mode(Q) == 0 && pf_next) prefetch_state(brick + gridDim.x);
+  if (pf_mode(Q) == 1 && tid == 0) prefetch_state(brick);
   const int bx = bc.x, by = bc.y, bz = bc.z;
   const BrickXYZ bnext = advance(bc);
   const double* st_brick = prm.state + (size_t)lay.brick_points() * brick * SP;
@@ -466,6 +484,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
       }
   }
   __syncthreads(); HXG_PHASE(1);
+  if (pf_mode(Q) == 2 && pf_next) prefetch_state(brick + gridDim.x);
   // P2: column owners (qx, qy): z pass for the three arrays.
   // Between the P1 and Q2 barriers the slab entries S[idx Q^2 + te] (idx <
   // 9N) belong to this thread alone (its column).  For (p, q) = (1, 2),
@@ -584,6 +603,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
       }
   }
   HXG_PHASE(2);
+  if (pf_mode(Q) == 3 && pf_next) prefetch_state(brick + gridDim.x);
 
   // ---- backward: exact adjoint of the forward passes ---------------------
   // Q1: column owners: z adjoints R0 = Bd_z^T Hz, R1 = B_z^T Hx, R2 = B_z^T Hy

@@ -14,6 +14,15 @@ namespace hxg {
 
 namespace {
 
+// IndefiniteOperatorError (errors.hpp:55-60); the curvature travels in the
+// error's value slot so the C++ drop-in can rethrow the reference type.
+Error indefinite(double curvature) {
+  Error e(HXG_ERR_INDEFINITE,
+          "operator is not positive definite (p^T A p = " + std::to_string(curvature) + ")");
+  e.jacobian = curvature;
+  return e;
+}
+
 // Krylov work vectors and the dot workspace (pinned result slots), kept
 // across calls: cudaMalloc / cudaMallocHost / cudaFree per solve would
 // synchronise the device and cost more than a V-cycle.  One set per vector
@@ -130,8 +139,7 @@ CgResult cg_solve(long long n, const DevOp& a, const DevOp& m, const double* b, 
   vsub_from(r.p, b, n, s);
   m(r.p, z.p);
   double rz = dot(r.p, z.p, n, ws, s);
-  if (rz < 0.0) throw Error(HXG_ERR_INDEFINITE, "operator is not positive definite (p^T A p = " +
-                                                    std::to_string(rz) + ")");
+  if (rz < 0.0) throw indefinite(rz);
   CgResult rep;
   double nat0 = std::sqrt(rz);
   if (nat0 == 0.0) {
@@ -145,8 +153,7 @@ CgResult cg_solve(long long n, const DevOp& a, const DevOp& m, const double* b, 
     a(p.p, ap.p);
     double pap = dot(p.p, ap.p, n, ws, s);
     if (pap <= 0.0)
-      throw Error(HXG_ERR_INDEFINITE,
-                  "operator is not positive definite (p^T A p = " + std::to_string(pap) + ")");
+      throw indefinite(pap);
     double alpha = rz / pap;
     alphas.push_back(alpha);
     cg_update_xr(x, r.p, p.p, ap.p, alpha, n, s);
