@@ -175,6 +175,7 @@ SIGNATURES = {
     "hxg_dot": [_vp, _vp, _i64, _vp, _P(_d)],
     "hxg_malloc": [_vp, _sz],
     "hxg_free": [_vp],
+    "hxg_pointer_is_device": [_vp, _vp],
     "hxg_memcpy_h2d": [_vp, _vp, _sz],
     "hxg_memcpy_d2h": [_vp, _vp, _sz],
     "hxg_device_synchronize": [],

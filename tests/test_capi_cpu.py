@@ -73,3 +73,15 @@ def test_invalid_arguments_raise(L):
         G.build_lagrange_basis(0, 2)
     with pytest.raises(ValueError):
         G.lame_from_young_poisson(1.0, 0.5)
+
+
+def test_dropin_binary_links():
+    """The C++ drop-in test binary (oracle/Makefile target, built from the
+    reference headers + include/hexmg_b200.hpp) resolves libhexmg_b200.so
+    in-tree; it runs under -m gpu (tests/test_gpu_dropin.py)."""
+    import subprocess
+    exe = os.path.join(ROOT, "oracle", "_ref", "test_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/test_dropin not built (needs /root/reference)")
+    out = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
+    assert "libhexmg_b200.so" in out and "not found" not in out, out
