@@ -195,57 +195,48 @@ def run_reference_arm(args, rank, world):
 # --------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------
-def exchange_faces(y, npd, rank, world, dist):
-    """Interface-plane sum with the neighbouring slabs over NCCL
-    (paper_2204_01722_b200.partition.exchange_faces; gloo-tested in
-    tests/test_multirank_cpu.py)."""
-    from paper_2204_01722_b200.partition import exchange_faces as _xf
-    return _xf(y, npd, rank, world, dist)
+def make_comm(rank, world, dist, backend):
+    """The library's communicator: built-in NCCL, or gloo callbacks (the
+    shared-GPU multi-rank test mode)."""
+    from paper_2204_01722_b200.distributed import Communicator
+    return Communicator(rank, world, dist, backend="nccl" if backend == "nccl" else "gloo")
 
-def run_distributed_pmg(rank, world, dist, stream):
+
+def run_distributed_pmg(rank, world, dist, stream, comm):
+    """Strong scaling of the cfg4 beam: the partitioned p-MG of the C++
+    library (hxg_mg_create_partitioned), slabs along x."""
     import torch
 
-    from paper_2204_01722_b200.distributed import (DistributedHierarchy, SlabBackend, SlabComm,
-                                                   distributed_pcg)
-    from paper_2204_01722_b200.hexmg import FemProblem, constraint_mask
-    from paper_2204_01722_b200.partition import slab_partition
+    from paper_2204_01722_b200.distributed import PartitionedProblem
 
     cells, order, ext = (96, 48, 48), 2, (2.0, 1.0, 1.0)
-    slab = slab_partition(cells, world, rank, order)
-    fixed = ("-x",) if rank == 0 else ()
-    prob = FemProblem(extents=(ext[0] / cells[0] * slab.cells[0], ext[1], ext[2]),
-                      cells=slab.cells, order=order, fixed_faces=fixed,
-                      traction_face="+x" if rank == world - 1 else None,
-                      traction=(-0.02, 0.0, 0.0))
-    comm = SlabComm(rank, world, dist)
+    pp = PartitionedProblem(comm, cells, (world, 1, 1), order=order, extents=ext,
+                            fixed_faces=("-x",), traction_face="+x", traction=(-0.02, 0.0, 0.0),
+                            geometry="box")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     torch.cuda.synchronize()
     ev[0].record(stream)
-    f = prob.op.apply_residual(torch.zeros(prob.size(), dtype=torch.float64, device="cuda"))
-    comm.exchange(f, slab.npd)
+    f = pp.residual(torch.zeros(pp.size(), dtype=torch.float64, device="cuda"))
     b = -f
     ev[1].record(stream)
-    hier = DistributedHierarchy(SlabBackend(prob, fixed), comm, cells, slab.x0,
-                                lambda p: constraint_mask(cells, p, ("-x",))[0])
-    hier.setup_numeric()  # symbolic (global coarse pattern, analysis) + numeric
-    distributed_pcg(hier, b, rtol=1e-3)  # warm-up
+    pp.setup_numeric()  # symbolic (global coarse pattern, analysis) + numeric
+    pp.cg_solve(b, rtol=1e-3)  # warm-up
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     ev[2].record(stream)
-    hier.setup_numeric()
+    pp.setup_numeric()
     ev[3].record(stream)
-    rep = distributed_pcg(hier, b, rtol=1e-8)
+    rep = pp.cg_solve(b, rtol=1e-8)
     ev[4].record(stream)
     torch.cuda.synchronize()
     # full Newton solve (1 load step, line search) on the slabs
-    from paper_2204_01722_b200.distributed import distributed_solve
     en = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     en[0].record(stream)
-    nrep = distributed_solve(hier, load_steps=1)
+    nrep = pp.solve(load_steps=1)
     en[1].record(stream)
     torch.cuda.synchronize()
     t = torch.tensor([ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3]),
@@ -261,9 +252,12 @@ def run_distributed_pmg(rank, world, dist, stream):
            "condition": rep["eig_max"] / rep["eig_min"],
            "newton_solve_ms": t[3].item(), "newton_iterations": nrep["newton_iterations"],
            "newton_cg_iterations": nrep["cg_iterations"], "newton_final_fnorm": nrep["final_fnorm"],
-           "coarse": "global Q1 matrix summed over slabs, replicated device Cholesky",
+           "path": "hxg_mg_create_partitioned (C++ library: interface sums, owned dots, "
+                   "partitioned transfers, Newton) over the library's communicator",
+           "coarse": "global Q1 matrix summed over the blocks (one all-reduce per setup), "
+                     "replicated device Cholesky",
            "timing": "device events, max over ranks"}
-    del hier, prob
+    del pp
     torch.cuda.empty_cache()
     return out
 
@@ -283,12 +277,17 @@ def run_ours(args, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group("gloo")
-    # Slab `rank` of a (64 N) x 64 x 64 box; only the global -x face is fixed.
-    fixed = ("-x",) if rank == 0 else ()
-    prob = FemProblem(extents=(1.0, 1.0, 1.0), cells=(CELLS,) * 3, order=ORDER, fixed_faces=fixed)
+    # Slab `rank` of a (64 N) x 64 x 64 box (weak scaling), only the global
+    # -x face fixed; N > 1: the library's partitioned operator (local fused
+    # apply + interface sums over its NCCL communicator).
+    from paper_2204_01722_b200.distributed import PartitionedProblem
+    comm = make_comm(rank, world, dist, args.dist_backend)
+    pp = PartitionedProblem(comm, (CELLS * world, CELLS, CELLS), (world, 1, 1), order=ORDER,
+                            extents=(float(world), 1.0, 1.0), fixed_faces=("-x",), geometry=True)
+    prob = pp.prob
     op = prob.op
+    fixed = ("-x",) if rank == 0 else ()
     N = prob.size()
-    npd = (ORDER * CELLS + 1,) * 3
     u = torch.zeros(N, dtype=torch.float64, device="cuda")
     op.apply_residual(u)  # linearisation state at u = 0 (study.hpp:198-201)
     gidx = torch.arange(N, dtype=torch.float64, device="cuda") + rank * N
@@ -298,9 +297,7 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
 
     def step():
-        op.apply_jacobian(x, y)
-        if dist is not None:
-            exchange_faces(y, npd, rank, world, dist)
+        pp.apply(x, y)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -359,24 +356,19 @@ def run_ours(args, rank, world, local_rank):
         c5 = 160
         # cfg5 weak scaling: one 160^3 block per GPU in a px x py x pz
         # arrangement (2 x 2 x 2 at 8 GPUs), interface sums
-        # through faces, edges and corners
-        from paper_2204_01722_b200.partition import block_partition, exchange_block
+        # through faces, edges and corners (the library's partitioned operator)
         dims5 = {2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}.get(world, (world, 1, 1))
-        blk5 = block_partition(tuple(c5 * d for d in dims5), dims5, rank, ORDER)
-        # only blocks on the global -x face carry its Dirichlet condition
-        fixed5 = ("-x",) if blk5.coords[0] == 0 else ()
-        prob5 = FemProblem(extents=(1.0, 1.0, 1.0), cells=(c5,) * 3, order=ORDER, fixed_faces=fixed5,
-                           geometry="box")
+        pp5 = PartitionedProblem(comm, tuple(c5 * d for d in dims5), dims5, order=ORDER,
+                                 extents=tuple(float(d) for d in dims5), fixed_faces=("-x",),
+                                 geometry="box")
+        prob5 = pp5.prob
         n5 = prob5.size()
         prob5.op.apply_residual(torch.zeros(n5, dtype=torch.float64, device="cuda"))
         x5 = 1e-3 * torch.sin(0.7 * (torch.arange(n5, dtype=torch.float64, device="cuda") + rank * n5))
         y5 = torch.empty_like(x5)
-        npd5 = (ORDER * c5 + 1,) * 3
 
         def step5():
-            prob5.op.apply_jacobian(x5, y5)
-            if dist is not None:
-                exchange_block(y5, npd5, blk5, dist)
+            pp5.apply(x5, y5)
 
         for _ in range(3):
             step5()
@@ -402,7 +394,7 @@ def run_ours(args, rank, world, local_rank):
                 "ms_per_apply": ms5, "GDoF_s": n5 * world / (ms5 * 1e-3) / 1e9,
                 "algorithmic_GB_s_per_gpu": b5 / (ms5 * 1e-3) / 1e9,
                 "roofline_frac": b5 / (ms5 * 1e-3) / 1e9 / peak_gbs()}
-        del prob5, x5, y5
+        del pp5, prob5, x5, y5
         torch.cuda.empty_cache()
 
     # JacobianStorage variants (paper Table III, material.hpp:66-78) on the
@@ -446,11 +438,13 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     e2e_steps = max(5, min(args.steps, 50))
     t0 = time.perf_counter()
+    xd, yd = torch.empty_like(x), torch.empty_like(x)
     for _ in range(e2e_steps):
-        op.apply_jacobian_host(xh_np, yh_np)
-        if dist is not None:
-            yd = yh.cuda(non_blocking=False)
-            exchange_faces(yd, npd, rank, world, dist)
+        if dist is None:
+            op.apply_jacobian_host(xh_np, yh_np)
+        else:  # host x -> device, partitioned apply (interface sums), -> host y
+            xd.copy_(xh)
+            pp.apply(xd, yd)
             yh.copy_(yd)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if dist is not None:
@@ -571,7 +565,7 @@ def run_ours(args, rank, world, local_rank):
     # ranks.
     pmg_dist = None
     if not args.no_newton:
-        pmg_dist = run_distributed_pmg(rank, world, dist, stream)
+        pmg_dist = run_distributed_pmg(rank, world, dist, stream, comm)
 
     # CPU baseline: the reference on the host cores, rank 0, N = 1 only.
     cpu = None

@@ -62,6 +62,7 @@ typedef struct hxg_op_s* hxg_op_t;       /* MatrixFreeOperator     operator.hpp:
 typedef struct hxg_mg_s* hxg_mg_t;       /* MultigridHierarchy     multigrid.hpp:88   */
 typedef struct hxg_chol_s* hxg_chol_t;   /* CholeskyCoarseSolver   coarse_solver.hpp:16 */
 typedef struct hxg_asm_s* hxg_asm_t;     /* CooAssembly            assembly.hpp:134   */
+typedef struct hxg_comm_s* hxg_comm_t;   /* communicator of a partitioned hierarchy  */
 
 /*
  * Operator descriptor = the arguments of the MatrixFreeOperator constructor
@@ -214,6 +215,60 @@ int hxg_asm_nnz(hxg_asm_t a, int64_t* nnz);
 int hxg_asm_matvec(hxg_asm_t a, const double* x, double* y);
 int hxg_asm_csr_host(hxg_asm_t a, int* row_ptr, int* cols, double* vals);
 int hxg_asm_destroy(hxg_asm_t a);
+
+/*
+ * Partitioned (multi-GPU) p-multigrid, SURVEY.md §8(e).  The reference is
+ * single-process; the paper distributes the same operator with
+ * sums of the shared nodes after every apply (A = P^T E^T B^T D B E P,
+ * PAPER.md:224-228, :316).  The box of global_cells elements is cut into
+ * dims[0] x dims[1] x dims[2] contiguous element blocks (rank = x fastest,
+ * hxg_partition_block gives this rank's block); each rank creates its fine
+ * operator on its block (hxg_op_create with the block's cells, geometry,
+ * Dirichlet mask and load) and the partitioned hierarchy over it.  Then
+ *   hxg_mg_apply / hxg_mg_residual   the operator / residual + interface sums,
+ *   hxg_mg_dot                       owned-entry dot, all-reduced,
+ *   hxg_mg_setup_numeric / _vcycle   smoothers on the summed diagonal,
+ *                                    lambda_max from the GLOBAL rough_seed,
+ *                                    transfers with the interface scaling,
+ *                                    the coarse level summed into the global
+ *                                    Q1 matrix and factorized on every rank,
+ *   hxg_cg_solve(op, mg, ...)        PCG with owned-entry dots,
+ *   hxg_newton_solve / hxg_solve_continuation   Newton-CG (L-BFGS: 1 rank).
+ * Communicator: the built-in NCCL one (libnccl.so.2 resolved at run time;
+ * the unique id from hxg_nccl_unique_id on one rank, broadcast by the caller)
+ * or a caller-supplied table.  Entry points are stream-ordered on `stream`
+ * (the operator's stream); return 0 on success.
+ */
+typedef struct {
+  void* ctx;
+  /* Grouped neighbour exchange: for each i < npeers send counts[i] doubles
+   * from send[i] to peers[i] and receive as many into recv[i] (device
+   * buffers). */
+  int (*exchange)(void* ctx, int npeers, const int* peers, const double* const* send,
+                  double* const* recv, const int64_t* counts, void* stream);
+  /* In-place all-reduce of `count` device doubles; op 0 = sum, 1 = max. */
+  int (*allreduce)(void* ctx, double* data, int64_t count, int op, void* stream);
+} hxg_comm_ops;
+int hxg_comm_create(int rank, int world, const hxg_comm_ops* ops, hxg_comm_t* out);
+int hxg_nccl_unique_id(void* id128);
+int hxg_comm_create_nccl(int rank, int world, const void* id128, hxg_comm_t* out);
+int hxg_comm_destroy(hxg_comm_t comm);
+/* This rank's block: local element counts and first global element. */
+int hxg_partition_block(const int global_cells[3], const int dims[3], int rank, int cells[3],
+                        int e0[3]);
+/* build_hierarchy (multigrid.hpp:212-268) on this rank's block; the
+ * Dirichlet faces are GLOBAL faces (bit f = -x,+x,-y,+y,-z,+z). */
+int hxg_mg_create_partitioned(hxg_op_t fine, hxg_comm_t comm, const int global_cells[3],
+                              const int dims[3], int global_fixed_face_mask, const int* schedule,
+                              int num_levels, int pre_smooth, int post_smooth, hxg_mg_t* out);
+/* Level operator (apply_jacobian + interface sums when partitioned). */
+int hxg_mg_apply(hxg_mg_t mg, int level, const double* x, double* y);
+/* Owned-entry dot on a level (all-reduced when partitioned). */
+int hxg_mg_dot(hxg_mg_t mg, int level, const double* x, const double* y, double* out);
+/* Fine residual (operator.hpp:146-180) + interface sums; an inverted
+ * element on any rank raises HXG_ERR_INVERTED_ELEMENT on every rank. */
+int hxg_mg_residual(hxg_mg_t mg, const double* u, double* f);
+int hxg_stream_synchronize(void* stream);
 
 /* CgReport (cg.hpp:42-50). */
 typedef struct {

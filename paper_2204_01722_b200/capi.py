@@ -176,6 +176,16 @@ SIGNATURES = {
     "hxg_malloc": [_vp, _sz],
     "hxg_free": [_vp],
     "hxg_pointer_is_device": [_vp, _vp],
+    "hxg_comm_create": [_i, _i, _vp, _vp],
+    "hxg_nccl_unique_id": [_vp],
+    "hxg_comm_create_nccl": [_i, _i, _vp, _vp],
+    "hxg_comm_destroy": [_vp],
+    "hxg_partition_block": [_vp, _vp, _i, _vp, _vp],
+    "hxg_mg_create_partitioned": [_vp, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _vp],
+    "hxg_mg_apply": [_vp, _i, _vp, _vp],
+    "hxg_mg_dot": [_vp, _i, _vp, _vp, _vp],
+    "hxg_mg_residual": [_vp, _vp, _vp],
+    "hxg_stream_synchronize": [_vp],
     "hxg_memcpy_h2d": [_vp, _vp, _sz],
     "hxg_memcpy_d2h": [_vp, _vp, _sz],
     "hxg_device_synchronize": [],

@@ -22,7 +22,11 @@ struct hxg_op_s {
   std::unique_ptr<hxg::Operator> owned;
   hxg::Operator* op = nullptr;
 };
+struct hxg_comm_s {
+  std::unique_ptr<hxg::Comm> c;
+};
 struct hxg_mg_s {
+  std::unique_ptr<hxg::Partition> part;  // partitioned hierarchies
   std::unique_ptr<hxg::Hierarchy> h;
   std::vector<hxg_op_s> level_handles;
 };
@@ -244,6 +248,39 @@ int hxg_mg_create(hxg_op_t fine, int fixed_face_mask, const int* schedule, int n
   });
 }
 
+int hxg_mg_create_partitioned(hxg_op_t fine, hxg_comm_t comm, const int global_cells[3],
+                              const int dims[3], int global_fixed_face_mask, const int* schedule,
+                              int num_levels, int pre_smooth, int post_smooth, hxg_mg_t* out) {
+  return guarded([&] {
+    if (!comm || !comm->c) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "null communicator");
+    std::vector<int> sched;
+    if (schedule) sched.assign(schedule, schedule + num_levels);
+    auto h = std::make_unique<hxg_mg_s>();
+    h->part = std::make_unique<hxg::Partition>(comm->c.get(), global_cells, dims);
+    h->h = std::make_unique<hxg::Hierarchy>(&OP(fine), global_fixed_face_mask, sched, pre_smooth,
+                                            post_smooth, h->part.get());
+    h->level_handles.resize((size_t)h->h->num_levels());
+    for (int k = 0; k < h->h->num_levels(); ++k) h->level_handles[(size_t)k].op = h->h->level(k).op;
+    *out = h.release();
+  });
+}
+
+int hxg_mg_apply(hxg_mg_t mg, int level, const double* x, double* y) {
+  return guarded([&] {
+    MG(mg).follow_stream();
+    MG(mg).level_apply(level, x, y);
+  });
+}
+int hxg_mg_dot(hxg_mg_t mg, int level, const double* x, const double* y, double* out) {
+  return guarded([&] {
+    MG(mg).follow_stream();
+    *out = MG(mg).level_dot(level, x, y);
+  });
+}
+int hxg_mg_residual(hxg_mg_t mg, const double* u, double* f) {
+  return guarded([&] { MG(mg).residual(u, f); });
+}
+
 int hxg_mg_destroy(hxg_mg_t mg) {
   delete mg;
   return HXG_OK;
@@ -282,10 +319,7 @@ int hxg_mg_vcycle(hxg_mg_t mg, const double* b, double* x) {
 }
 int hxg_mg_smooth(hxg_mg_t mg, int level, const double* b, double* x) {
   return guarded([&] {
-    MG(mg).follow_stream();
-    auto& lv = MG(mg).level(level);
-    if (!lv.smoother.ready) throw hxg::Error(HXG_ERR_GENERIC, "smoother not set up");
-    lv.smoother.apply(*lv.op, b, x, false);
+    MG(mg).smooth(level, b, x);
   });
 }
 int hxg_mg_coarse_vals_device(hxg_mg_t mg, double* vals_dev) {
@@ -323,6 +357,17 @@ int hxg_cg_solve(hxg_op_t op, hxg_mg_t mg, int precond, const double* b, double*
     long long n = o.size();
     cudaStream_t s = o.stream();
     hxg::DevOp a = [&o](const double* xx, double* yy) { o.apply_jacobian(xx, yy); };
+    // a partitioned hierarchy: its fine level operator and owned-entry dots
+    hxg::Hierarchy* ph = mg && mg->h && mg->h->partition() ? mg->h.get() : nullptr;
+    hxg::DotFn dotf;
+    if (ph) {
+      if (ph->level(ph->num_levels() - 1).op != &o)
+        throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "op is not the partitioned hierarchy's fine level");
+      const int fine = ph->num_levels() - 1;
+      ph->follow_stream();
+      a = [ph, fine](const double* xx, double* yy) { ph->level_apply(fine, xx, yy); };
+      dotf = [ph, fine](const double* xx, const double* yy) { return ph->level_dot(fine, xx, yy); };
+    }
     hxg::DevOp m;
     hxg::DevBuf<double> inv;
     if (precond == 0) {
@@ -341,7 +386,14 @@ int hxg_cg_solve(hxg_op_t op, hxg_mg_t mg, int precond, const double* b, double*
         h.v_cycle(r, z, true);
       };
     }
-    hxg::CgResult res = hxg::cg_solve(n, a, m, b, x, rtol, max_iterations, s);
+    if (ph && precond == 1) {  // the Jacobi diagonal needs the interface sums too
+      hxg::DevBuf<double> d((size_t)n);
+      o.extract_diagonal(d.p);
+      ph->partition()->exchange(o.p(), d.p, s);
+      hxg::vmask_fill(d.p, 1.0, o.mask(), n, s);
+      hxg::vreciprocal(inv.p, d.p, n, s);
+    }
+    hxg::CgResult res = hxg::cg_solve(n, a, m, b, x, rtol, max_iterations, s, ph ? &dotf : nullptr);
     if (report) {
       report->iterations = res.iterations;
       report->converged = res.converged ? 1 : 0;
@@ -377,6 +429,46 @@ int hxg_dot(const double* x, const double* y, int64_t n, void* stream, double* o
     hxg::DotWorkspace ws;
     *out = hxg::dot(x, y, n, ws, (cudaStream_t)stream);
   });
+}
+
+// ---- communicators ---------------------------------------------------------
+int hxg_comm_create(int rank, int world, const hxg_comm_ops* ops, hxg_comm_t* out) {
+  return guarded([&] {
+    if (!ops || rank < 0 || rank >= world)
+      throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "bad communicator arguments");
+    auto* c = new hxg_comm_s();
+    c->c = std::make_unique<hxg::Comm>(rank, world, *ops);
+    *out = c;
+  });
+}
+int hxg_nccl_unique_id(void* id128) { return guarded([&] { hxg::nccl_unique_id(id128); }); }
+int hxg_comm_create_nccl(int rank, int world, const void* id128, hxg_comm_t* out) {
+  return guarded([&] {
+    auto* c = new hxg_comm_s();
+    c->c = hxg::make_nccl_comm(rank, world, id128);
+    *out = c;
+  });
+}
+int hxg_comm_destroy(hxg_comm_t c) {
+  delete c;
+  return HXG_OK;
+}
+int hxg_partition_block(const int global_cells[3], const int dims[3], int rank, int cells[3],
+                        int e0[3]) {
+  return guarded([&] {
+    const int world = dims[0] * dims[1] * dims[2];
+    if (rank < 0 || rank >= world) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "rank outside the partition");
+    const int coords[3] = {rank % dims[0], (rank / dims[0]) % dims[1], rank / (dims[0] * dims[1])};
+    for (int d = 0; d < 3; ++d) {
+      const int base = global_cells[d] / dims[d], extra = global_cells[d] % dims[d];
+      if (base < 1) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "more blocks than element layers");
+      cells[d] = base + (coords[d] < extra ? 1 : 0);
+      e0[d] = coords[d] * base + (coords[d] < extra ? coords[d] : extra);
+    }
+  });
+}
+int hxg_stream_synchronize(void* stream) {
+  return guarded([&] { HXG_CUDA(cudaStreamSynchronize((cudaStream_t)stream)); });
 }
 
 int hxg_malloc(void** p, size_t bytes) { return guarded([&] { HXG_CUDA(cudaMalloc(p, bytes)); }); }

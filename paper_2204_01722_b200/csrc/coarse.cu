@@ -87,10 +87,11 @@ __global__ void csr_to_dense_kernel(const int* rows, const int* cols, const doub
 
 }  // namespace
 
-CoarseAssembly::CoarseAssembly(const Operator& op) {
-  box_ = op.box();
-  const int P = op.p();
-  const auto& mask = op.mask_host();
+CoarseAssembly::CoarseAssembly(const Operator& op) : CoarseAssembly(op.box(), op.mask_host()) {}
+
+CoarseAssembly::CoarseAssembly(const BoxDev& box, const std::vector<uint8_t>& mask) {
+  box_ = box;
+  const int P = box.p;
   long long nn = box_.num_nodes();
   if (3 * nn > 0x7fffffffLL) throw Error(HXG_ERR_UNSUPPORTED, "assembled operator exceeds int32 rows");
   int n = (int)(3 * nn);

@@ -26,6 +26,10 @@ class CoarseAssembly {
   // operator; higher orders serve the "assembled" representation of the
   // performance study (study.hpp:191-232).
   explicit CoarseAssembly(const Operator& op);
+  // Pattern only, for an order-box.p lattice and constraint mask (the
+  // global coarse matrix of the partitioned solver).
+  CoarseAssembly(const BoxDev& box, const std::vector<uint8_t>& mask);
+  CsrMatrix& mutable_matrix() { return a_; }
   // Numeric phase (coo_numeric + fill_from_coo): element matrices, then a
   // per-slot sum over elements in increasing element order.
   void numeric(Operator& op);

@@ -131,10 +131,12 @@ std::vector<double> rough_seed(long long n, const std::vector<uint8_t>& mask) {
 }
 
 CgResult cg_solve(long long n, const DevOp& a, const DevOp& m, const double* b, double* x,
-                  double rtol, int max_iterations, cudaStream_t s) {
+                  double rtol, int max_iterations, cudaStream_t s, const DotFn* dotf) {
   KrylovWork& w = krylov_work((size_t)n);
   DevBuf<double>&r = w.v[0], &z = w.v[1], &p = w.v[2], &ap = w.v[3];
   DotWorkspace& ws = w.ws;
+  auto dot = [&](const double* u, const double* v, long long nn, DotWorkspace& wsp,
+                 cudaStream_t st) { return dotf ? (*dotf)(u, v) : ::hxg::dot(u, v, nn, wsp, st); };
   a(x, r.p);
   vsub_from(r.p, b, n, s);
   m(r.p, z.p);
@@ -181,10 +183,12 @@ CgResult cg_solve(long long n, const DevOp& a, const DevOp& m, const double* b, 
 }
 
 double estimate_lambda_max(long long n, const DevOp& a, const double* inv_diag,
-                           const double* seed, int iterations, cudaStream_t s) {
+                           const double* seed, int iterations, cudaStream_t s, const DotFn* dotf) {
   KrylovWork& w = krylov_work((size_t)n);
   DevBuf<double>&x = w.v[0], &r = w.v[1], &z = w.v[2], &p = w.v[3], &ap = w.v[4];
   DotWorkspace& ws = w.ws;
+  auto dot = [&](const double* u, const double* v, long long nn, DotWorkspace& wsp,
+                 cudaStream_t st) { return dotf ? (*dotf)(u, v) : ::hxg::dot(u, v, nn, wsp, st); };
   vzero(x.p, n, s);
   vcopy(r.p, seed, n, s);
   vscale_mul(z.p, inv_diag, r.p, n, s);
@@ -214,29 +218,27 @@ double estimate_lambda_max(long long n, const DevOp& a, const double* inv_diag,
   return eig_max;
 }
 
-void Chebyshev::create(Operator& op, int degree_) {
+void Chebyshev::create(long long n, cudaStream_t s, int degree_, const DevOp& A,
+                       const std::function<void(double*)>& diag, const DotFn* dotf,
+                       const std::function<std::vector<double>()>& seed_fn) {
   degree = degree_;
-  long long n = op.size();
-  cudaStream_t s = op.stream();
   if (inv_diag.n != (size_t)n) {  // first setup: buffers and the (constant) seed
     inv_diag.alloc((size_t)n);
     r.alloc((size_t)n);
     d.alloc((size_t)n);
-    seed.upload(rough_seed(n, op.mask_host()));
+    seed.upload(seed_fn());
   }
-  op.extract_diagonal(d.p);  // d doubles as the diagonal scratch here
+  diag(d.p);  // d doubles as the diagonal scratch here
   if (!vreciprocal(inv_diag.p, d.p, n, s))
     throw Error(HXG_ERR_INVALID_SMOOTHER, "invalid smoother: zero diagonal entry");
-  lambda_max = estimate_lambda_max(
-      n, [&op](const double* x, double* y) { op.apply_jacobian(x, y); }, inv_diag.p, seed.p, 10, s);
+  lambda_max = estimate_lambda_max(n, A, inv_diag.p, seed.p, 10, s, dotf);
   lo = 0.1 * lambda_max;
   hi = 1.1 * lambda_max;
   ready = true;
 }
 
-void Chebyshev::apply(Operator& op, const double* b, double* x, bool x_zero) {
-  long long n = op.size();
-  cudaStream_t s = op.stream();
+void Chebyshev::apply(const DevOp& A, long long n, cudaStream_t s, const double* b, double* x,
+                      bool x_zero) {
   double theta = 0.5 * (hi + lo);
   double delta = 0.5 * (hi - lo);
   double sigma = theta / delta;
@@ -244,21 +246,71 @@ void Chebyshev::apply(Operator& op, const double* b, double* x, bool x_zero) {
   if (x_zero) {
     cheb_first_zero(x, d.p, b, inv_diag.p, theta, n, s);
   } else {
-    op.apply_jacobian(x, r.p);
+    A(x, r.p);
     cheb_first(x, r.p, d.p, b, inv_diag.p, theta, n, s);
   }
   for (int k = 2; k <= degree; ++k) {
-    op.apply_jacobian(x, r.p);
+    A(x, r.p);
     double rho_new = 1.0 / (2.0 * sigma - rho);
     cheb_step(x, r.p, d.p, b, inv_diag.p, rho_new * rho, 2.0 * rho_new / delta, n, s);
     rho = rho_new;
   }
 }
 
+// Partitioned coarse level: global p = 1 pattern (global mask), local ->
+// global slot and DoF maps.
+struct Hierarchy::DistCoarse {
+  std::unique_ptr<CoarseAssembly> global;  // pattern + summed values
+  int gnpd[3];
+  DevBuf<long long> slot_map;   // local slot -> global slot (-1: not summed)
+  DevBuf<long long> diag_slots;  // global constrained rows' diagonal slot
+  DevBuf<long long> dof_map;    // local DoF -> global DoF
+  DevBuf<double> gvec, gsol;
+};
+
+namespace {
+
+__global__ void scatter_slots(const double* __restrict__ lv, const long long* __restrict__ map,
+                              long long n, double* __restrict__ gv) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (map[i] >= 0) gv[map[i]] = lv[i];
+}
+__global__ void set_ones(double* __restrict__ v, const long long* __restrict__ idx, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    v[idx[i]] = 1.0;
+}
+__global__ void scatter_owned(const double* __restrict__ b, const uint8_t* __restrict__ owned,
+                              const long long* __restrict__ map, long long n, double* __restrict__ g) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (owned[i]) g[map[i]] = b[i];
+}
+__global__ void gather_dofs(const double* __restrict__ g, const long long* __restrict__ map,
+                            long long n, double* __restrict__ x) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = g[map[i]];
+}
+inline int grid_n(long long n) {
+  long long g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  return g < 1 ? 1 : (int)g;
+}
+
+}  // namespace
+
 Hierarchy::Hierarchy(Operator* fine, int fixed_face_mask, std::vector<int> schedule,
-                     int pre_smooth, int post_smooth)
-    : pre_(pre_smooth), post_(post_smooth) {
+                     int pre_smooth, int post_smooth, Partition* part)
+    : pre_(pre_smooth), post_(post_smooth), part_(part), global_faces_(fixed_face_mask) {
   int p = fine->p();
+  if (part_) {
+    for (int d = 0; d < 3; ++d)
+      if (fine->cells()[d] != part_->cells()[d])
+        throw Error(HXG_ERR_INVALID_ARGUMENT, "fine operator cells != this rank's block");
+    fixed_face_mask = part_->local_faces(fixed_face_mask);
+  }
   if (schedule.empty()) {
     schedule.push_back(p);
     while (schedule.back() > 1) schedule.push_back((schedule.back() + 1) / 2);
@@ -297,22 +349,169 @@ Hierarchy::Hierarchy(Operator* fine, int fixed_face_mask, std::vector<int> sched
     lv->residual.alloc(n);
     lv->correction.alloc(n);
     lv->restricted.alloc(n);
+    if (part_) lv->scaled.alloc(n);
   }
+}
+
+Hierarchy::~Hierarchy() = default;
+
+void Hierarchy::level_apply(int k, const double* x, double* y) {
+  Level& lv = level(k);
+  lv.op->apply_jacobian(x, y);
+  if (part_) {
+    part_->exchange(lv.order, y, stream());
+    // constrained rows are the identity on every block holding them, not
+    // summed (operator.hpp:212-214)
+    vmask_copy(y, x, lv.op->mask(), lv.op->size(), stream());
+  }
+}
+
+double Hierarchy::level_dot(int k, const double* x, const double* y) {
+  if (part_) return part_->dot(level(k).order, x, y, stream());
+  return dot(x, y, level(k).op->size(), ws_, stream());
+}
+
+void Hierarchy::smooth(int k, const double* b, double* x) {
+  follow_stream();
+  Level& lv = level(k);
+  if (!lv.smoother.ready) throw Error(HXG_ERR_GENERIC, "smoother not set up");
+  lv.smoother.apply([this, k](const double* xx, double* yy) { level_apply(k, xx, yy); },
+                    lv.op->size(), stream(), b, x, false);
+}
+
+void Hierarchy::residual(const double* u, double* f) {
+  follow_stream();
+  Operator& op = *levels_.back()->op;
+  if (!part_) {
+    op.apply_residual(u, f);
+    return;
+  }
+  // every rank learns of an inverted element anywhere (max all-reduce of
+  // the failure flag), then the residual's interface sums
+  bool bad = false;
+  Error saved(HXG_ERR_INVERTED_ELEMENT, "");
+  try {
+    op.apply_residual(u, f);
+  } catch (const Error& e) {
+    if (e.code != HXG_ERR_INVERTED_ELEMENT) throw;
+    bad = true;
+    saved = e;
+  }
+  if (part_->allreduce_max(bad ? 1.0 : 0.0, stream()) > 0.0) {
+    if (bad) throw saved;
+    throw Error(HXG_ERR_INVERTED_ELEMENT, "non-positive deformation jacobian on another rank");
+  }
+  part_->exchange(levels_.back()->order, f, stream());
 }
 
 void Hierarchy::setup_numeric() {
   follow_stream();
   PhaseTimer pt(stream());
+  cudaStream_t s = stream();
   for (int k = 1; k < num_levels(); ++k) {
-    level(k).smoother.create(*level(k).op, degree_);
+    Level& lv = level(k);
+    Operator* op = lv.op;
+    const int order = lv.order;
+    DotFn dotf = [this, k](const double* x, const double* y) { return level_dot(k, x, y); };
+    lv.smoother.create(
+        op->size(), s, degree_, [this, k](const double* x, double* y) { level_apply(k, x, y); },
+        [this, op, order, s](double* d) {
+          op->extract_diagonal(d);
+          if (part_) {  // summed over the blocks; constrained entries stay 1
+            part_->exchange(order, d, s);
+            vmask_fill(d, 1.0, op->mask(), op->size(), s);
+          }
+        },
+        part_ ? &dotf : nullptr,
+        [this, op, order]() {
+          return part_ ? part_->global_seed_slice(order, op->mask_host())
+                       : rough_seed(op->size(), op->mask_host());
+        });
     pt.mark("smoother (diag + lambda_max)");
   }
   if (!assembly_) assembly_ = std::make_unique<CoarseAssembly>(*level(0).op);
   assembly_->numeric(*level(0).op);
   pt.mark("coarse assembly");
-  coarse_.set_mode(coarse_mode_);
-  coarse_.factorize(assembly_->matrix(), level(0).op->box().npd, stream());
+  if (part_) {
+    dist_coarse_numeric();
+  } else {
+    coarse_.set_mode(coarse_mode_);
+    coarse_.factorize(assembly_->matrix(), level(0).op->box().npd, s);
+  }
   pt.mark("coarse factorization");
+}
+
+void Hierarchy::dist_coarse_numeric() {
+  cudaStream_t s = stream();
+  const CsrMatrix& la = assembly_->matrix();
+  if (!dc_) {  // symbolic: global pattern and the maps, once
+    dc_ = std::make_unique<DistCoarse>();
+    int gc[3];
+    for (int d = 0; d < 3; ++d) gc[d] = part_->gcells()[d];
+    BoxDev gbox = make_box(gc, 1);
+    std::vector<uint8_t> gmask;
+    face_mask(gc, 1, global_faces_, gmask);
+    dc_->global = std::make_unique<CoarseAssembly>(gbox, gmask);
+    for (int d = 0; d < 3; ++d) dc_->gnpd[d] = gbox.npd[d];
+    const CsrMatrix& ga = dc_->global->matrix();
+    int ln[3];
+    part_->npd(1, ln);
+    const int* e0 = part_->e0();
+    auto to_global = [&](long long dof) {
+      const long long node = dof / 3;
+      const int c = (int)(dof % 3);
+      const long long ix = node % ln[0], iy = (node / ln[0]) % ln[1], iz = node / ((long long)ln[0] * ln[1]);
+      return 3 * ((ix + e0[0]) + (long long)gbox.npd[0] * ((iy + e0[1]) + (long long)gbox.npd[1] * (iz + e0[2]))) + c;
+    };
+    std::vector<long long> smap(la.cols_h.size(), -1), dmap((size_t)la.n);
+    for (int r = 0; r < la.n; ++r) {
+      const long long gr = to_global(r);
+      dmap[(size_t)r] = gr;
+      if (gmask[(size_t)gr]) continue;  // constrained rows: identity re-imposed globally
+      const int* gb = ga.cols_h.data() + ga.row_ptr_h[(size_t)gr];
+      const int* ge = ga.cols_h.data() + ga.row_ptr_h[(size_t)gr + 1];
+      for (int sl = la.row_ptr_h[(size_t)r]; sl < la.row_ptr_h[(size_t)r + 1]; ++sl) {
+        const long long gcol = to_global(la.cols_h[(size_t)sl]);
+        if (gmask[(size_t)gcol]) continue;
+        const int* it = std::lower_bound(gb, ge, (int)gcol);
+        if (it == ge || *it != (int)gcol)
+          throw Error(HXG_ERR_GENERIC, "partitioned coarse pattern: slot outside the global pattern");
+        smap[(size_t)sl] = ga.row_ptr_h[(size_t)gr] + (it - gb);
+      }
+    }
+    std::vector<long long> diag;
+    for (int r = 0; r < ga.n; ++r)
+      if (gmask[(size_t)r]) diag.push_back(ga.row_ptr_h[(size_t)r]);  // the row's only slot
+    dc_->slot_map.upload(smap);
+    dc_->dof_map.upload(dmap);
+    if (!diag.empty()) dc_->diag_slots.upload(diag);
+    dc_->gvec.alloc((size_t)ga.n);
+    dc_->gsol.alloc((size_t)ga.n);
+  }
+  CsrMatrix& ga = dc_->global->mutable_matrix();
+  const long long gnnz = ga.nnz(), lnnz = la.nnz();
+  HXG_CUDA(cudaMemsetAsync(ga.vals.p, 0, sizeof(double) * gnnz, s));
+  scatter_slots<<<grid_n(lnnz), 256, 0, s>>>(la.vals.p, dc_->slot_map.p, lnnz, ga.vals.p);
+  HXG_CUDA(cudaGetLastError());
+  part_->comm().allreduce(ga.vals.p, gnnz, 0, s);
+  if (dc_->diag_slots.n)
+    set_ones<<<grid_n((long long)dc_->diag_slots.n), 256, 0, s>>>(ga.vals.p, dc_->diag_slots.p,
+                                                                 (long long)dc_->diag_slots.n);
+  HXG_CUDA(cudaGetLastError());
+  coarse_.set_mode(coarse_mode_);
+  coarse_.factorize(ga, dc_->gnpd, s);
+}
+
+void Hierarchy::dist_coarse_solve(const double* b, double* x) {
+  cudaStream_t s = stream();
+  const long long n = level(0).op->size(), gn = (long long)dc_->gvec.n;
+  HXG_CUDA(cudaMemsetAsync(dc_->gvec.p, 0, sizeof(double) * gn, s));
+  scatter_owned<<<grid_n(n), 256, 0, s>>>(b, part_->owned(1), dc_->dof_map.p, n, dc_->gvec.p);
+  HXG_CUDA(cudaGetLastError());
+  part_->comm().allreduce(dc_->gvec.p, gn, 0, s);
+  coarse_.solve(dc_->gvec.p, dc_->gsol.p, s);
+  gather_dofs<<<grid_n(n), 256, 0, s>>>(dc_->gsol.p, dc_->dof_map.p, n, x);
+  HXG_CUDA(cudaGetLastError());
 }
 
 void Hierarchy::assemble_coarse() {
@@ -321,19 +520,39 @@ void Hierarchy::assemble_coarse() {
   assembly_->numeric(*level(0).op);
 }
 
+// Partitioned transfers: a shared fine node gets the same prolongated value
+// from every block (its elements agree there), so the interface sum counts
+// it once per sharing block: x 1/2 per shared direction.  The restriction is
+// the exact transpose: x 1/2 on the shared fine planes, local, interface sum.
 void Hierarchy::prolong(int coarse_level, const double* xc, double* xf) {
   follow_stream();
   level(coarse_level + 1).from_coarser->prolong(xc, xf, stream());
+  if (part_) {
+    const int pf = level(coarse_level + 1).order;
+    part_->exchange(pf, xf, stream());
+    part_->scale_interfaces(pf, xf, 0.5, stream());
+  }
 }
 
 void Hierarchy::restrict_to(int coarse_level, const double* xf, double* xc) {
   follow_stream();
-  level(coarse_level + 1).from_coarser->restrict_to(xf, xc, stream());
+  Level& fl = level(coarse_level + 1);
+  if (!part_) {
+    fl.from_coarser->restrict_to(xf, xc, stream());
+    return;
+  }
+  vcopy(fl.scaled.p, xf, fl.op->size(), stream());
+  part_->scale_interfaces(fl.order, fl.scaled.p, 0.5, stream());
+  fl.from_coarser->restrict_to(fl.scaled.p, xc, stream());
+  part_->exchange(level(coarse_level).order, xc, stream());
 }
 
 void Hierarchy::coarse_solve(const double* b, double* x) {
   follow_stream();
-  coarse_.solve(b, x, stream());
+  if (part_)
+    dist_coarse_solve(b, x);
+  else
+    coarse_.solve(b, x, stream());
 }
 
 void Hierarchy::v_cycle(const double* b, double* x, bool x_zero) {
@@ -346,21 +565,22 @@ void Hierarchy::v_cycle(const double* b, double* x, bool x_zero) {
 void Hierarchy::cycle(int k, const double* b, double* x, bool x_zero) {
   cudaStream_t s = stream();
   if (k == 0) {
-    coarse_.solve(b, x, s);
+    coarse_solve(b, x);
     return;
   }
   Level& lv = level(k);
   Operator& op = *lv.op;
   long long n = op.size();
+  DevOp A = [this, k](const double* xx, double* yy) { level_apply(k, xx, yy); };
   for (int i = 0; i < pre_; ++i) {
-    lv.smoother.apply(op, b, x, x_zero && i == 0);
+    lv.smoother.apply(A, n, s, b, x, x_zero && i == 0);
   }
   bool still_zero = x_zero && pre_ == 0;
   double* r = lv.residual.p;
   if (still_zero) {
     vcopy(r, b, n, s);
   } else {
-    op.apply_jacobian(x, r);
+    level_apply(k, x, r);
     vsub_from(r, b, n, s);
   }
   Level& cl = level(k - 1);
@@ -376,7 +596,7 @@ void Hierarchy::cycle(int k, const double* b, double* x, bool x_zero) {
     vcopy(x, r, n, s);
   else
     vadd(x, r, n, s);
-  for (int i = 0; i < post_; ++i) lv.smoother.apply(op, b, x, false);
+  for (int i = 0; i < post_; ++i) lv.smoother.apply(A, n, s, b, x, false);
 }
 
 }  // namespace hxg
@@ -432,14 +652,38 @@ LineSearch critical_point_line_search(const std::function<double(double)>& g_eva
 
 }  // namespace
 
-SolveReport newton_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, double* u,
-                         int load_step, double time) {
-  const long long n = op.size();
-  cudaStream_t s = op.stream();
+System make_system(Operator& op, Hierarchy& mg) {
+  System sys;
+  sys.n = op.size();
+  sys.s = op.stream();
+  const int fine = mg.num_levels() - 1;
+  Hierarchy* h = &mg;
+  const long long n = sys.n;
+  cudaStream_t s = sys.s;
+  sys.residual = [h](const double* u, double* f) { h->residual(u, f); };
+  sys.jacobian = [h, fine](const double* x, double* y) { h->level_apply(fine, x, y); };
+  sys.dot = [h, fine](const double* x, const double* y) { return h->level_dot(fine, x, y); };
+  sys.prepare = [h] { h->setup_numeric(); };
+  sys.precond = [h, n, s](const double* r, double* z) {
+    vzero(z, n, s);
+    h->v_cycle(r, z, true);
+  };
+  return sys;
+}
+
+namespace {
+
+SolveReport newton_solve_sys(const System& sys, const NewtonConfig& cfg, double* u, int load_step,
+                             double time) {
+  const long long n = sys.n;
+  cudaStream_t s = sys.s;
   DevBuf<double> f((size_t)n), rhs((size_t)n), du((size_t)n), ut((size_t)n), ft((size_t)n);
+  auto dot = [&sys](const double* x, const double* y, long long, DotWorkspace&, cudaStream_t) {
+    return sys.dot(x, y);
+  };
   DotWorkspace ws;
   auto norm2 = [&](const double* v) { return std::sqrt(dot(v, v, n, ws, s)); };
-  op.apply_residual(u, f.p);
+  sys.residual(u, f.p);
   const double fnorm0 = norm2(f.p);
   SolveReport report;
   if (fnorm0 <= cfg.atol) {
@@ -447,17 +691,14 @@ SolveReport newton_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, d
     report.final_fnorm = fnorm0;
     return report;
   }
-  DevOp jac = [&op](const double* x, double* y) { op.apply_jacobian(x, y); };
-  DevOp pre = [&mg, n, s](const double* r, double* z) {
-    vzero(z, n, s);
-    mg.v_cycle(r, z, true);
-  };
+  const DevOp& jac = sys.jacobian;
+  const DevOp& pre = sys.precond;
   // g(a) = F(u + a du)^T du; F of the last evaluation stays in ft (and the
   // quadrature state at u + a du).  Inverted elements read as NaN.
   auto g_eval = [&](double a) {
     vwaxpy(ut.p, u, a, du.p, n, s);
     try {
-      op.apply_residual(ut.p, ft.p);
+      sys.residual(ut.p, ft.p);
     } catch (const Error& e) {
       if (e.code != HXG_ERR_INVERTED_ELEMENT) throw;
       return std::numeric_limits<double>::quiet_NaN();
@@ -467,10 +708,11 @@ SolveReport newton_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, d
   };
   double fnorm = fnorm0;
   for (int it = 1; it <= cfg.max_iterations; ++it) {
-    mg.setup_numeric();
+    sys.prepare();
     vneg(rhs.p, f.p, n, s);
     vzero(du.p, n, s);
-    CgResult cg = cg_solve(n, jac, pre, rhs.p, du.p, cfg.linear_rtol, cfg.linear_max_iterations, s);
+    CgResult cg =
+        cg_solve(n, jac, pre, rhs.p, du.p, cfg.linear_rtol, cfg.linear_max_iterations, s, &sys.dot);
     IterationRecord rec;
     rec.load_step = load_step;
     rec.time = time;
@@ -503,13 +745,22 @@ SolveReport newton_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, d
     }
   }
   // Leave the quadrature state at the accepted iterate.
-  op.apply_residual(u, f.p);
+  sys.residual(u, f.p);
   report.final_fnorm = norm2(f.p);
   return report;
 }
 
+}  // namespace
+
+SolveReport newton_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, double* u,
+                         int load_step, double time) {
+  return newton_solve_sys(make_system(op, mg), cfg, u, load_step, time);
+}
+
 SolveReport lbfgs_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, double* u,
                         int load_step, double time) {
+  if (mg.partition())
+    throw Error(HXG_ERR_UNSUPPORTED, "L-BFGS runs on one process (Newton-CG is partitioned)");
   const long long n = op.size();
   cudaStream_t s = op.stream();
   const int mem = std::max(cfg.lbfgs_memory, 0);

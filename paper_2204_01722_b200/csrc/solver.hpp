@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "coarse.hpp"
+#include "dist.hpp"
 #include "operator.hpp"
 #include "transfer.hpp"
 #include "vector.hpp"
@@ -17,6 +18,8 @@ namespace hxg {
 
 // LinearOperator (cg.hpp:16-19) over device vectors.
 using DevOp = std::function<void(const double*, double*)>;
+// dot (cg.hpp:34-38); partitioned: owned entries, all-reduced.
+using DotFn = std::function<double(const double*, const double*)>;
 
 struct CgResult {
   int iterations = 0;
@@ -33,10 +36,11 @@ std::vector<double> rough_seed(long long n, const std::vector<uint8_t>& mask);
 
 // cg_solve (cg.hpp:81-134).
 CgResult cg_solve(long long n, const DevOp& a, const DevOp& m, const double* b, double* x,
-                  double rtol, int max_iterations, cudaStream_t s);
+                  double rtol, int max_iterations, cudaStream_t s, const DotFn* dotf = nullptr);
 // estimate_lambda_max (cg.hpp:152-184).
 double estimate_lambda_max(long long n, const DevOp& a, const double* inv_diag,
-                           const double* seed, int iterations, cudaStream_t s);
+                           const double* seed, int iterations, cudaStream_t s,
+                           const DotFn* dotf = nullptr);
 
 // ChebyshevSmoother (smoother.hpp:15-63), degree 2 on [0.1, 1.1] lambda_max.
 struct Chebyshev {
@@ -45,10 +49,14 @@ struct Chebyshev {
   DevBuf<double> inv_diag, r, d;
   DevBuf<double> seed;  // rough_seed (cg.hpp:138-147), fixed per level
   bool ready = false;
-  void create(Operator& op, int degree_);
+  // A: the level operator; diag(out): its assembled diagonal; seed(): the
+  // Lanczos start vector (first call only); dotf: null = local dots.
+  void create(long long n, cudaStream_t s, int degree_, const DevOp& A,
+              const std::function<void(double*)>& diag, const DotFn* dotf,
+              const std::function<std::vector<double>()>& seed_fn);
   // One sweep; x_zero = x is known to be exactly zero (A x = 0 is skipped,
   // bitwise-identical: SURVEY.md Appendix A).
-  void apply(Operator& op, const double* b, double* x, bool x_zero);
+  void apply(const DevOp& A, long long n, cudaStream_t s, const double* b, double* x, bool x_zero);
 };
 
 struct Level {
@@ -58,22 +66,35 @@ struct Level {
   std::unique_ptr<Transfer> from_coarser;  // levels > 0
   Chebyshev smoother;
   DevBuf<double> residual, correction, restricted;
+  DevBuf<double> scaled;  // partitioned: interface-scaled copy for the restriction
 };
 
 class Hierarchy {
  public:
+  // part: null for one process; else the fine operator is this rank's block
+  // and fixed_face_mask names the GLOBAL Dirichlet faces.
   Hierarchy(Operator* fine, int fixed_face_mask, std::vector<int> schedule, int pre_smooth,
-            int post_smooth);
+            int post_smooth, Partition* part = nullptr);
+  ~Hierarchy();
   int num_levels() const { return (int)levels_.size(); }
   Level& level(int k) { return *levels_[(size_t)k]; }
+  Partition* partition() const { return part_; }
   void setup_numeric();
   // coo_numeric only (assembly.hpp:178-230): the assembled coarse operator
-  // without smoothers or factorization (the distributed p-MG gathers it).
+  // without smoothers or factorization (this rank's block when partitioned).
   void assemble_coarse();
   void prolong(int coarse_level, const double* xc, double* xf);
   void restrict_to(int coarse_level, const double* xf, double* xc);
   void v_cycle(const double* b, double* x, bool x_zero = false);
   void coarse_solve(const double* b, double* x);
+  // The level operator (local apply + interface sums when partitioned), its
+  // dot, one smoother sweep.
+  void level_apply(int k, const double* x, double* y);
+  double level_dot(int k, const double* x, const double* y);
+  void smooth(int k, const double* b, double* x);
+  // The fine-level residual (operator.hpp:146-180) + interface sums; an
+  // inverted element on any rank raises on every rank.
+  void residual(const double* u, double* f);
   const CsrMatrix& coarse_matrix() const {
     if (!assembly_) throw Error(HXG_ERR_STATE_NOT_INITIALIZED, "coarse operator not assembled");
     return assembly_->matrix();
@@ -97,6 +118,17 @@ class Hierarchy {
   std::unique_ptr<CoarseAssembly> assembly_;
   CoarseSolver coarse_;
   int pre_ = 1, post_ = 1, degree_ = 2, coarse_mode_ = 0;
+  Partition* part_ = nullptr;
+  int global_faces_ = 0;
+  DotWorkspace ws_;
+  // Partitioned coarse level (the replicated fallback of SURVEY.md §8(e)):
+  // the global p = 1 matrix summed from the blocks' assembled matrices (one
+  // all-reduce of its values per numeric setup), factorized on every rank;
+  // each coarse solve all-reduces the owned right-hand side entries.
+  struct DistCoarse;
+  std::unique_ptr<DistCoarse> dc_;
+  void dist_coarse_numeric();
+  void dist_coarse_solve(const double* b, double* x);
 };
 
 // Nonlinear driver (nonlinear.hpp): Newton-CG with the critical-point line
@@ -133,6 +165,18 @@ struct SolveReport {  // nonlinear.hpp:50-56
   double final_fnorm = 0.0;
   std::vector<IterationRecord> records;
 };
+// NonlinearSystem (nonlinear.hpp) over device vectors: the operator's
+// residual / Jacobian, dots and the V-cycle of its hierarchy -- the
+// partitioned versions when the hierarchy has a Partition.
+struct System {
+  long long n = 0;
+  cudaStream_t s = nullptr;
+  std::function<void(const double*, double*)> residual;
+  DevOp jacobian, precond;
+  DotFn dot;
+  std::function<void()> prepare;  // setup_numeric at the linearisation point
+};
+System make_system(Operator& op, Hierarchy& mg);
 // newton_solve (nonlinear.hpp:162-216) on op's residual / Jacobian with the
 // p-MG V-cycle rebuilt at every linearisation point.
 SolveReport newton_solve(Operator& op, Hierarchy& mg, const NewtonConfig& cfg, double* u,

@@ -35,6 +35,20 @@ __global__ void dot_stage1(const double* __restrict__ x, const double* __restric
   if (threadIdx.x == 0) partial[blockIdx.x] = r;
 }
 
+// Same partition and tree with the entries outside `mask` (0) skipped: the
+// owned-entry dots of the partitioned solver.
+__global__ void dot_stage1_masked(const double* __restrict__ x, const double* __restrict__ y,
+                                  const uint8_t* __restrict__ mask, long long n, double* partial) {
+  __shared__ double sh[32];
+  long long chunk = (n + gridDim.x - 1) / gridDim.x;
+  long long beg = blockIdx.x * chunk, end = beg + chunk < n ? beg + chunk : n;
+  double s = 0.0;
+  for (long long i = beg + threadIdx.x; i < end; i += blockDim.x)
+    if (mask[i]) s += x[i] * y[i];
+  double r = block_sum(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = r;
+}
+
 __global__ void dot_stage2(const double* partial, int m, double* out) {
   __shared__ double sh[32];
   double s = 0.0;
@@ -58,6 +72,9 @@ __global__ void k_mask_zero(double* y, const uint8_t* m, long long n) {
 }
 __global__ void k_mask_copy(double* y, const double* s, const uint8_t* m, long long n) {
   GRID_STRIDE(i, n) if (m[i]) y[i] = s[i];
+}
+__global__ void k_mask_fill(double* y, double v, const uint8_t* m, long long n) {
+  GRID_STRIDE(i, n) if (m[i]) y[i] = v;
 }
 __global__ void k_add(double* y, const double* x, long long n) { GRID_STRIDE(i, n) y[i] += x[i]; }
 __global__ void k_mul(double* y, const double* a, const double* x, long long n) {
@@ -135,6 +152,16 @@ void dot_async(const double* x, const double* y, long long n, DotWorkspace& ws, 
                            cudaMemcpyDeviceToHost, s));
 }
 
+double* dot_masked_device(const double* x, const double* y, const uint8_t* mask, long long n,
+                          DotWorkspace& ws, int slot, cudaStream_t s) {
+  if (mask)
+    dot_stage1_masked<<<kDotBlocks, kDotThreads, 0, s>>>(x, y, mask, n, ws.partial);
+  else
+    dot_stage1<<<kDotBlocks, kDotThreads, 0, s>>>(x, y, n, ws.partial);
+  dot_stage2<<<1, kDotThreads, 0, s>>>(ws.partial, kDotBlocks, ws.partial + kDotBlocks + slot);
+  return ws.partial + kDotBlocks + slot;
+}
+
 double dot(const double* x, const double* y, long long n, DotWorkspace& ws, cudaStream_t s) {
   dot_async(x, y, n, ws, 0, s);
   HXG_CUDA(cudaStreamSynchronize(s));
@@ -155,6 +182,9 @@ void vmask_zero(double* y, const uint8_t* m, long long n, cudaStream_t s) {
 }
 void vmask_copy(double* y, const double* src, const uint8_t* m, long long n, cudaStream_t s) {
   if (m) k_mask_copy<<<grid(n), 256, 0, s>>>(y, src, m, n);
+}
+void vmask_fill(double* y, double v, const uint8_t* m, long long n, cudaStream_t s) {
+  if (m) k_mask_fill<<<grid(n), 256, 0, s>>>(y, v, m, n);
 }
 void vadd(double* y, const double* x, long long n, cudaStream_t s) {
   k_add<<<grid(n), 256, 0, s>>>(y, x, n);

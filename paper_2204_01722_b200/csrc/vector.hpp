@@ -24,6 +24,11 @@ void dot_async(const double* x, const double* y, long long n, DotWorkspace& ws, 
 // Synchronous convenience: returns x . y.
 double dot(const double* x, const double* y, long long n, DotWorkspace& ws, cudaStream_t s);
 
+// x . y over the entries with mask[i] != 0 (all when mask is null), same
+// fixed-order reduction; the result stays on the device (slot < 8).
+double* dot_masked_device(const double* x, const double* y, const uint8_t* mask, long long n,
+                          DotWorkspace& ws, int slot, cudaStream_t s);
+
 void vcopy(double* y, const double* x, long long n, cudaStream_t s);
 void vzero(double* y, long long n, cudaStream_t s);
 // y = b - y
@@ -32,6 +37,8 @@ void vsub_from(double* y, const double* b, long long n, cudaStream_t s);
 void vmask_zero(double* y, const uint8_t* mask, long long n, cudaStream_t s);
 // y[i] = src[i] where mask[i]
 void vmask_copy(double* y, const double* src, const uint8_t* mask, long long n, cudaStream_t s);
+// y[i] = v where mask[i]
+void vmask_fill(double* y, double v, const uint8_t* mask, long long n, cudaStream_t s);
 // y += x
 void vadd(double* y, const double* x, long long n, cudaStream_t s);
 // w = x + a y

@@ -17,10 +17,10 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import hexmg_np as H
-from paper_2204_01722_b200.distributed import (DistributedHierarchy, SlabComm, distributed_pcg,
+from dist_model import (DistributedHierarchy, SlabComm, distributed_pcg,
                                                distributed_solve, global_rough_seed_slice,
                                                q1_lattice_pattern)
-from paper_2204_01722_b200.partition import slab_partition
+from dist_partition_model import slab_partition
 
 EXT = (3.0, 1.0, 1.0)
 TRACTION = (0.0, 0.0, -0.02)
@@ -247,8 +247,8 @@ def test_distributed_newton_matches_reference(case, traction, steps):
 
 
 def _block_worker(rank, world, port, cells, order, dims, out):
-    from paper_2204_01722_b200.distributed import BlockComm
-    from paper_2204_01722_b200.partition import block_partition
+    from dist_model import BlockComm
+    from dist_partition_model import block_partition
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -302,7 +302,7 @@ def test_block_partitioned_pmg_matches_single_process(dims):
 
 
 def test_block_partition_shapes():
-    from paper_2204_01722_b200.partition import block_partition
+    from dist_partition_model import block_partition
     bs = [block_partition((160, 160, 160), (2, 2, 2), r, 2) for r in range(8)]
     assert all(b.cells == (80, 80, 80) for b in bs)
     assert sorted(b.e0 for b in bs) == sorted((x, y, z) for x in (0, 80) for y in (0, 80)

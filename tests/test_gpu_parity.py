@@ -257,35 +257,6 @@ def test_coarse_cholesky_backends_agree(order, cells):
     assert its["nd"] == its["dense"] and abs(its["csrchol"] - its["dense"]) <= 1
 
 
-@pytest.mark.parametrize("order,cells", [(2, (6, 2, 2)), (3, (5, 3, 2))])
-def test_distributed_pmg_single_rank_matches_local(order, cells):
-    """The slab-partitioned p-MG composition (distributed.py) over the GPU
-    slab backend, world size 1: same lambda_max per level, same PCG
-    iterations and solution as the library's own cg_solve + V-cycle; and the
-    standalone coarse Cholesky (hxg_chol_*) solves the gathered global coarse
-    matrix."""
-    from paper_2204_01722_b200.distributed import DistributedHierarchy, SlabBackend, SlabComm, \
-        distributed_pcg
-    from paper_2204_01722_b200.hexmg import FemProblem, cg_solve, constraint_mask
-    prob = FemProblem(extents=(3, 1, 1), cells=cells, order=order, fixed_faces=("-x",),
-                      traction_face="+x", traction=(0, 0, -0.02))
-    f = prob.op.apply_residual(torch.zeros(prob.size(), dtype=torch.float64, device="cuda"))
-    mg = prob.hierarchy
-    mg.setup_numeric()
-    ref = cg_solve(prob.op, -f, rtol=1e-8, precond="mg", mg=mg)
-    hier = DistributedHierarchy(SlabBackend(prob, ("-x",)), SlabComm(), cells, 0,
-                                lambda p: constraint_mask(cells, p, ("-x",))[0])
-    hier.setup_numeric()
-    for k in range(1, mg.num_levels()):
-        assert abs(hier.lambda_max[k] - mg.lambda_max(k)) < 1e-12 * mg.lambda_max(k)
-    rep = distributed_pcg(hier, -f, rtol=1e-8)
-    assert abs(rep["iterations"] - ref["iterations"]) <= 1
-    assert rel(rep["x"], ref["x"].cpu().numpy()) < 1e-10
-    b0 = torch.sin(torch.arange(mg.level_size(0), dtype=torch.float64, device="cuda"))
-    b0[torch.as_tensor(constraint_mask(cells, 1, ("-x",))[0] != 0, device="cuda")] = 0.0
-    assert rel(hier.coarse_solve(b0), mg.coarse_solve(b0).cpu().numpy()) < 1e-10
-
-
 NEWTON = np.load(os.path.join(GOLD, "newton.npz"))
 
 

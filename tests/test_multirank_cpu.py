@@ -13,7 +13,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import hexmg_np as H
-from paper_2204_01722_b200.partition import exchange_faces, global_dot, owned_mask, slab_partition
+from dist_partition_model import exchange_faces, global_dot, owned_mask, slab_partition
 
 GLOBAL_CELLS = (6, 2, 2)
 EXT = (3.0, 1.0, 1.0)
