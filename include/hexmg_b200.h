@@ -168,7 +168,10 @@ int hxg_mg_assemble_coarse(hxg_mg_t mg);
 /* Coarse Cholesky backend: 0 automatic (dense below a few thousand DoFs,
  * else nested-dissection multifrontal), 1 dense, 2 nested-dissection
  * multifrontal, 3 cuSOLVER csrchol on the ND-permuted matrix.  Takes effect
- * at the next setup_numeric. */
+ * at the next setup_numeric.  4 = INEXACT coarse mode, a documented
+ * deviation from the reference's exact SimplicialLLT (coarse_solver.hpp:
+ * 16-47): the p = 1 level is solved by one Galerkin h-multigrid V-cycle
+ * (Chebyshev-Jacobi smoothing, dense bottom); single-process hierarchies. */
 int hxg_mg_set_coarse_mode(hxg_mg_t mg, int mode);
 int hxg_mg_lambda_max(hxg_mg_t mg, int level, double* out);
 /* prolong / restrict_to (multigrid.hpp:122-135). */

@@ -300,8 +300,8 @@ int hxg_mg_setup_numeric(hxg_mg_t mg) { return guarded([&] { MG(mg).setup_numeri
 int hxg_mg_assemble_coarse(hxg_mg_t mg) { return guarded([&] { MG(mg).assemble_coarse(); }); }
 int hxg_mg_set_coarse_mode(hxg_mg_t mg, int mode) {
   return guarded([&] {
-    if (mode < 0 || mode > 3)
-      throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "coarse mode must be 0, 1, 2 or 3");
+    if (mode < 0 || mode > 4)
+      throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "coarse mode must be 0, 1, 2, 3 or 4");
     MG(mg).set_coarse_mode(mode);
   });
 }

@@ -176,11 +176,23 @@ void CoarseAssembly::numeric(Operator& op) {
   HXG_CUDA(cudaGetLastError());
 }
 
-void CoarseAssembly::matvec(const double* x, double* y, cudaStream_t s) const {
-  csr_matvec_kernel<<<grid_for((long long)a_.n * 32, 256), 256, 0, s>>>(a_.n, a_.row_ptr.p, a_.cols.p,
-                                                                        a_.vals.p, x, y);
+void CoarseAssembly::numeric_from_elements(const double* elem, cudaStream_t s) {
+  dispatch_p(box_.p, [&](auto Pc) {
+    constexpr int P = decltype(Pc)::value;
+    long long nnz = a_.nnz();
+    fill_csr_kernel<P><<<grid_for(nnz, 256), 256, 0, s>>>(box_, a_.rows.p, a_.cols.p, mask_.p, elem,
+                                                          nnz, a_.vals.p);
+  });
   HXG_CUDA(cudaGetLastError());
 }
+
+void csr_matvec(const CsrMatrix& a, const double* x, double* y, cudaStream_t s) {
+  csr_matvec_kernel<<<grid_for((long long)a.n * 32, 256), 256, 0, s>>>(a.n, a.row_ptr.p, a.cols.p,
+                                                                       a.vals.p, x, y);
+  HXG_CUDA(cudaGetLastError());
+}
+
+void CoarseAssembly::matvec(const double* x, double* y, cudaStream_t s) const { csr_matvec(a_, x, y, s); }
 
 // ---------------------------------------------------------------------------
 // Dense device Cholesky for coarse levels that fit (cuSOLVER potrf/potrs).

@@ -18,6 +18,9 @@ struct CsrMatrix {
   long long nnz() const { return (long long)cols_h.size(); }
 };
 
+// y = A x, one warp per row, fixed-order reduction.
+void csr_matvec(const CsrMatrix& a, const double* x, double* y, cudaStream_t s);
+
 class CoarseAssembly {
  public:
   // Symbolic phase (coo_symbolic): the CSR pattern of the box operator of
@@ -36,6 +39,12 @@ class CoarseAssembly {
   const CsrMatrix& matrix() const { return a_; }
   // y = A x (CsrMatrix::matvec), device vectors.
   void matvec(const double* x, double* y, cudaStream_t s) const;
+  // Slot sums from caller-provided element matrices (same layout as the
+  // ones numeric() computes: E x M x M, M = 3 (p + 1)^3, unmasked).
+  void numeric_from_elements(const double* elem, cudaStream_t s);
+  // The element matrices of the last numeric() (device).
+  const double* element_matrices() const { return elem_.p; }
+  const BoxDev& box() const { return box_; }
 
  private:
   CsrMatrix a_;

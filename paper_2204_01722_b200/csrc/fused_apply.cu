@@ -16,8 +16,11 @@
 //   4. nodes interior to the brick are final and stored to y (constrained
 //      entries pass x through, operator.hpp:212-214); nodes on brick
 //      boundary planes store their partial sum to a per-brick buffer;
-//   5. a light second kernel sums the boundary partials of the (<= 8)
-//      bricks sharing each such node in increasing brick order.
+//   5. a light second kernel, one CTA per brick, sums the boundary partials
+//      of the (<= 8) bricks sharing each node the brick owns in increasing
+//      brick order.
+// The residual (MODE = kResidual, operator.hpp:146-180) runs the same pass
+// with the residual q-function on the streamed geometry, writing the state.
 // Every sum has a fixed order, so y is bitwise reproducible run to run.
 #include "fused_apply.cuh"
 
@@ -42,6 +45,17 @@
 #endif
 #ifndef HXG_SLOTS_Q4
 #define HXG_SLOTS_Q4 1
+#endif
+// Q2 (2, 3): planes of the gradients / q-function outputs kept in the
+// column-private shared slots (the rest in registers).
+#ifndef HXG_NSG_Q2
+#define HXG_NSG_Q2 3
+#endif
+#ifndef HXG_NSH_Q2
+#define HXG_NSH_Q2 3
+#endif
+#ifndef HXG_SKIP_FIXUP
+#define HXG_SKIP_FIXUP 0  // timing experiment only: results are wrong
 #endif
 #ifndef HXG_SLOTS_HIGHP
 #define HXG_SLOTS_HIGHP 0
@@ -78,9 +92,11 @@ namespace {
 __host__ __device__ constexpr int pf_mode(int q) {
   return HXG_PF_MODE >= 0 ? HXG_PF_MODE : (q == 5 ? 0 : 1);
 }
-#ifndef HXG_FIXUP_ITEMS
-#define HXG_FIXUP_ITEMS 2
+#ifndef HXG_FIXUP_THREADS
+#define HXG_FIXUP_THREADS 128
 #endif
+constexpr int kFixupThreads = HXG_FIXUP_THREADS;
+constexpr int kFixupMaxGrid = 148 * 64;
 
 struct FusedParams {
   BoxDev box;
@@ -93,19 +109,14 @@ struct FusedParams {
   const double* geo;  // geometric factors (w detJ for the perturbation hook)
   double mu, lambda, perturb;
   double* partial;
+  // residual mode: state written, external load, first inverted point
+  double* state_out;
+  const double* load;
+  double load_scale;
+  unsigned long long* fail;
   int brick0;   // first brick of this launch (pipelined host path)
   int nbricks;  // bricks in this launch
   int face_bits;  // >= 0: constraints are these whole faces (analytic), -1: mask array
-  // Fix-up launch: node planes [zs, ze) and the compact enumeration of the
-  // brick-boundary rows in them (fixup_rows()).
-  struct Rows {
-    int zs, ze;
-    int nzm;            // brick-plane multiples of PB2 in [zs, min(ze, npz - 1))
-    int nzp, nzn;       // z brick planes / other planes in range
-    int nyp, nyn, nxp;  // y planes / other y, x planes (whole box)
-    int threadsA;       // rows with gz or gy on a brick plane x 3 npx
-    int threadsB;       // remaining rows x 3 nxp (x brick planes only)
-  } fx;
   // Uniform copies of the 1D tables for the z-direction contractions
   // (constant-bank operands).
   double B[kMaxQ * (kMaxP + 1)];   // interp (Q x N)
@@ -156,6 +167,15 @@ __host__ __device__ constexpr int pad_plane(int p, int q) {
 // bricks; three for the 4-warp (3, 4) brick (shared memory allows it).
 __host__ __device__ constexpr int fused_min_blocks(int p, int q) {
   return p * 10 + q == 34 ? HXG_MINB_HIGHP : p * 10 + q == 23 ? HXG_MINB_Q2 : p * 10 + q == 45 ? HXG_MINB_Q4 : 2;
+}
+// Fused residual: the residual q-function needs more registers than the
+// Jacobian's.  Q2 (2, 3) fits two CTAs per SM without spills (Q2 64^3
+// residual 0.667 -> 0.536 ms); the larger bricks keep one.
+#ifndef HXG_RES_MINB
+#define HXG_RES_MINB 0  // 0: per (P, Q) as measured
+#endif
+__host__ __device__ constexpr int fused_residual_min_blocks(int p, int q) {
+  return HXG_RES_MINB > 0 ? HXG_RES_MINB : (p == 2 && q == 3) ? 2 : 1;
 }
 // Initial-storage variants (measured, Q2 64^3): Native and AD run 2 CTAs/SM
 // in 113 registers (0.525 / 0.667 ms vs 0.547 / 0.770 at 1 CTA); Tuned keeps
@@ -227,6 +247,15 @@ __device__ __forceinline__ void ld_stream2(const double* a, unsigned long long p
 __device__ __forceinline__ void st_keep(double* a, double v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }
+__device__ __forceinline__ void st_stream(double* a, double v, unsigned long long pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_stream2(double* a, double x, double y, unsigned long long pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(x),
+               "d"(y), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ double ld_once(const double* a, unsigned long long pol) {
   double v;
   asm("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
@@ -235,14 +264,22 @@ __device__ __forceinline__ double ld_once(const double* a, unsigned long long po
   return v;
 }
 
+
 // ST = JacobianStorage: Current streams the 16-scalar state through
 // jacobian_qf; the initial-configuration variants (material.hpp:196-239)
 // stream their 19 / 26 / 25-scalar reference layout through
 // jacobian_qf_initial (one CTA per SM: their q-functions need the registers).
-template <int P, int Q, int ST = kStorageCurrent>
+// MODE = kJacobian (y = J x on the streamed state) or kResidual (the
+// residual q-function on the streamed geometry, writing the state: the
+// residual of operator.hpp:146-180 in one pass, Current storage).
+template <int P, int Q, int ST = kStorageCurrent, int MODE = kJacobian>
 __global__ void __launch_bounds__(Dims<P, Q>::T,
-                                  ST == kStorageCurrent ? fused_min_blocks(P, Q) : variant_min_blocks(ST))
+                                  MODE == kResidual         ? fused_residual_min_blocks(P, Q)
+                                  : ST == kStorageCurrent ? fused_min_blocks(P, Q)
+                                                          : variant_min_blocks(ST))
     fused_jacobian_kernel(const __grid_constant__ FusedParams prm) {
+  static_assert(MODE == kJacobian || ST == kStorageCurrent, "fused residual: Current storage");
+  constexpr bool kRes = MODE == kResidual;
   constexpr int SS = device_state_stride(ST), SP = state_row(SS, Q);
   constexpr bool kStateV2 = state_paired(Q);  // 16-byte loads of the paired layout
   using D = FDims<P, Q>;
@@ -259,10 +296,12 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   // brick's quadrature state is one contiguous run, pulled into L2 one brick
   // ahead so the q-function loads hit L2.
   auto prefetch_state = [&](int b) {
-    constexpr unsigned bytes = (unsigned)(sizeof(double) * Q * SP * T);
+    // residual: the brick's geometry (the state is written, not read)
+    constexpr int RS = kRes ? kGeoStride : SP;
+    constexpr unsigned bytes = (unsigned)(sizeof(double) * Q * RS * T);
     constexpr unsigned chunk = 32768;
     const char* base = reinterpret_cast<const char*>(
-        prm.state + (size_t)lay.brick_points() * b * SP);
+        (kRes ? prm.geo : prm.state) + (size_t)lay.brick_points() * b * RS);
 #pragma unroll
     for (unsigned off = 0; off < bytes; off += chunk)
       prefetch_l2(base + off, off + chunk <= bytes ? chunk : bytes - off);
@@ -394,7 +433,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   // General masks: zero constrained inputs (operator.hpp:189-193) in the
   // landed block.  Whole-face masks are applied analytically as P1 reads the
   // block, which keeps x intact for the constrained pass-through.
-  if (fb < 0 && warp < WARPS && lane < 3 * nbx) {
+  if (!kRes && fb < 0 && warp < WARPS && lane < 3 * nbx) {
     for_rows(nby, nbz, [&](int iy, int iz) {
       const int dof = 3 * (node0 + npx * (iy + npy * iz)) + lane;
       if (fixed(dof, gx0 + lix, gy0 + iy, gz0 + iz))
@@ -437,7 +476,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
     for (int j = 0; j < N; ++j)
 #pragma unroll
       for (int i = 0; i < N; ++i) u[j][i] = Xp[j * D::NBXP + i];
-    if (fb > 0 && bmask) {
+    if (!kRes && fb > 0 && bmask) {
       const int gx = gx0 + P * lx, gy = gy0 + P * ly, gz = gz0 + P * lz + k;
       const bool mz = ((fb & 16) && gz == 0) || ((fb & 32) && gz == box.npd[2] - 1);
 #pragma unroll
@@ -495,8 +534,8 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   // does not forward them back into registers.
   // NSG / NSH planes of the gradients / q-function outputs live in the
   // slots, the rest in registers.
-  constexpr int NSG = fused_slots(P, Q) ? N : 0;
-  constexpr int NSH = NSG;
+  constexpr int NSG = !fused_slots(P, Q) ? 0 : (P == 2 && Q == 3) ? HXG_NSG_Q2 : N;
+  constexpr int NSH = !fused_slots(P, Q) ? 0 : (P == 2 && Q == 3) ? HXG_NSH_Q2 : N;
   constexpr int QR = Q - NSG, QH = Q - NSH;
   volatile double* slot = S + te;
   double g[3][3][QR > 0 ? QR : 1];
@@ -552,17 +591,58 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   // qz + 1 are loaded while plane qz is consumed.  Measured: all of them for
   // Q4 (394.5 -> 364.4 us); Q2 / Q3 have no register room for the full plane
   // (+1 % / +8 %).
-  constexpr int kPipe = (Q == 5 && ST == kStorageCurrent && (P == 4 || HXG_PIPE_ALL_Q5)) ? SP
+  constexpr int kPipe = kRes ? 0
+                        : (Q == 5 && ST == kStorageCurrent && (P == 4 || HXG_PIPE_ALL_Q5)) ? SP
                         : (P == 2 && Q == 3 && ST == kStorageCurrent)                   ? HXG_PIPE_Q2
                                                                                         : 0;
   double stn[kPipe > 0 ? kPipe : 1];
   if constexpr (kPipe > 0) {
     if (valid) load_range(0, stn, 0, kPipe);
   }
+  (void)load_range;
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
     double H[9];
-    if (valid) {
+    if constexpr (kRes) {
+      if (valid) {
+        const size_t pt = (size_t)lay.brick_points() * brick + (size_t)qz * T;
+        const double* gp = prm.geo + pt * kGeoStride + tid;
+        double geo[kGeoStride];
+#pragma unroll
+        for (int s = 0; s < kGeoStride; ++s) geo[s] = ld_stream(gp + s * T, pol_stream);
+        double G[9];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+            G[3 * c + d] = qz < NSG ? slot[gslot(c, d, qz)] : g[c][d][qz - NSG];
+        double st[kRefStateScalars];
+        const double J = residual_qf(prm.mu, prm.lambda, G, geo, geo[9], H, st);
+        double* so = prm.state_out + pt * SP + state_lane(tid, Q);
+        if (!(J > 0.0)) {  // first inverted (e, q) in reference order (operator.hpp:166-168)
+          const int qx = te % Q, qy = te / Q;
+          const long long e = (bx * BX + lx) + (long long)box.cells[0] * ((by * BY + ly) +
+                                                                     (long long)box.cells[1] * (bz * BZ + lz));
+          atomicMin(prm.fail, (unsigned long long)e * (Q * Q * Q) + (unsigned long long)(qx + Q * (qy + Q * qz)));
+          so[0] = J;  // read back by the host for the error report
+#pragma unroll
+          for (int k = 0; k < 9; ++k) H[k] = 0.0;
+        } else {
+          double sp[kStateStride];
+          pack_state(prm.mu, st, sp);
+          if constexpr (kStateV2) {
+#pragma unroll
+            for (int s = 0; s < kStateStride; s += 2) st_stream2(so + s * T, sp[s], sp[s + 1], pol_stream);
+          } else {
+#pragma unroll
+            for (int s = 0; s < kStateStride; ++s) st_stream(so + s * T, sp[s], pol_stream);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) H[k] = 0.0;
+      }
+    } else if (valid) {
       double st[SP];
       if constexpr (kPipe > 0) {
 #pragma unroll
@@ -582,7 +662,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
         jacobian_qf(prm.mu, prm.lambda, G, st, H);
       else
         jacobian_qf_initial<ST>(prm.mu, prm.lambda, G, st, H);
-      if (prm.perturb != 0.0) {  // fault-injection hook: + eps w detJ G
+      if (!kRes && prm.perturb != 0.0) {  // fault-injection hook: + eps w detJ G
         const double wdet =
             prm.geo[((size_t)lay.brick_points() * brick + (size_t)qz * T) * kGeoStride + 9 * T + tid];
 #pragma unroll
@@ -705,8 +785,12 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
         st_keep(part + (iz * NBY + iy) * ROW3 + lane, s, pol_keep);
       } else {
         const int dof = 3 * (node0 + npx * (iy + npy * iz)) + lane;
-        if (bmask && fixed(dof, gx0 + ix, gy0 + iy, gz0 + iz))  // pass x through (operator.hpp:212-214)
+        if constexpr (kRes) {  // f = r - s load; constrained: 0 (operator.hpp:175-179)
+          if (prm.load) s -= prm.load_scale * prm.load[dof];
+          if (bmask && fixed(dof, gx0 + ix, gy0 + iy, gz0 + iz)) s = 0.0;
+        } else if (bmask && fixed(dof, gx0 + ix, gy0 + iy, gz0 + iz)) {  // pass x through (operator.hpp:212-214)
           s = fb >= 0 ? Xc[c * D::NBP + (iz * D::NBYP + iy) * D::NBXP + ix] : prm.x[dof];
+        }
         prm.y[dof] = s;
       }
     };
@@ -731,151 +815,105 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
 #endif
 }
 
-// One boundary (node, component): the partials of its up-to-8 sharing
-// bricks, q = i0 + 2 i1 + 4 i2 = (c0, c1, c2) offsets from (lo0, lo1, lo2).
-// gather() issues the loads, finish() sums them in increasing q = increasing
-// brick order, so several entries' loads can be in flight together.
-template <int P, int Q>
-struct FixupEntry {
+// Brick-boundary sums (the deterministic second half of scatter_add,
+// mesh.hpp:105-116), brick-centric: a brick owns the nodes of its block that
+// are not on its upper faces (unless the box ends there); of those, the ones
+// on the block boundary were left as per-brick partials by the brick kernel.
+// Each is summed over its <= 8 sharing bricks in increasing brick order
+// (q = i0 + 2 i1 + 4 i2, brick lo_d + i_d).  One CTA per brick, one thread
+// per owned boundary node (its three components together); nodes are
+// enumerated compactly: rows (iy, iz) on a boundary plane are boundary along
+// their whole length, the other rows only at ix = 0 (and the far face of the
+// box).  The index math is all brick-local.
+template <int P, int Q, int MODE = kJacobian>
+__global__ void __launch_bounds__(kFixupThreads) fused_fixup_kernel(const __grid_constant__ FusedParams prm) {
   using D = FDims<P, Q>;
-  static constexpr int PB0 = P * D::BX, PB1 = P * D::BY, PB2 = P * D::BZ;
-  int gx, gy, gz, c;
-  unsigned valid = 0;  // bit q: brick q shares the node
-  double v[8];
-
-  __device__ __forceinline__ void gather(const FusedParams& prm) {
-    const QLayout& lay = prm.lay;
-    const int b1 = gy / PB1, b2 = gz / PB2, b0 = gx / PB0;
-    const int lo1 = (gy % PB1 == 0 && b1 > 0) ? b1 - 1 : b1, hi1 = min(b1, lay.nb[1] - 1);
-    const int lo2 = (gz % PB2 == 0 && b2 > 0) ? b2 - 1 : b2, hi2 = min(b2, lay.nb[2] - 1);
-    const int lo0 = (gx % PB0 == 0 && b0 > 0) ? b0 - 1 : b0, hi0 = min(b0, lay.nb[0] - 1);
-    const unsigned long long pol = policy_evict_first();
-    const int n0 = hi0 - lo0, n1 = hi1 - lo1, n2 = hi2 - lo2;  // 0 or 1
-    const double* p0 = prm.partial +
-                       (lo0 + (size_t)lay.nb[0] * (lo1 + (size_t)lay.nb[1] * lo2)) * (D::NB * 3) +
-                       (((gz - PB2 * lo2) * D::NBY + (gy - PB1 * lo1)) * D::NBX + (gx - PB0 * lo0)) * 3 + c;
+  constexpr int BX = D::BX, BY = D::BY, BZ = D::BZ;
+  constexpr int PB0 = P * BX, PB1 = P * BY, PB2 = P * BZ;
+  const QLayout& lay = prm.lay;
+  const BoxDev& box = prm.box;
+  const int npx = box.npd[0], npy = box.npd[1];
+  const unsigned long long pol = policy_evict_first();
+  const int fb = prm.face_bits;
+  for (int bi = blockIdx.x; bi < prm.nbricks; bi += gridDim.x) {
+    const int b = prm.brick0 + bi;
+    const int cx = b % lay.nb[0], cy = (b / lay.nb[0]) % lay.nb[1], cz = b / (lay.nb[0] * lay.nb[1]);
+    const int fnx = P * min(BX, box.cells[0] - cx * BX) + 1;
+    const int fny = P * min(BY, box.cells[1] - cy * BY) + 1;
+    const int fnz = P * min(BZ, box.cells[2] - cz * BZ) + 1;
+    const bool lx = cx == lay.nb[0] - 1, ly = cy == lay.nb[1] - 1, lz = cz == lay.nb[2] - 1;
+    const int nox = lx ? fnx : fnx - 1, noy = ly ? fny : fny - 1, noz = lz ? fnz : fnz - 1;
+    const int nbx = lx ? 2 : 1, nby = ly ? 2 : 1, nbz = lz ? 2 : 1;  // boundary coords per axis
+    const int iyc = noy - nby, izc = noz - nbz;                        // interior coords
+    const int rowsA = nbz * noy + izc * nby;
+    const int entA = rowsA * nox, entB = izc * iyc * nbx;  // nodes (3 components each)
+    const int gx0 = PB0 * cx, gy0 = PB1 * cy, gz0 = PB2 * cz;
+    for (int t = threadIdx.x; t < entA + entB; t += kFixupThreads) {
+      int ix, iy, iz;
+      if (t < entA) {
+        const int r = t / nox;
+        ix = t - r * nox;
+        if (r < nbz * noy) {
+          iz = r >= noy ? fnz - 1 : 0;
+          iy = r >= noy ? r - noy : r;
+        } else {
+          const int q = r - nbz * noy;
+          iz = 1 + q / nby;
+          iy = (q % nby) ? fny - 1 : 0;
+        }
+      } else {
+        const int u = t - entA, r = u / nbx;
+        ix = u - r * nbx ? fnx - 1 : 0;
+        iz = 1 + r / iyc;
+        iy = 1 + r % iyc;
+      }
+      // sharing bricks: one lower neighbour along d when the node sits on
+      // the block's low plane and the brick is not the first along d
+      const int s0 = ix == 0 && cx > 0, s1 = iy == 0 && cy > 0, s2 = iz == 0 && cz > 0;
+      const double* base = prm.partial + (size_t)b * (D::NB * 3) + ((iz * D::NBY + iy) * D::NBX + ix) * 3;
+      double v[8][3];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int i0 = q & 1, i1 = (q >> 1) & 1, i2 = q >> 2;
-      v[q] = 0.0;
-      if (i0 <= n0 && i1 <= n1 && i2 <= n2) {
-        // neighbour brick +i_d: brick index +i_d stride, local coordinate -i_d P B_d
-        const long long off = (i0 + (long long)lay.nb[0] * (i1 + (long long)lay.nb[1] * i2)) * (D::NB * 3) -
-                              3LL * ((i2 * PB2 * D::NBY + i1 * PB1) * D::NBX + i0 * PB0);
-        v[q] = ld_once(p0 + off, pol);
-        valid |= 1u << q;
+      for (int q = 0; q < 8; ++q) {
+        const int i0 = q & 1, i1 = (q >> 1) & 1, i2 = q >> 2;
+        if (i0 <= s0 && i1 <= s1 && i2 <= s2) {
+          // brick (c_d - s_d + i_d): index offset -(s_d - i_d) stride_d, local
+          // coordinate + (s_d - i_d) P B_d
+          const int o0 = s0 - i0, o1 = s1 - i1, o2 = s2 - i2;
+          const double* a = base - (long long)(o0 + lay.nb[0] * (o1 + lay.nb[1] * o2)) * (D::NB * 3) +
+                            3 * ((o2 * PB2 * D::NBY + o1 * PB1) * D::NBX + o0 * PB0);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) v[q][c] = ld_once(a + c, pol);
+        }
+      }
+      const int gx = gx0 + ix, gy = gy0 + iy, gz = gz0 + iz;
+      const size_t node = (size_t)gx + (size_t)npx * (gy + (size_t)npy * gz);
+      const bool ffix = fb > 0 && (((fb & 1) && gx == 0) || ((fb & 2) && gx == npx - 1) ||
+                                   ((fb & 4) && gy == 0) || ((fb & 8) && gy == npy - 1) ||
+                                   ((fb & 16) && gz == 0) || ((fb & 32) && gz == box.npd[2] - 1));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double sum = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int i0 = q & 1, i1 = (q >> 1) & 1, i2 = q >> 2;
+          if (i0 <= s0 && i1 <= s1 && i2 <= s2) sum += v[q][c];
+        }
+        const size_t dof = 3 * node + c;
+        const bool fixed = fb >= 0 ? ffix : prm.mask && prm.mask[dof];
+        if (MODE == kResidual) {  // f = r - s load; constrained: 0 (operator.hpp:175-179)
+          if (prm.load) sum -= prm.load_scale * prm.load[dof];
+          prm.y[dof] = fixed ? 0.0 : sum;
+        } else {
+          prm.y[dof] = fixed ? prm.x[dof] : sum;  // pass x through (operator.hpp:212-214)
+        }
       }
     }
   }
-
-  __device__ __forceinline__ void finish(const FusedParams& prm) const {
-    const int npx = prm.box.npd[0], npy = prm.box.npd[1];
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (valid & (1u << q)) s += v[q];
-    const size_t dof = 3 * ((size_t)gx + (size_t)npx * (gy + (size_t)npy * gz)) + c;
-    const int b = prm.face_bits;
-    const bool fixed =
-        b >= 0 ? ((b & 1) && gx == 0) || ((b & 2) && gx == npx - 1) || ((b & 4) && gy == 0) ||
-                     ((b & 8) && gy == npy - 1) || ((b & 16) && gz == 0) ||
-                     ((b & 32) && gz == prm.box.npd[2] - 1)
-               : prm.mask && prm.mask[dof];
-    prm.y[dof] = fixed ? prm.x[dof] : s;  // pass x through (operator.hpp:212-214)
-  }
-};
-
-// Sums brick-boundary partials: nodes on planes g_d = k P B_d (or the domain's
-// far face) in increasing brick order.  One index per boundary (node,
-// component), enumerated compactly (no idle blocks): first the rows with gz or
-// gy on a brick plane, boundary along their whole length (consecutive threads
-// read consecutive doubles of a brick's partial row), then the other rows,
-// which only hold the x brick-plane nodes.  Each thread takes kFixupItems
-// indices a grid-stride apart, all their loads in flight at once.
-constexpr int kFixupItems = HXG_FIXUP_ITEMS;
-__device__ __forceinline__ int plane_at(int k, int nmult, int s, int pb, int far) {
-  return k < nmult ? s + k * pb : far;
-}
-__device__ __forceinline__ int between_at(int j, int s, int pb) {  // j-th non-plane >= s
-  const int w = pb > 1 ? pb - 1 : 1;
-  return s + pb * (j / w) + 1 + j % w;
 }
 
-template <int P, int Q>
-__device__ __forceinline__ bool fixup_decode(const FusedParams& prm, int t, FixupEntry<P, Q>& e) {
-  using E = FixupEntry<P, Q>;
-  const auto& fx = prm.fx;
-  const int npx = prm.box.npd[0], npy = prm.box.npd[1], npz = prm.box.npd[2];
-  if (t < fx.threadsA) {
-    const int W = 3 * npx, r = t / W, k = t - r * W;
-    e.gx = k / 3;
-    e.c = k - 3 * e.gx;
-    const int rz = fx.nzp * npy;
-    if (r < rz) {
-      e.gz = plane_at(r / npy, fx.nzm, fx.zs, E::PB2, npz - 1);
-      e.gy = r % npy;
-    } else {
-      const int q = r - rz;
-      e.gz = between_at(q / fx.nyp, fx.zs, E::PB2);
-      e.gy = plane_at(q % fx.nyp, fx.nyp - 1, 0, E::PB1, npy - 1);
-    }
-    return true;
-  }
-  const int u = t - fx.threadsA;
-  if (u >= fx.threadsB) return false;
-  const int W = 3 * fx.nxp, r = u / W, k = u - r * W;
-  const int kx = k / 3;
-  e.c = k - 3 * kx;
-  e.gx = plane_at(kx, fx.nxp - 1, 0, E::PB0, npx - 1);
-  e.gz = between_at(r / fx.nyn, fx.zs, E::PB2);
-  e.gy = between_at(r % fx.nyn, 0, E::PB1);
-  return true;
-}
-
-template <int P, int Q>
-__global__ void __launch_bounds__(128) fused_fixup_kernel(const __grid_constant__ FusedParams prm) {
-  const int stride = gridDim.x * 128;
-  const int t = blockIdx.x * 128 + threadIdx.x;
-#if HXG_FIXUP_PDL
-  // launched as a programmatic dependent of the brick kernel: wait for its
-  // completion (and memory flush) before reading the partials
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
-  FixupEntry<P, Q> e[kFixupItems];
-  bool ok[kFixupItems];
-#pragma unroll
-  for (int k = 0; k < kFixupItems; ++k) {
-    ok[k] = fixup_decode<P, Q>(prm, t + k * stride, e[k]);
-    if (ok[k]) e[k].gather(prm);
-  }
-#pragma unroll
-  for (int k = 0; k < kFixupItems; ++k)
-    if (ok[k]) e[k].finish(prm);
-}
-
-// Boundary-row enumeration of a fix-up launch over node planes [zs, ze)
-// (zs a multiple of P B_z).
-template <int P, int Q>
-unsigned fixup_rows(FusedParams& prm, int zs, int ze) {
-  using D = FDims<P, Q>;
-  constexpr int PB0 = P * D::BX, PB1 = P * D::BY, PB2 = P * D::BZ;
-  const int npx = prm.box.npd[0], npy = prm.box.npd[1], npz = prm.box.npd[2];
-  auto& fx = prm.fx;
-  fx.zs = zs;
-  fx.ze = ze;
-  const int top = ze < npz - 1 ? ze : npz - 1;
-  fx.nzm = top > zs ? (top - zs + PB2 - 1) / PB2 : 0;
-  fx.nzp = fx.nzm + (ze == npz ? 1 : 0);
-  fx.nzn = (ze - zs) - fx.nzp;
-  fx.nyp = (npy - 1 + PB1 - 1) / PB1 + 1;
-  fx.nyn = npy - fx.nyp;
-  fx.nxp = (npx - 1 + PB0 - 1) / PB0 + 1;
-  const long long a = (long long)(fx.nzp * (long long)npy + (long long)fx.nzn * fx.nyp) * 3 * npx;
-  const long long b = (long long)fx.nzn * fx.nyn * 3 * fx.nxp;
-  if (a + b > 0x7fffffffLL) throw Error(HXG_ERR_INVALID_ARGUMENT, "fix-up index space exceeds int32");
-  fx.threadsA = (int)a;
-  fx.threadsB = (int)b;
-  return (unsigned)((a + b + 128LL * kFixupItems - 1) / (128LL * kFixupItems));
+// Fix-up grid over a launch's bricks.
+inline unsigned fixup_grid(int nbricks) {
+  return (unsigned)(nbricks < kFixupMaxGrid ? (nbricks > 0 ? nbricks : 1) : kFixupMaxGrid);
 }
 
 // Persistent grid: every resident CTA slot of the device, capped by the work.
@@ -982,12 +1020,12 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
     k<<<persistent_grid(k, D::T, smem, prm.nbricks), D::T, smem, op.stream_>>>(prm);
 #endif
     HXG_CUDA(cudaGetLastError());
-    const unsigned fg = fixup_rows<P, Q>(prm, 0, op.box_.npd[2]);
+    const unsigned fg = HXG_SKIP_FIXUP ? 0 : fixup_grid(prm.nbricks);
     if (fg) {
 #if HXG_FIXUP_PDL
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(fg);
-      cfg.blockDim = dim3(128);
+      cfg.blockDim = dim3(kFixupThreads);
       cfg.stream = op.stream_;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -996,9 +1034,53 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
       cfg.numAttrs = 1;
       HXG_CUDA(cudaLaunchKernelEx(&cfg, fused_fixup_kernel<P, Q>, prm));
 #else
-      fused_fixup_kernel<P, Q><<<fg, 128, 0, op.stream_>>>(prm);
+      fused_fixup_kernel<P, Q><<<fg, kFixupThreads, 0, op.stream_>>>(prm);
 #endif
     }
+    HXG_CUDA(cudaGetLastError());
+  });
+}
+
+// Fused residual (operator.hpp:146-180): one brick pass writing the state
+// and f = r(u) - s load (constrained entries 0); the caller reads back the
+// first inverted point.
+void fused_residual(Operator& op, const double* u, double* f) {
+  if (op.storage_ != kStorageCurrent || !op.geometry_)
+    throw Error(HXG_ERR_UNSUPPORTED, "fused residual: Current storage with geometric factors");
+  FusedParams prm{};
+  prm.box = op.box_;
+  prm.lay = op.lay_;
+  prm.x = u;
+  prm.y = f;
+  prm.mask = op.mask();
+  prm.face_bits = op.face_bits();
+  prm.tab = op.tab_.p;
+  prm.state = nullptr;
+  prm.state_out = op.state_->data.p;
+  prm.geo = op.geometry_->data.p;
+  prm.load = op.load_.n ? op.load_.p : nullptr;
+  prm.load_scale = op.load_scale_;
+  prm.fail = op.fail_.p;
+  prm.mu = op.mu_;
+  prm.lambda = op.lambda_;
+  for (size_t i = 0; i < op.interp_.size(); ++i) prm.B[i] = op.interp_[i];
+  for (size_t i = 0; i < op.deriv_.size(); ++i) prm.Bd[i] = op.deriv_[i];
+  dispatch_pq(op.p_, op.q_, [&](auto Pc, auto Qc) {
+    constexpr int P = decltype(Pc)::value, Q = decltype(Qc)::value;
+    using D = FDims<P, Q>;
+    size_t need = (size_t)op.lay_.num_bricks() * D::NB * 3;
+    if (op.partial_.n != need) op.partial_.alloc(need);
+    prm.partial = op.partial_.p;
+    size_t smem = sizeof(double) * D::SMEM;
+    auto k = fused_jacobian_kernel<P, Q, kStorageCurrent, kResidual>;
+    HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+    prm.brick0 = 0;
+    prm.nbricks = (int)op.lay_.num_bricks();
+    k<<<persistent_grid(k, D::T, smem, prm.nbricks), D::T, smem, op.stream_>>>(prm);
+    HXG_CUDA(cudaGetLastError());
+    fused_fixup_kernel<P, Q, kResidual><<<fixup_grid(prm.nbricks), kFixupThreads, 0, op.stream_>>>(prm);
     HXG_CUDA(cudaGetLastError());
   });
 }
@@ -1072,8 +1154,7 @@ void fused_jacobian_host(Operator& op, const double* xh, double* yh) {
       HXG_CUDA(cudaGetLastError());
       const int zs = i == 0 ? 0 : pb2 * lb;
       const int ze = i == C - 1 ? npz : pb2 * le;
-      const unsigned fg = fixup_rows<P, Q>(pc, zs, ze);
-      if (fg) fused_fixup_kernel<P, Q><<<fg, 128, 0, pp.comp>>>(pc);
+      fused_fixup_kernel<P, Q><<<fixup_grid(pc.nbricks), kFixupThreads, 0, pp.comp>>>(pc);
       HXG_CUDA(cudaGetLastError());
       HXG_CUDA(cudaEventRecord(pp.out_ready[i], pp.comp));
       HXG_CUDA(cudaStreamWaitEvent(pp.d2h, pp.out_ready[i], 0));

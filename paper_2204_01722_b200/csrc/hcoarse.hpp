@@ -1,0 +1,72 @@
+// Inexact coarse mode (SURVEY.md §7.2 hard part 3): the p = 1 coarse level of
+// the p-multigrid hierarchy is solved by ONE geometric h-multigrid V-cycle
+// instead of the reference's exact SimplicialLLT solve (coarse_solver.hpp:
+// 16-47, called from multigrid.hpp:167-170).  A documented deviation, opt-in
+// (hxg_mg_set_coarse_mode(mg, 4)), reported beside the exact mode.
+//
+// Levels: the assembled Q1 matrix A_0 on the lattice of the fine cells, then
+// Galerkin operators A_{l+1} = P~^T A_l P~ on lattices of ceil(c / 2) cells,
+// P = trilinear interpolation (x I3), P~ = M_f P M_c with constrained rows
+// (fine) and columns (coarse) removed.  A_{l+1} is formed element by element
+// from the level's element matrices (children of a coarse element are its
+// 2 x 2 x 2 fine cells; trilinear interpolation is continuous, so the sum of
+// the element products is the exact triple product) and assembled with the
+// coarse-assembly slot sums.  Smoothing: degree-2 Chebyshev-Jacobi on [0.1,
+// 1.1] lambda_max (the reference's smoother, smoother.hpp:15-63) with
+// lambda_max from 10 Lanczos steps on rough_seed (cg.hpp:138-184), one pre
+// and one post sweep; bottom (<= kHmgBottomMax DoFs): dense Cholesky inverse
+// applied by a fixed-order GEMV.  The cycle is a fixed symmetric linear
+// operator, so the outer PCG stays valid.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "coarse.hpp"
+#include "solver.hpp"
+
+namespace hxg {
+
+constexpr int kHmgBottomMax = 4000;
+
+// Dense SPD inverse (potrf + potri once per setup), applied with a
+// hand-written fixed-order GEMV.
+class DenseInverse {
+ public:
+  ~DenseInverse();
+  void factorize(const CsrMatrix& a, cudaStream_t s);
+  void solve(const double* b, double* x, cudaStream_t s) const;
+  int n() const { return n_; }
+
+ private:
+  void* handle_ = nullptr;  // cusolverDnHandle_t
+  int n_ = 0;
+  DevBuf<double> inv_, work_;
+  DevBuf<int> info_;
+};
+
+class HmgCoarse {
+ public:
+  HmgCoarse();
+  ~HmgCoarse();
+  // a0: assembled Q1 matrix on box0 (order 1) with constraint mask0 (host,
+  // empty = none); elem0: its element matrices (E x 24 x 24, unmasked, the
+  // CoarseAssembly layout).  Symbolic work (lattices, masks, patterns) on the
+  // first call, numeric work every call.
+  void setup(const CsrMatrix& a0, const BoxDev& box0, const std::vector<uint8_t>& mask0,
+             const double* elem0, cudaStream_t s);
+  // x = V(b): one h-multigrid V-cycle from x = 0.
+  void solve(const double* b, double* x, cudaStream_t s);
+  bool ready() const { return ready_; }
+  int num_levels() const { return (int)levels_.size(); }
+  long long level_size(int l) const;
+
+ private:
+  struct HLevel;
+  void cycle(size_t l, const double* b, double* x, cudaStream_t s);
+  std::vector<std::unique_ptr<HLevel>> levels_;
+  DenseInverse bottom_;
+  bool ready_ = false;
+};
+
+}  // namespace hxg

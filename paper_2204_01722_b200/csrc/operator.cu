@@ -233,7 +233,12 @@ void Operator::apply_residual(const double* u, double* f) {
   ++residual_applies_;
   const unsigned long long none = ~0ull;
   HXG_CUDA(cudaMemcpyAsync(fail_.p, &none, sizeof(none), cudaMemcpyHostToDevice, stream_));
-  launch_element(kResidual, u, false);
+  // one brick pass (state + f) where the fused kernel covers the operator
+  const bool fz = variant_ == 0 && storage_ == kStorageCurrent && fused_supported(p_, q_);
+  if (fz)
+    fused_residual(*this, u, f);
+  else
+    launch_element(kResidual, u, false);
   unsigned long long fail = none;
   HXG_CUDA(cudaMemcpyAsync(&fail, fail_.p, sizeof(fail), cudaMemcpyDeviceToHost, stream_));
   HXG_CUDA(cudaStreamSynchronize(stream_));
@@ -257,7 +262,7 @@ void Operator::apply_residual(const double* u, double* f) {
     throw err;
   }
   state_->valid = true;
-  launch_node_sum(evec_.p, f, nullptr, kEpiResidual);
+  if (!fz) launch_node_sum(evec_.p, f, nullptr, kEpiResidual);
 }
 
 void Operator::apply_jacobian_host(const double* xh, double* yh) {

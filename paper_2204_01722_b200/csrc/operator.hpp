@@ -152,6 +152,7 @@ class Operator {
   void apply_jacobian_host(const double* xh, double* yh);
 
   friend void fused_jacobian(Operator& op, const double* du, double* y);
+  friend void fused_residual(Operator& op, const double* u, double* f);
   friend void fused_jacobian_host(Operator& op, const double* xh, double* yh);
 
  private:

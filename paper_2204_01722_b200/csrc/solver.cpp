@@ -1,5 +1,7 @@
 #include "solver.hpp"
 
+#include "hcoarse.hpp"
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -434,6 +436,10 @@ void Hierarchy::setup_numeric() {
   pt.mark("coarse assembly");
   if (part_) {
     dist_coarse_numeric();
+  } else if (coarse_mode_ == 4) {
+    if (!hmg_) hmg_ = std::make_unique<HmgCoarse>();
+    hmg_->setup(assembly_->matrix(), level(0).op->box(), level(0).op->mask_host(),
+                assembly_->element_matrices(), s);
   } else {
     coarse_.set_mode(coarse_mode_);
     coarse_.factorize(assembly_->matrix(), level(0).op->box().npd, s);
@@ -551,6 +557,8 @@ void Hierarchy::coarse_solve(const double* b, double* x) {
   follow_stream();
   if (part_)
     dist_coarse_solve(b, x);
+  else if (coarse_mode_ == 4 && hmg_ && hmg_->ready())
+    hmg_->solve(b, x, stream());
   else
     coarse_.solve(b, x, stream());
 }

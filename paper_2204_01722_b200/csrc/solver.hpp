@@ -99,8 +99,11 @@ class Hierarchy {
     if (!assembly_) throw Error(HXG_ERR_STATE_NOT_INITIALIZED, "coarse operator not assembled");
     return assembly_->matrix();
   }
-  // 0 automatic (dense below kDenseCoarseMax DoFs), 1 dense, 2 sparse ND.
+  // 0 automatic (dense below kDenseCoarseMax DoFs), 1 dense, 2 sparse ND,
+  // 3 csrchol, 4 inexact: one Galerkin h-multigrid V-cycle (hcoarse.hpp).
   void set_coarse_mode(int m) { coarse_mode_ = m; }
+  int coarse_mode() const { return coarse_mode_; }
+  const class HmgCoarse* hmg() const { return hmg_.get(); }
   cudaStream_t stream() const { return levels_.back()->op->stream(); }
   // The level operators follow the fine operator's stream: a caller may
   // hxg_op_set_stream the fine operator after the hierarchy is built, and
@@ -117,6 +120,7 @@ class Hierarchy {
   std::vector<std::unique_ptr<Level>> levels_;
   std::unique_ptr<CoarseAssembly> assembly_;
   CoarseSolver coarse_;
+  std::unique_ptr<class HmgCoarse> hmg_;
   int pre_ = 1, post_ = 1, degree_ = 2, coarse_mode_ = 0;
   Partition* part_ = nullptr;
   int global_faces_ = 0;

@@ -342,8 +342,9 @@ class MultigridHierarchy:
         check(lib().hxg_mg_assemble_coarse(self.h))
 
     def set_coarse_mode(self, mode):
-        """0 automatic, 1 dense, 2 nested-dissection multifrontal, 3 cuSOLVER csrchol."""
-        mode = {"auto": 0, "dense": 1, "sparse": 2, "nd": 2, "csrchol": 3}.get(mode, mode)
+        """0 automatic, 1 dense, 2 nested-dissection multifrontal, 3 cuSOLVER csrchol,
+        4 ("hmg") inexact: one Galerkin h-multigrid V-cycle on the p = 1 level."""
+        mode = {"auto": 0, "dense": 1, "sparse": 2, "nd": 2, "csrchol": 3, "hmg": 4}.get(mode, mode)
         check(lib().hxg_mg_set_coarse_mode(self.h, int(mode)))
 
     def lambda_max(self, k):

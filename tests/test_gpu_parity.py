@@ -297,20 +297,17 @@ def test_newton_line_search_quirk_reproduces_reference():
 
 
 def test_distributed_newton_single_rank_matches_library():
-    """The slab-partitioned Newton driver (distributed.py) over the GPU slab
-    backend at world size 1 reproduces the library's Newton (same iterations,
-    same solution) on the compressed bar."""
-    from paper_2204_01722_b200.distributed import DistributedHierarchy, SlabBackend, SlabComm, \
-        distributed_solve
-    from paper_2204_01722_b200.hexmg import FemProblem, constraint_mask
+    """The partitioned Newton driver (hxg_mg_create_partitioned, built-in
+    NCCL communicator) at world size 1 reproduces the library's Newton (same
+    iterations, same solution) on the compressed bar."""
+    from paper_2204_01722_b200.distributed import Communicator, PartitionedProblem
+    from paper_2204_01722_b200.hexmg import FemProblem
     cells = (4, 2, 2)
-    kw = dict(extents=(2, 1, 1), cells=cells, order=2, fixed_faces=("-x",), traction_face="+x",
+    kw = dict(extents=(2, 1, 1), order=2, fixed_faces=("-x",), traction_face="+x",
               traction=(-0.05, 0, 0))
-    ref = FemProblem(**kw).solve(load_steps=2)
-    prob = FemProblem(**kw)
-    hier = DistributedHierarchy(SlabBackend(prob, ("-x",)), SlabComm(), cells, 0,
-                                lambda p: constraint_mask(cells, p, ("-x",))[0])
-    rep = distributed_solve(hier, load_steps=2)
+    ref = FemProblem(cells=cells, geometry="box", **kw).solve(load_steps=2)
+    pp = PartitionedProblem(Communicator(0, 1, None, backend="nccl"), cells, (1, 1, 1), **kw)
+    rep = pp.solve(load_steps=2)
     assert rep["newton_iterations"] == ref["newton_iterations"]
     assert abs(rep["cg_iterations"] - ref["cg_iterations"]) <= rep["newton_iterations"]
     assert rel(rep["u"], ref["u"].cpu().numpy()) < 1e-9
