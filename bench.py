@@ -202,9 +202,11 @@ def make_comm(rank, world, dist, backend):
     return Communicator(rank, world, dist, backend="nccl" if backend == "nccl" else "gloo")
 
 
-def run_distributed_pmg(rank, world, dist, stream, comm):
+def run_distributed_pmg(rank, world, dist, stream, comm, mode="auto"):
     """Strong scaling of the cfg4 beam: the partitioned p-MG of the C++
-    library (hxg_mg_create_partitioned), slabs along x."""
+    library (hxg_mg_create_partitioned), slabs along x.  mode "auto": the
+    exact coarse solve (global Q1 matrix replicated); "hmg": the inexact
+    coarse mode, its h-levels distributed with the slabs."""
     import torch
 
     from paper_2204_01722_b200.distributed import PartitionedProblem
@@ -213,6 +215,7 @@ def run_distributed_pmg(rank, world, dist, stream, comm):
     pp = PartitionedProblem(comm, cells, (world, 1, 1), order=order, extents=ext,
                             fixed_faces=("-x",), traction_face="+x", traction=(-0.02, 0.0, 0.0),
                             geometry="box")
+    pp.set_coarse_mode(mode)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     torch.cuda.synchronize()
     ev[0].record(stream)
@@ -254,8 +257,10 @@ def run_distributed_pmg(rank, world, dist, stream, comm):
            "newton_cg_iterations": nrep["cg_iterations"], "newton_final_fnorm": nrep["final_fnorm"],
            "path": "hxg_mg_create_partitioned (C++ library: interface sums, owned dots, "
                    "partitioned transfers, Newton) over the library's communicator",
-           "coarse": "global Q1 matrix summed over the blocks (one all-reduce per setup), "
-                     "replicated device Cholesky",
+           "coarse": "exact: global Q1 matrix summed over the blocks (one all-reduce per setup), "
+                     "replicated device Cholesky" if mode == "auto" else
+                     "inexact: one Galerkin h-multigrid V-cycle, h-levels distributed with the "
+                     "slabs (interface sums, owned dots), replicated dense bottom",
            "timing": "device events, max over ranks"}
     del pp
     torch.cuda.empty_cache()
@@ -458,21 +463,25 @@ def run_ours(args, rank, world, local_rank):
     # numeric setup (diagonals, Chebyshev lambda_max, coarse assembly +
     # nested-dissection Cholesky), PCG to the reference's linear_rtol = 1e-3
     # (nonlinear.hpp:20), device-timed.
-    newton = None
-    pmg = []
+    newton = newton_inexact = None
+    pmg, pmg_inexact = [], []
     if world == 1 and not args.no_newton:
         from paper_2204_01722_b200.hexmg import cg_solve
 
-        def pmg_case(order, cells, newton_step):
+        def pmg_case(order, cells, newton_step, mode="auto"):
             """p-MG on the cube (fixed -x, traction (0,0,-0.02) on +x, u = 0):
             residual (state), setup_numeric (diagonals, Chebyshev lambda_max,
-            coarse assembly + nested-dissection Cholesky), PCG; device-timed."""
+            coarse assembly + coarse factorization), PCG; device-timed.
+            mode "auto": the reference's exact coarse solve (nested-dissection
+            Cholesky); "hmg": the inexact coarse mode (one Galerkin h-multigrid
+            V-cycle on the p = 1 level, a documented deviation)."""
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
             prob_n = FemProblem(extents=(1.0, 1.0, 1.0), cells=(cells,) * 3, order=order,
                                 fixed_faces=("-x",), traction_face="+x",
                                 traction=(0.0, 0.0, -0.02))
             un = torch.zeros(prob_n.size(), dtype=torch.float64, device="cuda")
             mg = prob_n.hierarchy
+            mg.set_coarse_mode(mode)
             prob_n.op.apply_residual(un)
             # warm-up pass of the timed sequence: symbolic analysis, library
             # workspaces and the torch allocations of these calls
@@ -520,21 +529,32 @@ def run_ours(args, rank, world, local_rank):
                    "pcg_rtol1e-8_ms": min(evs[3].elapsed_time(evs[4]), ev8[0].elapsed_time(ev8[1])),
                    "pcg_rtol1e-8_iterations": rep8["iterations"],
                    "vcycle_ms": ev_v[0].elapsed_time(ev_v[1]) / 5,
-                   "condition": rep8["eig_max"] / rep8["eig_min"]}
+                   "condition": rep8["eig_max"] / rep8["eig_min"],
+                   "coarse_mode": "exact (nested-dissection Cholesky)" if mode == "auto"
+                   else "inexact (one Galerkin h-multigrid V-cycle)"}
             del prob_n, mg
             torch.cuda.empty_cache()
             return out
 
         # BASELINE.json configs[1]: single Newton-Krylov step at Q2 64^3
         # (linear_rtol = 1e-3, nonlinear.hpp:20); configs[2]: Q3 / Q4 p-MG.
+        def nk_step(nk, solver):
+            return {"config": nk["config"] + ", fixed -x, traction (0,0,-0.02) on +x, u = 0",
+                    "step_ms": nk["residual_ms"] + nk["setup_numeric_ms"] + nk["pcg_rtol1e-3_ms"],
+                    "residual_ms": nk["residual_ms"], "setup_numeric_ms": nk["setup_numeric_ms"],
+                    "pcg_ms": nk["pcg_rtol1e-3_ms"], "cg_iterations": nk["pcg_rtol1e-3_iterations"],
+                    "linear_rtol": 1e-3, "coarse_solver": solver}
+
         nk = pmg_case(ORDER, CELLS, True)
-        newton = {"config": nk["config"] + ", fixed -x, traction (0,0,-0.02) on +x, u = 0",
-                  "step_ms": nk["residual_ms"] + nk["setup_numeric_ms"] + nk["pcg_rtol1e-3_ms"],
-                  "residual_ms": nk["residual_ms"], "setup_numeric_ms": nk["setup_numeric_ms"],
-                  "pcg_ms": nk["pcg_rtol1e-3_ms"], "cg_iterations": nk["pcg_rtol1e-3_iterations"],
-                  "linear_rtol": 1e-3,
-                  "coarse_solver": "nested-dissection multifrontal Cholesky (device, inverse-panel solve)"}
+        newton = nk_step(nk, "exact: nested-dissection multifrontal Cholesky (device, "
+                             "inverse-panel solve)")
         pmg = [nk] + [pmg_case(o, c, False) for o, c in ((3, 43), (4, 32))]
+        # the inexact coarse mode beside the exact one (SURVEY.md §7.2 hard
+        # part 3): same problems, coarse level = one h-multigrid V-cycle
+        nki = pmg_case(ORDER, CELLS, True, "hmg")
+        newton_inexact = nk_step(nki, "inexact: one Galerkin h-multigrid V-cycle on the p = 1 "
+                                      "level (Chebyshev-Jacobi, dense-inverse bottom)")
+        pmg_inexact = [nki] + [pmg_case(o, c, False, "hmg") for o, c in ((3, 43), (4, 32))]
 
     # Full Newton solve of the compressed beam (BASELINE.json configs[3] on one
     # GPU): FemProblem::solve with load continuation (1 step), critical-point
@@ -558,14 +578,31 @@ def run_ours(args, rank, world, local_rank):
                        "note": "includes the symbolic (first) p-MG setup"}
         del prob_b, rep_b
         torch.cuda.empty_cache()
+        # the same solve with the inexact coarse mode
+        prob_b = FemProblem(extents=(2.0, 1.0, 1.0), cells=(96, 48, 48), order=2,
+                            fixed_faces=("-x",), traction_face="+x", traction=(-0.02, 0.0, 0.0))
+        prob_b.hierarchy.set_coarse_mode("hmg")
+        torch.cuda.synchronize()
+        eb[0].record(stream)
+        rep_b = prob_b.solve(load_steps=1)
+        eb[1].record(stream)
+        torch.cuda.synchronize()
+        newton_full["inexact_coarse"] = {
+            "solve_ms": eb[0].elapsed_time(eb[1]), "newton_iterations": rep_b["newton_iterations"],
+            "cg_iterations": rep_b["cg_iterations"], "final_fnorm": rep_b["final_fnorm"],
+            "converged": rep_b["converged"],
+            "coarse_solver": "one Galerkin h-multigrid V-cycle on the p = 1 level"}
+        del prob_b, rep_b
+        torch.cuda.empty_cache()
 
     # Slab-partitioned p-MG PCG on the compressed beam (BASELINE.json
     # configs[3]: Q2, 96 x 48 x 48 cells over N GPUs, strong scaling; halo
-    # exchange over NCCL, replicated coarse Cholesky), device-timed, max over
-    # ranks.
-    pmg_dist = None
+    # exchange over NCCL), device-timed, max over ranks: exact coarse mode
+    # (replicated Cholesky) and the inexact mode (distributed h-levels).
+    pmg_dist = pmg_dist_inexact = None
     if not args.no_newton:
         pmg_dist = run_distributed_pmg(rank, world, dist, stream, comm)
+        pmg_dist_inexact = run_distributed_pmg(rank, world, dist, stream, comm, "hmg")
 
     # CPU baseline: the reference on the host cores, rank 0, N = 1 only.
     cpu = None
@@ -633,8 +670,11 @@ def run_ours(args, rank, world, local_rank):
             "cpu_baseline": cpu,
             "cpu_pmg": cpu_pmg,
             "newton_krylov_step": newton,
+            "newton_krylov_step_inexact": newton_inexact,
             "pmg_solves": pmg,
+            "pmg_solves_inexact": pmg_inexact,
             "pmg_distributed": pmg_dist,
+            "pmg_distributed_inexact": pmg_dist_inexact,
             "newton_solve": newton_full,
             "apply_cfg5": cfg5,
             "storage_variants": storage_table,

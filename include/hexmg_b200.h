@@ -187,6 +187,14 @@ int hxg_mg_coarse_nnz(hxg_mg_t mg, int64_t* nnz);
  * hxg_mg_coarse_csr_host), no host round trip. */
 int hxg_mg_coarse_vals_device(hxg_mg_t mg, double* vals_dev);
 int hxg_mg_coarse_csr_host(hxg_mg_t mg, int* row_ptr, int* cols, double* vals);
+/* Inexact coarse mode (4): number of h-multigrid levels after the last
+ * setup_numeric (0 when the mode is not active), and level l's Galerkin
+ * matrix (CSR, sorted columns; l = 0 is the p = 1 level) with its constraint
+ * mask (n bytes) -- for inspection and tests. */
+int hxg_mg_hmg_levels(hxg_mg_t mg, int* levels);
+int hxg_mg_hmg_level_nnz(hxg_mg_t mg, int level, int64_t* n, int64_t* nnz);
+int hxg_mg_hmg_level_csr_host(hxg_mg_t mg, int level, int* row_ptr, int* cols, double* vals,
+                              uint8_t* mask);
 /* Coarse Cholesky solve (coarse_solver.hpp:35-40). */
 int hxg_mg_coarse_solve(hxg_mg_t mg, const double* b, double* x);
 

@@ -152,6 +152,9 @@ SIGNATURES = {
     "hxg_mg_smooth": [_vp, _i, _vp, _vp],
     "hxg_mg_coarse_nnz": [_vp, _P(_i64)],
     "hxg_mg_coarse_csr_host": [_vp, _vp, _vp, _vp],
+    "hxg_mg_hmg_levels": [_vp, _P(_i)],
+    "hxg_mg_hmg_level_nnz": [_vp, _i, _P(_i64), _P(_i64)],
+    "hxg_mg_hmg_level_csr_host": [_vp, _i, _vp, _vp, _vp, _vp],
     "hxg_mg_coarse_solve": [_vp, _vp, _vp],
     "hxg_mg_assemble_coarse": [_vp],
     "hxg_chol_create": [_i, _vp, _vp, _vp, _i, _vp],

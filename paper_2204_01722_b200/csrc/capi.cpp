@@ -13,6 +13,7 @@
 #include "operator.hpp"
 #include "setup.hpp"
 #include "solver.hpp"
+#include "hcoarse.hpp"
 #include "vector.hpp"
 
 struct hxg_state_s {
@@ -340,6 +341,37 @@ int hxg_mg_coarse_csr_host(hxg_mg_t mg, int* row_ptr, int* cols, double* vals) {
     const auto& a = MG(mg).coarse_matrix();
     std::memcpy(row_ptr, a.row_ptr_h.data(), sizeof(int) * a.row_ptr_h.size());
     std::memcpy(cols, a.cols_h.data(), sizeof(int) * a.cols_h.size());
+    cudaStream_t s = MG(mg).stream();
+    HXG_CUDA(cudaMemcpyAsync(vals, a.vals.p, sizeof(double) * a.cols_h.size(),
+                             cudaMemcpyDeviceToHost, s));
+    HXG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+int hxg_mg_hmg_levels(hxg_mg_t mg, int* levels) {
+  return guarded([&] {
+    const hxg::HmgCoarse* h = MG(mg).hmg();
+    *levels = h && h->ready() ? h->num_levels() : 0;
+  });
+}
+int hxg_mg_hmg_level_nnz(hxg_mg_t mg, int level, int64_t* n, int64_t* nnz) {
+  return guarded([&] {
+    const hxg::HmgCoarse* h = MG(mg).hmg();
+    if (!h || !h->ready() || level < 0 || level >= h->num_levels())
+      throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "no such h-multigrid level");
+    *n = h->level_matrix(level).n;
+    *nnz = h->level_matrix(level).nnz();
+  });
+}
+int hxg_mg_hmg_level_csr_host(hxg_mg_t mg, int level, int* row_ptr, int* cols, double* vals,
+                              uint8_t* mask) {
+  return guarded([&] {
+    const hxg::HmgCoarse* h = MG(mg).hmg();
+    if (!h || !h->ready() || level < 0 || level >= h->num_levels())
+      throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "no such h-multigrid level");
+    const auto& a = h->level_matrix(level);
+    std::memcpy(row_ptr, a.row_ptr_h.data(), sizeof(int) * a.row_ptr_h.size());
+    std::memcpy(cols, a.cols_h.data(), sizeof(int) * a.cols_h.size());
+    std::memcpy(mask, h->level_mask(level).data(), h->level_mask(level).size());
     cudaStream_t s = MG(mg).stream();
     HXG_CUDA(cudaMemcpyAsync(vals, a.vals.p, sizeof(double) * a.cols_h.size(),
                              cudaMemcpyDeviceToHost, s));

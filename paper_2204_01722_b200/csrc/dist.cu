@@ -126,12 +126,17 @@ __global__ void pack_plane(const double* __restrict__ y, int d, int i, int nx, i
     buf[t] = y[plane_dof(d, i, t, nx, ny)];
 }
 
-// plane = own + received (a + b == b + a bitwise: both sides agree)
+// plane = own + received (a + b == b + a bitwise: both sides agree);
+// with a mask, constrained entries are the identity row's x instead of a sum
+// (operator.hpp:212-214 on every block holding them).
 __global__ void add_plane(double* __restrict__ y, int d, int i, int nx, int ny, long long count,
-                          const double* __restrict__ own, const double* __restrict__ recv) {
+                          const double* __restrict__ own, const double* __restrict__ recv,
+                          const double* __restrict__ x, const uint8_t* __restrict__ mask) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < count;
-       t += (long long)gridDim.x * blockDim.x)
-    y[plane_dof(d, i, t, nx, ny)] = own[t] + recv[t];
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long dof = plane_dof(d, i, t, nx, ny);
+    y[dof] = mask && mask[dof] ? x[dof] : own[t] + recv[t];
+  }
 }
 
 __global__ void scale_plane(double* __restrict__ y, int d, int i, int nx, int ny, long long count,
@@ -217,10 +222,37 @@ void Partition::global_npd(int p, int out[3]) const {
   for (int d = 0; d < 3; ++d) out[d] = p * gcells_[d] + 1;
 }
 
-void Partition::exchange(int p, double* y, cudaStream_t s) {
+Lattice Partition::lattice(int p) const {
+  Lattice L;
+  for (int d = 0; d < 3; ++d) {
+    L.n[d] = p * cells_[d] + 1;
+    L.g[d] = p * gcells_[d] + 1;
+    L.off[d] = (long long)p * e0_[d];
+  }
+  return L;
+}
+
+Lattice Partition::h_lattice(int l) const {
+  Lattice L;
+  const int f = 1 << l;
+  for (int d = 0; d < 3; ++d) {
+    if (cells_[d] % f || e0_[d] % f || gcells_[d] % f)
+      throw Error(HXG_ERR_INVALID_ARGUMENT, "h-lattice: block not aligned to the coarsening");
+    L.n[d] = cells_[d] / f + 1;
+    L.g[d] = gcells_[d] / f + 1;
+    L.off[d] = e0_[d] / f;
+  }
+  return L;
+}
+
+void Partition::exchange(int p, double* y, cudaStream_t s, const double* x, const uint8_t* mask) {
+  exchange(lattice(p), y, s, x, mask);
+}
+
+void Partition::exchange(const Lattice& L, double* y, cudaStream_t s, const double* x,
+                         const uint8_t* mask) {
   if (comm_->world() == 1) return;
-  int n[3];
-  npd(p, n);
+  const int* n = L.n;
   for (int d = 0; d < 3; ++d) {
     const int lo = neighbour(d, -1), hi = neighbour(d, +1);
     if (lo < 0 && hi < 0) continue;
@@ -243,17 +275,21 @@ void Partition::exchange(int p, double* y, cudaStream_t s) {
     HXG_CUDA(cudaGetLastError());
     comm_->exchange(np, peers, send, recv, counts, s);
     if (lo >= 0)
-      add_plane<<<grid_for_count(count), 256, 0, s>>>(y, d, 0, n[0], n[1], count, buf_[0].p, buf_[2].p);
+      add_plane<<<grid_for_count(count), 256, 0, s>>>(y, d, 0, n[0], n[1], count, buf_[0].p, buf_[2].p,
+                                                      x, mask);
     if (hi >= 0)
       add_plane<<<grid_for_count(count), 256, 0, s>>>(y, d, n[d] - 1, n[0], n[1], count, buf_[1].p,
-                                                      buf_[3].p);
+                                                      buf_[3].p, x, mask);
     HXG_CUDA(cudaGetLastError());
   }
 }
 
 void Partition::scale_interfaces(int p, double* y, double f, cudaStream_t s) {
-  int n[3];
-  npd(p, n);
+  scale_interfaces(lattice(p), y, f, s);
+}
+
+void Partition::scale_interfaces(const Lattice& L, double* y, double f, cudaStream_t s) {
+  const int* n = L.n;
   for (int d = 0; d < 3; ++d) {
     const long long count = 3LL * n[0] * n[1] * n[2] / n[d];
     if (neighbour(d, -1) >= 0)
@@ -264,15 +300,16 @@ void Partition::scale_interfaces(int p, double* y, double f, cudaStream_t s) {
   HXG_CUDA(cudaGetLastError());
 }
 
-const uint8_t* Partition::owned(int p) {
-  auto it = owned_.find(p);
+const uint8_t* Partition::owned(int p) { return owned(lattice(p)); }
+
+const uint8_t* Partition::owned(const Lattice& L) {
+  const std::vector<int> key{L.n[0], L.n[1], L.n[2]};
+  auto it = owned_.find(key);
   if (it != owned_.end()) return it->second.p;
-  int n[3];
-  npd(p, n);
-  DevBuf<uint8_t>& m = owned_[p];
-  const long long total = 3LL * n[0] * n[1] * n[2];
+  DevBuf<uint8_t>& m = owned_[key];
+  const long long total = L.size();
   m.alloc((size_t)total);
-  owned_kernel<<<grid_for_count(total), 256>>>(m.p, n[0], n[1], n[2], neighbour(0, -1) >= 0,
+  owned_kernel<<<grid_for_count(total), 256>>>(m.p, L.n[0], L.n[1], L.n[2], neighbour(0, -1) >= 0,
                                                neighbour(1, -1) >= 0, neighbour(2, -1) >= 0);
   HXG_CUDA(cudaGetLastError());
   HXG_CUDA(cudaDeviceSynchronize());
@@ -280,11 +317,12 @@ const uint8_t* Partition::owned(int p) {
 }
 
 double Partition::dot(int p, const double* x, const double* y, cudaStream_t s) {
-  int n[3];
-  npd(p, n);
-  const long long total = 3LL * n[0] * n[1] * n[2];
-  const uint8_t* m = comm_->world() > 1 ? owned(p) : nullptr;
-  double* r = dot_masked_device(x, y, m, total, ws_, 0, s);
+  return dot(lattice(p), x, y, s);
+}
+
+double Partition::dot(const Lattice& L, const double* x, const double* y, cudaStream_t s) {
+  const uint8_t* m = comm_->world() > 1 ? owned(L) : nullptr;
+  double* r = dot_masked_device(x, y, m, L.size(), ws_, 0, s);
   comm_->allreduce(r, 1, 0, s);
   HXG_CUDA(cudaMemcpyAsync(host_, r, sizeof(double), cudaMemcpyDeviceToHost, s));
   HXG_CUDA(cudaStreamSynchronize(s));
@@ -302,10 +340,14 @@ double Partition::allreduce_max(double v, cudaStream_t s) {
 }
 
 std::vector<double> Partition::global_seed_slice(int p, const std::vector<uint8_t>& mask) const {
-  int n[3], g[3];
-  npd(p, n);
-  global_npd(p, g);
-  const long long x0 = (long long)p * e0_[0], y0 = (long long)p * e0_[1], z0 = (long long)p * e0_[2];
+  return global_seed_slice(lattice(p), mask);
+}
+
+std::vector<double> Partition::global_seed_slice(const Lattice& L,
+                                                 const std::vector<uint8_t>& mask) const {
+  const int* n = L.n;
+  const int* g = L.g;
+  const long long x0 = L.off[0], y0 = L.off[1], z0 = L.off[2];
   std::vector<double> v(3 * (size_t)n[0] * n[1] * n[2]);
   std::mt19937 rng(0x9e3779b9u);
   long long pos = 0;  // global entries consumed so far

@@ -54,6 +54,17 @@ class Comm {
 std::unique_ptr<Comm> make_nccl_comm(int rank, int world, const void* unique_id);
 void nccl_unique_id(void* out128);
 
+// A node lattice of the partitioned box as this rank sees it: local nodes
+// per direction, global nodes per direction, global index of local node 0.
+// Order-p lattices: n = p cells + 1; h-multigrid levels of the p = 1 lattice
+// (coarsened by 2^l): n = cells / 2^l + 1.
+struct Lattice {
+  int n[3] = {1, 1, 1};
+  int g[3] = {1, 1, 1};
+  long long off[3] = {0, 0, 0};
+  long long size() const { return 3LL * n[0] * n[1] * n[2]; }
+};
+
 class Partition {
  public:
   // gcells: the whole box; dims: blocks per direction (rank = x fastest).
@@ -75,8 +86,10 @@ class Partition {
   int local_faces(int global_faces) const;
 
   // y (local L-vector of an order-p lattice) += the neighbours' partial sums
-  // on the shared planes (x, y, z passes).
-  void exchange(int p, double* y, cudaStream_t s);
+  // on the shared planes (x, y, z passes).  With mask (device), constrained
+  // entries on the shared planes become x instead (identity rows).
+  void exchange(int p, double* y, cudaStream_t s, const double* x = nullptr,
+                const uint8_t* mask = nullptr);
   // y *= f on every shared plane (once per shared direction: a node on k
   // partition planes gets f^k), the multiplicity correction of the transfers.
   void scale_interfaces(int p, double* y, double f, cudaStream_t s);
@@ -93,10 +106,22 @@ class Partition {
   void npd(int p, int out[3]) const;
   void global_npd(int p, int out[3]) const;
 
+  // The same operations on an explicit lattice (the p-variants call these).
+  Lattice lattice(int p) const;
+  // h-level l of the p = 1 lattice; requires 2^l | the block's cells and
+  // offsets (checked).
+  Lattice h_lattice(int l) const;
+  void exchange(const Lattice& L, double* y, cudaStream_t s, const double* x = nullptr,
+                const uint8_t* mask = nullptr);
+  void scale_interfaces(const Lattice& L, double* y, double f, cudaStream_t s);
+  const uint8_t* owned(const Lattice& L);
+  double dot(const Lattice& L, const double* x, const double* y, cudaStream_t s);
+  std::vector<double> global_seed_slice(const Lattice& L, const std::vector<uint8_t>& local_mask) const;
+
  private:
   Comm* comm_;
   int gcells_[3], dims_[3], coords_[3], cells_[3], e0_[3];
-  std::map<int, DevBuf<uint8_t>> owned_;
+  std::map<std::vector<int>, DevBuf<uint8_t>> owned_;
   DevBuf<double> buf_[4];  // send lo / hi, recv lo / hi
   DevBuf<double> scalar_;
   double* host_ = nullptr;  // pinned scalar

@@ -202,6 +202,30 @@ __global__ void dense_symv_kernel(int n, const double* __restrict__ a, const dou
   }
 }
 
+__global__ void slots_to_global(const double* __restrict__ lv, const long long* __restrict__ map,
+                                long long n, double* __restrict__ gv) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (map[i] >= 0) gv[map[i]] = lv[i];
+}
+__global__ void ones_at(double* __restrict__ v, const long long* __restrict__ idx, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    v[idx[i]] = 1.0;
+}
+__global__ void owned_to_global(const double* __restrict__ b, const uint8_t* __restrict__ owned,
+                                const long long* __restrict__ map, long long n, double* __restrict__ g) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (!owned || owned[i]) g[map[i]] = b[i];
+}
+__global__ void from_global(const double* __restrict__ g, const long long* __restrict__ map,
+                            long long n, double* __restrict__ x) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = g[map[i]];
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -255,43 +279,144 @@ void DenseInverse::solve(const double* b, double* x, cudaStream_t s) const {
 
 struct HmgCoarse::HLevel {
   BoxDev box;
+  Lattice lat;  // partitioned: this block of the level's global lattice
   std::vector<uint8_t> mask_h;
   DevBuf<uint8_t> mask;
   const CsrMatrix* A = nullptr;
   std::unique_ptr<CoarseAssembly> asmb;  // levels >= 1
   DevBuf<double> elem;                   // levels >= 1: Galerkin element matrices
   DevBuf<double> b, x, r;
+  DevBuf<double> scaled;  // partitioned: interface-scaled residual for the restriction
   Chebyshev smoother;
   long long n() const { return 3 * box.num_nodes(); }
   const uint8_t* m() const { return mask.n ? mask.p : nullptr; }
+};
+
+// The partitioned bottom: global lattice pattern + local -> global slot and
+// DoF maps (built once), summed values (one all-reduce per setup), dense
+// inverse on every rank.
+struct HmgCoarse::Replicated {
+  std::unique_ptr<CoarseAssembly> global;
+  DevBuf<long long> slot_map, dof_map, diag_slots;
+  DevBuf<double> gvec, gsol;
+  DenseInverse inv;
+
+  void symbolic(Partition& part, const Lattice& L, const CsrMatrix& la,
+                const std::vector<uint8_t>& lmask, cudaStream_t s) {
+    int gc[3] = {L.g[0] - 1, L.g[1] - 1, L.g[2] - 1};
+    BoxDev gbox = make_box(gc, 1);
+    const long long gn = 3 * gbox.num_nodes();
+    auto to_global = [&](long long dof) {
+      const long long node = dof / 3;
+      const int c = (int)(dof % 3);
+      const long long ix = node % L.n[0], iy = (node / L.n[0]) % L.n[1],
+                      iz = node / ((long long)L.n[0] * L.n[1]);
+      return 3 * ((ix + L.off[0]) + (long long)L.g[0] * ((iy + L.off[1]) + (long long)L.g[1] * (iz + L.off[2]))) + c;
+    };
+    // global mask: the blocks' masks agree on shared nodes; max-reduce them
+    std::vector<double> gm((size_t)gn, 0.0);
+    for (long long d = 0; d < la.n; ++d) gm[(size_t)to_global(d)] = lmask[(size_t)d];
+    DevBuf<double> gmd;
+    gmd.upload(gm);
+    part.comm().allreduce(gmd.p, gn, 1, s);
+    HXG_CUDA(cudaMemcpyAsync(gm.data(), gmd.p, sizeof(double) * gn, cudaMemcpyDeviceToHost, s));
+    HXG_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint8_t> gmask((size_t)gn);
+    for (long long d = 0; d < gn; ++d) gmask[(size_t)d] = gm[(size_t)d] > 0.5 ? 1 : 0;
+    global = std::make_unique<CoarseAssembly>(gbox, gmask);
+    const CsrMatrix& ga = global->matrix();
+    std::vector<long long> smap(la.cols_h.size(), -1), dmap((size_t)la.n);
+    for (int r = 0; r < la.n; ++r) {
+      const long long gr = to_global(r);
+      dmap[(size_t)r] = gr;
+      if (gmask[(size_t)gr]) continue;  // identity re-imposed globally
+      const int* gb = ga.cols_h.data() + ga.row_ptr_h[(size_t)gr];
+      const int* ge = ga.cols_h.data() + ga.row_ptr_h[(size_t)gr + 1];
+      for (int sl = la.row_ptr_h[(size_t)r]; sl < la.row_ptr_h[(size_t)r + 1]; ++sl) {
+        const long long gcol = to_global(la.cols_h[(size_t)sl]);
+        if (gmask[(size_t)gcol]) continue;
+        const int* it = std::lower_bound(gb, ge, (int)gcol);
+        if (it == ge || *it != (int)gcol)
+          throw Error(HXG_ERR_GENERIC, "h-multigrid bottom: slot outside the global pattern");
+        smap[(size_t)sl] = ga.row_ptr_h[(size_t)gr] + (it - gb);
+      }
+    }
+    std::vector<long long> diag;
+    for (int r = 0; r < ga.n; ++r)
+      if (gmask[(size_t)r]) diag.push_back(ga.row_ptr_h[(size_t)r]);
+    slot_map.upload(smap);
+    dof_map.upload(dmap);
+    if (!diag.empty()) diag_slots.upload(diag);
+    gvec.alloc((size_t)ga.n);
+    gsol.alloc((size_t)ga.n);
+  }
+
+  void numeric(Partition& part, const CsrMatrix& la, cudaStream_t s) {
+    CsrMatrix& ga = global->mutable_matrix();
+    const long long gnnz = ga.nnz(), lnnz = la.nnz();
+    HXG_CUDA(cudaMemsetAsync(ga.vals.p, 0, sizeof(double) * gnnz, s));
+    slots_to_global<<<grid_for(lnnz, 256), 256, 0, s>>>(la.vals.p, slot_map.p, lnnz, ga.vals.p);
+    HXG_CUDA(cudaGetLastError());
+    part.comm().allreduce(ga.vals.p, gnnz, 0, s);
+    if (diag_slots.n)
+      ones_at<<<grid_for((long long)diag_slots.n, 256), 256, 0, s>>>(ga.vals.p, diag_slots.p,
+                                                                    (long long)diag_slots.n);
+    HXG_CUDA(cudaGetLastError());
+    inv.factorize(ga, s);
+  }
+
+  void solve(Partition& part, const Lattice& L, const double* b, double* x, cudaStream_t s) {
+    const long long n = L.size(), gn = (long long)gvec.n;
+    HXG_CUDA(cudaMemsetAsync(gvec.p, 0, sizeof(double) * gn, s));
+    const uint8_t* own = part.comm().world() > 1 ? part.owned(L) : nullptr;
+    owned_to_global<<<grid_for(n, 256), 256, 0, s>>>(b, own, dof_map.p, n, gvec.p);
+    HXG_CUDA(cudaGetLastError());
+    part.comm().allreduce(gvec.p, gn, 0, s);
+    inv.solve(gvec.p, gsol.p, s);
+    from_global<<<grid_for(n, 256), 256, 0, s>>>(gsol.p, dof_map.p, n, x);
+    HXG_CUDA(cudaGetLastError());
+  }
 };
 
 HmgCoarse::HmgCoarse() = default;
 HmgCoarse::~HmgCoarse() = default;
 
 long long HmgCoarse::level_size(int l) const { return levels_[(size_t)l]->n(); }
+const CsrMatrix& HmgCoarse::level_matrix(int l) const { return *levels_[(size_t)l]->A; }
+const std::vector<uint8_t>& HmgCoarse::level_mask(int l) const { return levels_[(size_t)l]->mask_h; }
 
 void HmgCoarse::setup(const CsrMatrix& a0, const BoxDev& box0, const std::vector<uint8_t>& mask0,
-                      const double* elem0, cudaStream_t s) {
+                      const double* elem0, cudaStream_t s, Partition* part) {
   if (box0.p != 1) throw Error(HXG_ERR_UNSUPPORTED, "h-multigrid coarse mode needs the p = 1 level");
-  if (levels_.empty() || levels_[0]->A != &a0) {  // symbolic: lattices, masks, patterns
+  if (levels_.empty() || levels_[0]->A != &a0 || part_ != part) {  // symbolic
     levels_.clear();
+    rep_.reset();
+    part_ = part;
     auto l0 = std::make_unique<HLevel>();
     l0->box = box0;
     l0->mask_h = mask0.empty() ? std::vector<uint8_t>((size_t)(3 * box0.num_nodes()), 0) : mask0;
     l0->mask.upload(l0->mask_h);
     l0->A = &a0;
+    if (part_) l0->lat = part_->h_lattice(0);
     levels_.push_back(std::move(l0));
     for (;;) {
       HLevel& f = *levels_.back();
-      const bool can = f.box.cells[0] >= 2 && f.box.cells[1] >= 2 && f.box.cells[2] >= 2;
-      if (f.n() <= kHmgBottomMax || !can) break;
+      bool can = f.box.cells[0] >= 2 && f.box.cells[1] >= 2 && f.box.cells[2] >= 2;
+      long long global_n = f.n();
+      if (part_) {  // coarsen while every block stays aligned; all ranks agree
+        global_n = 3LL * f.lat.g[0] * f.lat.g[1] * f.lat.g[2];
+        for (int d = 0; d < 3; ++d) can = can && f.box.cells[d] % 2 == 0 && f.lat.off[d] % 2 == 0;
+        can = part_->allreduce_max(can ? 0.0 : 1.0, s) == 0.0;
+      }
+      if (global_n <= kHmgBottomMax || !can) break;
       auto c = std::make_unique<HLevel>();
       int cc[3];
       for (int d = 0; d < 3; ++d) cc[d] = (f.box.cells[d] + 1) / 2;
       c->box = make_box(cc, 1);
+      if (part_) c->lat = part_->h_lattice((int)levels_.size());
       // a coarse DoF is constrained iff every fine DoF it interpolates to is
-      // (its column of P~ is zero)
+      // (its column of P~ is zero); with whole-face constraints the block's
+      // view of the support decides like the global one
       c->mask_h.assign((size_t)c->n(), 1);
       for (long long node = 0; node < c->box.num_nodes(); ++node) {
         const int G[3] = {(int)(node % c->box.npd[0]), (int)((node / c->box.npd[0]) % c->box.npd[1]),
@@ -320,9 +445,20 @@ void HmgCoarse::setup(const CsrMatrix& a0, const BoxDev& box0, const std::vector
       c->x.alloc((size_t)c->n());
       levels_.push_back(std::move(c));
     }
-    if (levels_.back()->n() > 4 * kHmgBottomMax)
+    for (size_t l = 0; l + 1 < levels_.size(); ++l) {
+      levels_[l]->r.alloc((size_t)levels_[l]->n());
+      if (part_) levels_[l]->scaled.alloc((size_t)levels_[l]->n());
+    }
+    if (part_) {
+      HLevel& bl = *levels_.back();
+      rep_ = std::make_unique<Replicated>();
+      rep_->symbolic(*part_, bl.lat, *bl.A, bl.mask_h, s);
+      if (rep_->global->matrix().n > 4 * kHmgBottomMax)
+        throw Error(HXG_ERR_UNSUPPORTED, "h-multigrid coarse mode: bottom level too large (block "
+                                         "cells odd early: use even block sizes)");
+    } else if (levels_.back()->n() > 4 * kHmgBottomMax) {
       throw Error(HXG_ERR_UNSUPPORTED, "h-multigrid coarse mode: bottom level too large (thin box)");
-    for (size_t l = 0; l + 1 < levels_.size(); ++l) levels_[l]->r.alloc((size_t)levels_[l]->n());
+    }
   }
   // numeric: Galerkin element matrices + slot sums, level by level
   for (size_t l = 0; l + 1 < levels_.size(); ++l) {
@@ -338,33 +474,59 @@ void HmgCoarse::setup(const CsrMatrix& a0, const BoxDev& box0, const std::vector
     HLevel& lv = *levels_[l];
     const CsrMatrix* A = lv.A;
     const long long n = lv.n();
+    Partition* part_l = part_;
+    DotFn dotf = [part_l, &lv, s](const double* x, const double* y) { return part_l->dot(lv.lat, x, y, s); };
     lv.smoother.create(
-        n, s, 2, [A, s](const double* x, double* y) { csr_matvec(*A, x, y, s); },
-        [A, n, s](double* d) {
+        n, s, 2, [this, &lv, s](const double* x, double* y) { apply_level(lv, x, y, s); },
+        [this, A, n, s, &lv](double* d) {
           csr_diag_kernel<<<grid_for(n, 256), 256, 0, s>>>((int)n, A->row_ptr.p, A->cols.p, A->vals.p, d);
           HXG_CUDA(cudaGetLastError());
+          if (part_) {  // summed over the blocks; constrained entries stay 1
+            part_->exchange(lv.lat, d, s);
+            vmask_fill(d, 1.0, lv.m(), n, s);
+          }
         },
-        nullptr, [&lv, n]() { return rough_seed(n, lv.mask_h); });
+        part_ ? &dotf : nullptr,
+        [this, &lv, n]() {
+          return part_ ? part_->global_seed_slice(lv.lat, lv.mask_h) : rough_seed(n, lv.mask_h);
+        });
   }
-  bottom_.factorize(*levels_.back()->A, s);
+  if (part_)
+    rep_->numeric(*part_, *levels_.back()->A, s);
+  else
+    bottom_.factorize(*levels_.back()->A, s);
   ready_ = true;
+}
+
+void HmgCoarse::apply_level(HLevel& lv, const double* x, double* y, cudaStream_t s) {
+  csr_matvec(*lv.A, x, y, s);
+  if (part_) part_->exchange(lv.lat, y, s, x, lv.m());  // constrained rows: identity
 }
 
 void HmgCoarse::cycle(size_t l, const double* b, double* x, cudaStream_t s) {
   HLevel& lv = *levels_[l];
   if (l + 1 == levels_.size()) {
-    bottom_.solve(b, x, s);
+    if (part_)
+      rep_->solve(*part_, lv.lat, b, x, s);
+    else
+      bottom_.solve(b, x, s);
     return;
   }
-  const CsrMatrix* A = lv.A;
   const long long n = lv.n();
-  DevOp op = [A, s](const double* xx, double* yy) { csr_matvec(*A, xx, yy, s); };
+  DevOp op = [this, &lv, s](const double* xx, double* yy) { apply_level(lv, xx, yy, s); };
   lv.smoother.apply(op, n, s, b, x, true);
-  csr_matvec(*A, x, lv.r.p, s);
+  apply_level(lv, x, lv.r.p, s);
   vsub_from(lv.r.p, b, n, s);
   HLevel& c = *levels_[l + 1];
-  restrict_kernel<<<grid_for(c.n(), 256), 256, 0, s>>>(lv.box, c.box, lv.m(), c.m(), lv.r.p, c.b.p);
+  const double* rf = lv.r.p;
+  if (part_) {  // shared fine entries are counted once per block: x 1/2 per shared direction
+    vcopy(lv.scaled.p, lv.r.p, n, s);
+    part_->scale_interfaces(lv.lat, lv.scaled.p, 0.5, s);
+    rf = lv.scaled.p;
+  }
+  restrict_kernel<<<grid_for(c.n(), 256), 256, 0, s>>>(lv.box, c.box, lv.m(), c.m(), rf, c.b.p);
   HXG_CUDA(cudaGetLastError());
+  if (part_) part_->exchange(c.lat, c.b.p, s);
   cycle(l + 1, c.b.p, c.x.p, s);
   prolong_add_kernel<<<grid_for(n, 256), 256, 0, s>>>(lv.box, c.box, lv.m(), c.m(), c.x.p, x);
   HXG_CUDA(cudaGetLastError());

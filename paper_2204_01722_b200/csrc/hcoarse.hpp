@@ -17,12 +17,23 @@
 // and one post sweep; bottom (<= kHmgBottomMax DoFs): dense Cholesky inverse
 // applied by a fixed-order GEMV.  The cycle is a fixed symmetric linear
 // operator, so the outer PCG stays valid.
+//
+// Partitioned: every h-level is distributed like the
+// p-levels -- this rank's block of each lattice (the Galerkin element
+// products are block-local while the block's cells stay even), level
+// operator = local CSR product + interface sums (constrained rows identity),
+// owned-entry dots, global rough_seed slices, restriction = x 1/2 on the
+// shared fine planes, local, interface sum; prolongation local (consistent).
+// Only the bottom (<= kHmgBottomMax DoFs globally, or where a block's cells
+// turn odd) is replicated: its matrix summed over the blocks once per setup
+// (one all-reduce), its right-hand side once per cycle.
 #pragma once
 
 #include <memory>
 #include <vector>
 
 #include "coarse.hpp"
+#include "dist.hpp"
 #include "solver.hpp"
 
 namespace hxg {
@@ -53,19 +64,28 @@ class HmgCoarse {
   // empty = none); elem0: its element matrices (E x 24 x 24, unmasked, the
   // CoarseAssembly layout).  Symbolic work (lattices, masks, patterns) on the
   // first call, numeric work every call.
+  // part: null for one process; else box0 / mask0 / a0 / elem0 are this
+  // rank's block of the p = 1 level.
   void setup(const CsrMatrix& a0, const BoxDev& box0, const std::vector<uint8_t>& mask0,
-             const double* elem0, cudaStream_t s);
+             const double* elem0, cudaStream_t s, Partition* part = nullptr);
   // x = V(b): one h-multigrid V-cycle from x = 0.
   void solve(const double* b, double* x, cudaStream_t s);
   bool ready() const { return ready_; }
   int num_levels() const { return (int)levels_.size(); }
   long long level_size(int l) const;
+  // Level l's assembled matrix (l = 0: the p = 1 level it was set up on).
+  const CsrMatrix& level_matrix(int l) const;
+  const std::vector<uint8_t>& level_mask(int l) const;
 
  private:
   struct HLevel;
+  struct Replicated;
   void cycle(size_t l, const double* b, double* x, cudaStream_t s);
+  void apply_level(HLevel& lv, const double* x, double* y, cudaStream_t s);
   std::vector<std::unique_ptr<HLevel>> levels_;
   DenseInverse bottom_;
+  std::unique_ptr<Replicated> rep_;  // partitioned bottom
+  Partition* part_ = nullptr;
   bool ready_ = false;
 };
 

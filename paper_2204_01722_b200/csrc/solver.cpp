@@ -360,12 +360,10 @@ Hierarchy::~Hierarchy() = default;
 void Hierarchy::level_apply(int k, const double* x, double* y) {
   Level& lv = level(k);
   lv.op->apply_jacobian(x, y);
-  if (part_) {
-    part_->exchange(lv.order, y, stream());
-    // constrained rows are the identity on every block holding them, not
-    // summed (operator.hpp:212-214)
-    vmask_copy(y, x, lv.op->mask(), lv.op->size(), stream());
-  }
+  // constrained rows are the identity on every block holding them, not
+  // summed (operator.hpp:212-214): the interface sum keeps x there (only
+  // shared-plane entries were summed; one rank: nothing to exchange)
+  if (part_) part_->exchange(lv.order, y, stream(), x, lv.op->mask());
 }
 
 double Hierarchy::level_dot(int k, const double* x, const double* y) {
@@ -434,12 +432,12 @@ void Hierarchy::setup_numeric() {
   if (!assembly_) assembly_ = std::make_unique<CoarseAssembly>(*level(0).op);
   assembly_->numeric(*level(0).op);
   pt.mark("coarse assembly");
-  if (part_) {
-    dist_coarse_numeric();
-  } else if (coarse_mode_ == 4) {
+  if (coarse_mode_ == 4) {  // inexact: h-multigrid (distributed with the hierarchy)
     if (!hmg_) hmg_ = std::make_unique<HmgCoarse>();
     hmg_->setup(assembly_->matrix(), level(0).op->box(), level(0).op->mask_host(),
-                assembly_->element_matrices(), s);
+                assembly_->element_matrices(), s, part_);
+  } else if (part_) {
+    dist_coarse_numeric();
   } else {
     coarse_.set_mode(coarse_mode_);
     coarse_.factorize(assembly_->matrix(), level(0).op->box().npd, s);
@@ -555,10 +553,10 @@ void Hierarchy::restrict_to(int coarse_level, const double* xf, double* xc) {
 
 void Hierarchy::coarse_solve(const double* b, double* x) {
   follow_stream();
-  if (part_)
-    dist_coarse_solve(b, x);
-  else if (coarse_mode_ == 4 && hmg_ && hmg_->ready())
+  if (coarse_mode_ == 4 && hmg_ && hmg_->ready())
     hmg_->solve(b, x, stream());
+  else if (part_)
+    dist_coarse_solve(b, x);
   else
     coarse_.solve(b, x, stream());
 }

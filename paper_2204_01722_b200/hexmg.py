@@ -385,6 +385,24 @@ class MultigridHierarchy:
         check(lib().hxg_mg_coarse_csr_host(self.h, _ptr(rp), _ptr(cols), _ptr(vals)))
         return rp, cols, vals
 
+    def hmg_levels(self):
+        """Number of h-multigrid levels of the inexact coarse mode (0 if inactive)."""
+        k = ctypes.c_int()
+        check(lib().hxg_mg_hmg_levels(self.h, ctypes.byref(k)))
+        return k.value
+
+    def hmg_level_csr(self, level):
+        """(row_ptr, cols, vals, mask) of h-multigrid level `level`'s Galerkin matrix."""
+        n, nnz = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().hxg_mg_hmg_level_nnz(self.h, int(level), ctypes.byref(n), ctypes.byref(nnz)))
+        rp = np.zeros(n.value + 1, np.int32)
+        cols = np.zeros(nnz.value, np.int32)
+        vals = np.zeros(nnz.value)
+        mask = np.zeros(n.value, np.uint8)
+        check(lib().hxg_mg_hmg_level_csr_host(self.h, int(level), _ptr(rp), _ptr(cols), _ptr(vals),
+                                              _ptr(mask)))
+        return rp, cols, vals, mask
+
     def coarse_vals_device(self):
         """The assembled coarse values as a CUDA tensor (CSR order of coarse_csr)."""
         nnz = ctypes.c_int64()

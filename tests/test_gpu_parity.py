@@ -535,8 +535,11 @@ def test_edge_cases_against_oracle(order, cells, maskkind):
     (one component + scattered DoFs): residual, Jacobian apply (fused and
     two-pass) and diagonal against the numpy oracle to 1e-12."""
     P, op, u, _ = _edge_case_problem(order, cells, maskkind)
-    f = op.apply_residual(cuda(u))
-    assert rel(f, P.op.apply_residual(u)) < 1e-12
+    f_ref = P.op.apply_residual(u)
+    for variant in (1, 0):  # two-pass element path, then the fused brick residual
+        op.set_variant(variant)
+        f = op.apply_residual(cuda(u))
+        assert rel(f, f_ref) < 1e-12
     x = np.cos(0.37 * np.arange(P.op.size))
     jref = P.op.apply_jacobian(x)
     for variant in (0, 1):

@@ -48,7 +48,7 @@ def _smooth_u(npd, node0, gnpd, scale=0.2):
     return u.reshape(-1)
 
 
-def _run(rank, world, port, dims, order, out_dir):
+def _run(rank, world, port, dims, order, out_dir, cells=CELLS, mode="auto"):
     import torch.distributed as dist
 
     from paper_2204_01722_b200.distributed import Communicator, PartitionedProblem
@@ -59,11 +59,11 @@ def _run(rank, world, port, dims, order, out_dir):
                                 init_method=f"tcp://127.0.0.1:{port}")
     comm = Communicator(rank, world, dist if world > 1 else None,
                         backend="gloo" if world > 1 else "nccl")
-    pp = PartitionedProblem(comm, CELLS, dims, order=order, extents=EXT, fixed_faces=("-x",),
+    pp = PartitionedProblem(comm, cells, dims, order=order, extents=EXT, fixed_faces=("-x",),
                             traction_face="+x", traction=TRACTION)
     p = order
     npd = tuple(p * c + 1 for c in pp.cells)
-    gnpd = tuple(p * c + 1 for c in CELLS)
+    gnpd = tuple(p * c + 1 for c in cells)
     node0 = tuple(p * e for e in pp.e0)
     n = pp.size()
     res = {}
@@ -73,6 +73,7 @@ def _run(rank, world, port, dims, order, out_dir):
     res["y"] = pp.apply(x).cpu().numpy()
     # linearised at u = 0 (b = -F(0)), p-MG PCG to 1e-8
     f0 = pp.residual(torch.zeros(n, dtype=torch.float64, device="cuda"))
+    pp.set_coarse_mode(mode)
     pp.setup_numeric()
     res["lam"] = np.array([pp.lambda_max(k) for k in range(1, pp.levels)])
     r = pp.cg_solve(-f0, rtol=1e-8)
@@ -88,11 +89,11 @@ def _run(rank, world, port, dims, order, out_dir):
         dist.destroy_process_group()
 
 
-def _whole_box(order):
+def _whole_box(order, cells=CELLS, mode="auto"):
     from paper_2204_01722_b200.hexmg import FemProblem, cg_solve
-    prob = FemProblem(extents=EXT, cells=CELLS, order=order, fixed_faces=("-x",),
+    prob = FemProblem(extents=EXT, cells=cells, order=order, fixed_faces=("-x",),
                       traction_face="+x", traction=TRACTION, geometry="box")
-    gnpd = tuple(order * c + 1 for c in CELLS)
+    gnpd = tuple(order * c + 1 for c in cells)
     n = prob.size()
     out = {}
     u = torch.from_numpy(_smooth_u(gnpd, (0, 0, 0), gnpd)).cuda()
@@ -101,6 +102,7 @@ def _whole_box(order):
     out["y"] = prob.op.apply_jacobian(x).cpu().numpy()
     f0 = prob.op.apply_residual(torch.zeros(n, dtype=torch.float64, device="cuda"))
     mg = prob.hierarchy
+    mg.set_coarse_mode(mode)
     mg.setup_numeric()
     out["lam"] = np.array([mg.lambda_max(k) for k in range(1, mg.num_levels())])
     r = cg_solve(prob.op, -f0, rtol=1e-8, precond="mg", mg=mg)
@@ -125,14 +127,27 @@ def rel(a, b):
                                               (3, (3, 1, 1), 2), (4, (2, 2, 1), 2),
                                               (2, (2, 1, 1), 3)])
 def test_partitioned_matches_whole_box(world, dims, order, tmp_path):
+    _check_partitioned(world, dims, order, tmp_path, CELLS, "auto")
+
+
+@pytest.mark.parametrize("world,dims", [(1, (1, 1, 1)), (2, (2, 1, 1)), (4, (2, 2, 1))])
+def test_partitioned_inexact_coarse_matches_whole_box(world, dims, tmp_path):
+    """The inexact coarse mode distributed with the hierarchy (csrc/hcoarse.cu):
+    h-levels on the blocks (32 x 16 x 16 Q2: the Q1 level and two Galerkin
+    levels), replicated dense bottom -- the same lambda_max, iterations and
+    solutions as the single-process h-multigrid."""
+    _check_partitioned(world, dims, 2, tmp_path, (32, 16, 16), "hmg")
+
+
+def _check_partitioned(world, dims, order, tmp_path, cells, mode):
     import torch.multiprocessing as mp
-    ref, gnpd = _whole_box(order)
+    ref, gnpd = _whole_box(order, cells, mode)
     port = _free_port()
     if world == 1:
-        _run(0, 1, port, dims, order, str(tmp_path))
+        _run(0, 1, port, dims, order, str(tmp_path), cells, mode)
     else:
         ctx = mp.get_context("spawn")
-        procs = [ctx.Process(target=_run, args=(r, world, port, dims, order, str(tmp_path)))
+        procs = [ctx.Process(target=_run, args=(r, world, port, dims, order, str(tmp_path), cells, mode))
                  for r in range(world)]
         for p in procs:
             p.start()
