@@ -365,7 +365,7 @@ def run_ours(args, rank, world, local_rank):
         dims5 = {2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}.get(world, (world, 1, 1))
         pp5 = PartitionedProblem(comm, tuple(c5 * d for d in dims5), dims5, order=ORDER,
                                  extents=tuple(float(d) for d in dims5), fixed_faces=("-x",),
-                                 geometry="box")
+                                 traction_face="+x", traction=(0.0, 0.0, -0.02), geometry="box")
         prob5 = pp5.prob
         n5 = prob5.size()
         prob5.op.apply_residual(torch.zeros(n5, dtype=torch.float64, device="cuda"))
@@ -399,6 +399,36 @@ def run_ours(args, rank, world, local_rank):
                 "ms_per_apply": ms5, "GDoF_s": n5 * world / (ms5 * 1e-3) / 1e9,
                 "algorithmic_GB_s_per_gpu": b5 / (ms5 * 1e-3) / 1e9,
                 "roofline_frac": b5 / (ms5 * 1e-3) / 1e9 / peak_gbs()}
+        if args.cfg5_pmg:
+            # the configs[4] p-MG solve at ~1e8 DoF per GPU: only the inexact
+            # coarse mode is feasible (an exact factorization of the 12.5 M-DoF
+            # Q1 level per GPU is not, SURVEY.md §7.2 hard part 3)
+            pp5.set_coarse_mode("hmg")
+            z5 = torch.zeros(n5, dtype=torch.float64, device="cuda")
+            f5 = pp5.residual(z5)
+            pp5.setup_numeric()  # symbolic (patterns) + first numeric
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            torch.cuda.synchronize()
+            if dist is not None:
+                dist.barrier()
+            e[0].record(stream)
+            f5 = pp5.residual(z5)
+            e[1].record(stream)
+            pp5.setup_numeric()
+            e[2].record(stream)
+            r5 = pp5.cg_solve(-f5, rtol=1e-8)
+            e[3].record(stream)
+            torch.cuda.synchronize()
+            tt = torch.tensor([e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]),
+                               e[2].elapsed_time(e[3])], dtype=torch.float64, device="cuda")
+            if dist is not None:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            cfg5["pmg_inexact"] = {"residual_ms": tt[0].item(), "setup_numeric_ms": tt[1].item(),
+                                   "pcg_rtol1e-8_ms": tt[2].item(),
+                                   "pcg_rtol1e-8_iterations": r5["iterations"],
+                                   "condition": r5["eig_max"] / r5["eig_min"],
+                                   "coarse": "one Galerkin h-multigrid V-cycle (h-levels on the blocks)"}
+            del z5, f5, r5
         del pp5, prob5, x5, y5
         torch.cuda.empty_cache()
 
@@ -698,6 +728,8 @@ def main():
                     help="order:cells,... of the CPU p-MG solve baseline ('' to skip)")
     ap.add_argument("--no-newton", action="store_true")
     ap.add_argument("--no-cfg5", action="store_true")
+    ap.add_argument("--cfg5-pmg", action="store_true",
+                    help="also run the configs[4] p-MG solve (inexact coarse mode) at Q2 160^3 per GPU")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test the N > 1 path with every rank on one GPU")
     args = ap.parse_args()

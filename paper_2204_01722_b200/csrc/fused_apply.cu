@@ -96,6 +96,9 @@ __host__ __device__ constexpr int pf_mode(int q) {
 #define HXG_FIXUP_THREADS 128
 #endif
 constexpr int kFixupThreads = HXG_FIXUP_THREADS;
+#ifndef HXG_FIXUP_MINB
+#define HXG_FIXUP_MINB 1
+#endif
 constexpr int kFixupMaxGrid = 148 * 64;
 
 struct FusedParams {
@@ -826,7 +829,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
 // their whole length, the other rows only at ix = 0 (and the far face of the
 // box).  The index math is all brick-local.
 template <int P, int Q, int MODE = kJacobian>
-__global__ void __launch_bounds__(kFixupThreads) fused_fixup_kernel(const __grid_constant__ FusedParams prm) {
+__global__ void __launch_bounds__(kFixupThreads, HXG_FIXUP_MINB) fused_fixup_kernel(const __grid_constant__ FusedParams prm) {
   using D = FDims<P, Q>;
   constexpr int BX = D::BX, BY = D::BY, BZ = D::BZ;
   constexpr int PB0 = P * BX, PB1 = P * BY, PB2 = P * BZ;
