@@ -151,4 +151,85 @@ __global__ void assemble_element_kernel(DiagParams prm) {
   }
 }
 
+// p = 1 element matrices (the coarse level's, coo_numeric assembly.hpp:
+// 188-230), two-stage: per chunk of points, D_q by one q-function probe per
+// thread (point, column), T[q][(ca,i)][(b,cb)] = sum_j D_q[(ca,i),(cb,j)]
+// g_b,j(q), then K[(a,ca),(b,cb)] += sum_q sum_i g_a,i(q) T[q][(ca,i)][(b,cb)]
+// (each thread owns two entries of K).  ~90 k flops per element instead of
+// the generic kernel's ~500 k.
+constexpr int kQ1AsmThreads = 288;
+constexpr int kQ1AsmChunk = 27;
+template <int Q>
+__global__ void __launch_bounds__(kQ1AsmThreads) assemble_element_q1_kernel(DiagParams prm) {
+  constexpr int N = 2, N3 = 8, Q3 = Q * Q * Q, M = 3 * N3, QC = kQ1AsmChunk;
+  extern __shared__ double smem[];
+  double* sD = smem;              // QC x 81
+  double* sG = sD + QC * 81;      // QC x 8 x 3
+  double* sT = sG + QC * N3 * 3;  // QC x 9 x 24
+  const long long e = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int S = device_state_stride(prm.storage);
+  double acc[2] = {0.0, 0.0};
+  for (int q0 = 0; q0 < Q3; q0 += QC) {
+    const int qn = Q3 - q0 < QC ? Q3 - q0 : QC;
+    // D_q columns: one probe per (point, u)
+    for (int w = tid; w < qn * 9; w += kQ1AsmThreads) {
+      const int ql = w / 9, u = w - 9 * ql, qpt = q0 + ql;
+      const long long off = state_offset(prm.lay, e, qpt, S);
+      double st[kMaxStateStride];
+      for (int s = 0; s < S; ++s) st[s] = prm.state[off + state_pair_off(s, prm.lay.T, prm.lay.Q)];
+      double G[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, H[9];
+      G[u] = 1.0;
+      switch (prm.storage) {
+        case kStorageInitialNative: jacobian_qf_initial<kStorageInitialNative>(prm.mu, prm.lambda, G, st, H); break;
+        case kStorageInitialTuned: jacobian_qf_initial<kStorageInitialTuned>(prm.mu, prm.lambda, G, st, H); break;
+        case kStorageInitialAD: jacobian_qf_initial<kStorageInitialAD>(prm.mu, prm.lambda, G, st, H); break;
+        default: jacobian_qf(prm.mu, prm.lambda, G, st, H);
+      }
+      if (prm.perturb != 0.0) {  // + eps w detJ G (as point_tensor)
+        const long long T = prm.lay.T, row = off / T / state_row(S, prm.lay.Q);
+        const long long t = state_paired(prm.lay.Q) ? (off % (2 * T)) / 2 : off % T;
+        H[u] += prm.perturb * prm.geo[(row * kGeoStride + 9) * T + t];
+      }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) sD[ql * 81 + k * 9 + u] = H[k];
+    }
+    // node gradients at the chunk's points (dense tabulation, basis.hpp:439-447)
+    for (int w = tid; w < qn * N3; w += kQ1AsmThreads) {
+      const int ql = w / N3, a = w - N3 * ql, qpt = q0 + ql;
+      const int i = a & 1, j = (a >> 1) & 1, k = a >> 2;
+      const int qa = qpt % Q, qb = (qpt / Q) % Q, qc = qpt / (Q * Q);
+      const double bi = prm.interp[qa * N + i], bj = prm.interp[qb * N + j], bk = prm.interp[qc * N + k];
+      const double di = prm.deriv[qa * N + i], dj = prm.deriv[qb * N + j], dk = prm.deriv[qc * N + k];
+      sG[(ql * N3 + a) * 3 + 0] = di * bj * bk;
+      sG[(ql * N3 + a) * 3 + 1] = bi * dj * bk;
+      sG[(ql * N3 + a) * 3 + 2] = bi * bj * dk;
+    }
+    __syncthreads();
+    for (int w = tid; w < qn * 9 * M; w += kQ1AsmThreads) {
+      const int ql = w / (9 * M), r = w - ql * 9 * M, ki = r / M, bc = r - ki * M;
+      const int b = bc / 3, cb = bc - 3 * b;
+      const double* d = sD + ql * 81 + ki * 9 + cb * 3;
+      const double* gb = sG + (ql * N3 + b) * 3;
+      sT[w] = d[0] * gb[0] + d[1] * gb[1] + d[2] * gb[2];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int idx = tid + h * kQ1AsmThreads;  // (a ca) * 24 + (b cb)
+      const int rowi = idx / M, bc = idx - rowi * M, a = rowi / 3, ca = rowi - 3 * a;
+      double s = 0.0;
+      for (int ql = 0; ql < qn; ++ql) {
+        const double* ga = sG + (ql * N3 + a) * 3;
+        const double* t = sT + ql * 9 * M + (ca * 3) * M + bc;
+        s += ga[0] * t[0] + ga[1] * t[M] + ga[2] * t[2 * M];
+      }
+      acc[h] += s;
+    }
+    __syncthreads();
+  }
+  prm.out[e * (long long)(M * M) + tid] = acc[0];
+  prm.out[e * (long long)(M * M) + tid + kQ1AsmThreads] = acc[1];
+}
+
 }  // namespace hxg

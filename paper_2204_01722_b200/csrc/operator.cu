@@ -354,6 +354,17 @@ void Operator::element_matrices(double* out) {
   if (perturb_ != 0.0 && !prm.geo)
     throw Error(HXG_ERR_INVALID_ARGUMENT, "the perturbation hook needs geometric factors");
   prm.out = out;
+  if (p_ == 1) {  // the coarse level: two-stage contraction
+    dispatch_q(q_, [&](auto Qc) {
+      constexpr int Q = decltype(Qc)::value;
+      constexpr size_t smem = sizeof(double) * kQ1AsmChunk * (81 + 24 + 9 * 24);
+      auto k = assemble_element_q1_kernel<Q>;
+      HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k<<<(unsigned)num_elements(), kQ1AsmThreads, smem, stream_>>>(prm);
+    });
+    HXG_CUDA(cudaGetLastError());
+    return;
+  }
   dispatch_pq(p_, q_, [&](auto Pc, auto Qc) {
     constexpr int P = decltype(Pc)::value, Q = decltype(Qc)::value;
     size_t smem = sizeof(double) * (2 * Q * (P + 1) + Q * Q * Q * 81);
