@@ -508,7 +508,7 @@ def run_ours(args, rank, world, local_rank):
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
             prob_n = FemProblem(extents=(1.0, 1.0, 1.0), cells=(cells,) * 3, order=order,
                                 fixed_faces=("-x",), traction_face="+x",
-                                traction=(0.0, 0.0, -0.02))
+                                traction=(0.0, 0.0, -0.02), geometry="box")
             un = torch.zeros(prob_n.size(), dtype=torch.float64, device="cuda")
             mg = prob_n.hierarchy
             mg.set_coarse_mode(mode)
@@ -592,7 +592,8 @@ def run_ours(args, rank, world, local_rank):
     newton_full = None
     if world == 1 and not args.no_newton:
         prob_b = FemProblem(extents=(2.0, 1.0, 1.0), cells=(96, 48, 48), order=2,
-                            fixed_faces=("-x",), traction_face="+x", traction=(-0.02, 0.0, 0.0))
+                            fixed_faces=("-x",), traction_face="+x", traction=(-0.02, 0.0, 0.0),
+                            geometry="box")
         eb = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         torch.cuda.synchronize()
         eb[0].record(stream)
@@ -610,7 +611,8 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.empty_cache()
         # the same solve with the inexact coarse mode
         prob_b = FemProblem(extents=(2.0, 1.0, 1.0), cells=(96, 48, 48), order=2,
-                            fixed_faces=("-x",), traction_face="+x", traction=(-0.02, 0.0, 0.0))
+                            fixed_faces=("-x",), traction_face="+x", traction=(-0.02, 0.0, 0.0),
+                            geometry="box")
         prob_b.hierarchy.set_coarse_mode("hmg")
         torch.cuda.synchronize()
         eb[0].record(stream)

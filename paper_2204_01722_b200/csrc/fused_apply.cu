@@ -54,6 +54,9 @@
 #ifndef HXG_NSH_Q2
 #define HXG_NSH_Q2 3
 #endif
+#ifndef HXG_RES_BOX_GEO
+#define HXG_RES_BOX_GEO 1  // residual on box meshes: geometry in registers
+#endif
 #ifndef HXG_SKIP_FIXUP
 #define HXG_SKIP_FIXUP 0  // timing experiment only: results are wrong
 #endif
@@ -117,6 +120,10 @@ struct FusedParams {
   const double* load;
   double load_scale;
   unsigned long long* fail;
+  // residual on a box mesh: the geometric factors formed in registers (the
+  // stored ones are the same products, Operator::make_box_geometry)
+  int geo_box;
+  double geo_g[3], geo_jac, geo_qw[kMaxQ];
   int brick0;   // first brick of this launch (pipelined host path)
   int nbricks;  // bricks in this launch
   int face_bits;  // >= 0: constraints are these whole faces (analytic), -1: mask array
@@ -401,8 +408,8 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   for (int bi = blockIdx.x; bi < prm.nbricks; bi += gridDim.x, cur ^= 1) {
   const int brick = prm.brick0 + bi;
   const bool pf_next = tid == 0 && bi + (int)gridDim.x < prm.nbricks;
-  if (pf_mode(Q) == 0 && pf_next) prefetch_state(brick + gridDim.x);
-  if (pf_mode(Q) == 1 && tid == 0) prefetch_state(brick);
+  if (pf_mode(Q) == 0 && pf_next && !(kRes && prm.geo_box)) prefetch_state(brick + gridDim.x);
+  if (pf_mode(Q) == 1 && tid == 0 && !(kRes && prm.geo_box)) prefetch_state(brick);
   const int bx = bc.x, by = bc.y, bz = bc.z;
   const BrickXYZ bnext = advance(bc);
   const double* st_brick = prm.state + (size_t)lay.brick_points() * brick * SP;
@@ -609,10 +616,20 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
     if constexpr (kRes) {
       if (valid) {
         const size_t pt = (size_t)lay.brick_points() * brick + (size_t)qz * T;
-        const double* gp = prm.geo + pt * kGeoStride + tid;
         double geo[kGeoStride];
+        if (prm.geo_box) {
+          const int qx = te % Q, qy = te / Q;
 #pragma unroll
-        for (int s = 0; s < kGeoStride; ++s) geo[s] = ld_stream(gp + s * T, pol_stream);
+          for (int s = 0; s < 9; ++s) geo[s] = 0.0;
+          geo[0] = prm.geo_g[0];
+          geo[4] = prm.geo_g[1];
+          geo[8] = prm.geo_g[2];
+          geo[9] = prm.geo_qw[qx] * prm.geo_qw[qy] * prm.geo_qw[qz] * prm.geo_jac;
+        } else {
+          const double* gp = prm.geo + pt * kGeoStride + tid;
+#pragma unroll
+          for (int s = 0; s < kGeoStride; ++s) geo[s] = ld_stream(gp + s * T, pol_stream);
+        }
         double G[9];
 #pragma unroll
         for (int c = 0; c < 3; ++c)
@@ -1061,6 +1078,10 @@ void fused_residual(Operator& op, const double* u, double* f) {
   prm.state = nullptr;
   prm.state_out = op.state_->data.p;
   prm.geo = op.geometry_->data.p;
+  prm.geo_box = op.geometry_->box && HXG_RES_BOX_GEO;
+  for (int d = 0; d < 3; ++d) prm.geo_g[d] = op.geometry_->g[d];
+  prm.geo_jac = op.geometry_->jac;
+  for (int i = 0; i < kMaxQ; ++i) prm.geo_qw[i] = op.geometry_->qw[i];
   prm.load = op.load_.n ? op.load_.p : nullptr;
   prm.load_scale = op.load_scale_;
   prm.fail = op.fail_.p;

@@ -83,8 +83,12 @@ std::shared_ptr<Geometry> Operator::make_box_geometry(const int cells[3], int q,
     if (!(extents[d] > 0.0)) throw Error(HXG_ERR_INVALID_ARGUMENT, "box extents must be positive");
     h[d] = extents[d] / cells[d];
   }
+  g->box = true;
+  for (int d = 0; d < 3; ++d) g->g[d] = 2.0 / h[d];
+  g->jac = 0.125 * h[0] * h[1] * h[2];
+  for (int i = 0; i < q && i < kMaxQ; ++i) g->qw[i] = qweights[i];
   box_geometry_kernel<<<grid_for(g->lay.total_points(), 256), 256>>>(
-      g->lay, 2.0 / h[0], 2.0 / h[1], 2.0 / h[2], 0.125 * h[0] * h[1] * h[2], qw.p, g->data.p);
+      g->lay, g->g[0], g->g[1], g->g[2], g->jac, qw.p, g->data.p);
   HXG_CUDA(cudaGetLastError());
   HXG_CUDA(cudaDeviceSynchronize());  // qw is released on return
   return g;

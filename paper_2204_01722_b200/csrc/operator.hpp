@@ -51,6 +51,13 @@ struct State {
 struct Geometry {
   DevBuf<double> data;
   QLayout lay;
+  // Box meshes (build_box_mesh: every element the same affine map): the
+  // factors are dxi/dX = diag(g), w detJ = w_qx w_qy w_qz jac, so kernels
+  // that only read them (the fused residual) can form them in registers.
+  bool box = false;
+  double g[3] = {0.0, 0.0, 0.0};
+  double jac = 0.0;
+  double qw[kMaxQ] = {0.0, 0.0, 0.0, 0.0, 0.0};
 };
 
 // Streams, events and device staging for the pipelined host-buffer apply

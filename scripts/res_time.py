@@ -6,9 +6,11 @@ import numpy as np, torch
 from paper_2204_01722_b200.hexmg import FemProblem
 
 cases = [tuple(map(int, c.split(":"))) for c in (sys.argv[1] if len(sys.argv) > 1 else "2:64,3:43,4:32").split(",")]
+geo = sys.argv[2] if len(sys.argv) > 2 else "box"
 for order, n in cases:
     prob = FemProblem(extents=(1, 1, 1), cells=(n, n, n), order=order, fixed_faces=("-x",),
-                      traction_face="+x", traction=(0, 0, -0.02))
+                      traction_face="+x", traction=(0, 0, -0.02),
+                      geometry="box" if geo == "box" else True)
     N = prob.size()
     gn = order * n + 1
     idx = torch.arange(N // 3, device="cuda", dtype=torch.float64)
@@ -32,6 +34,6 @@ for order, n in cases:
     srel = None
     if out[0][2] is not None:
         srel = float(np.abs(out[0][2] - out[1][2]).max() / np.abs(out[1][2]).max())
-    print(json.dumps(dict(case=f"Q{order} {n}^3", two_pass_ms=out[1][0], fused_ms=out[0][0],
+    print(json.dumps(dict(case=f"Q{order} {n}^3", geometry=geo, two_pass_ms=out[1][0], fused_ms=out[0][0],
                           f_rel=rel, state_maxrel=srel)), flush=True)
     del prob; torch.cuda.empty_cache()
