@@ -24,6 +24,8 @@
 // Every sum has a fixed order, so y is bitwise reproducible run to run.
 #include "fused_apply.cuh"
 
+#include <cstdlib>
+
 #include "apply_kernels.cuh"
 #include "dispatch.hpp"
 #include "operator.hpp"
@@ -57,6 +59,10 @@
 #ifndef HXG_RES_BOX_GEO
 #define HXG_RES_BOX_GEO 1  // residual on box meshes: geometry in registers
 #endif
+#ifndef HXG_HOST_CHUNKS_DEFAULT
+#define HXG_HOST_CHUNKS_DEFAULT 8
+#endif
+constexpr int kHostChunks = HXG_HOST_CHUNKS_DEFAULT;
 #ifndef HXG_SKIP_FIXUP
 #define HXG_SKIP_FIXUP 0  // timing experiment only: results are wrong
 #endif
@@ -1153,7 +1159,15 @@ void fused_jacobian_host(Operator& op, const double* xh, double* yh) {
     const int nbz = op.lay_.nb[2], layer = op.lay_.nb[0] * op.lay_.nb[1];
     const int pb2 = P * D::BZ, npz = op.box_.npd[2];
     const size_t plane = (size_t)op.box_.npd[0] * op.box_.npd[1] * 3;
-    const int C = nbz < HostPipe::kMaxChunks / 2 ? nbz : HostPipe::kMaxChunks / 2;
+    // chunks of brick layers: enough to overlap the two PCIe directions with
+    // little pipeline fill (HXG_HOST_CHUNKS overrides, for measurements)
+    static const int env_chunks = [] {
+      const char* e = std::getenv("HXG_HOST_CHUNKS");
+      return e ? std::atoi(e) : 0;
+    }();
+    int want = env_chunks > 0 ? env_chunks : kHostChunks;
+    if (want > HostPipe::kMaxChunks) want = HostPipe::kMaxChunks;
+    const int C = nbz < want ? nbz : want;
     // Order after earlier work on the operator's stream.
     HXG_CUDA(cudaEventRecord(pp.done_evt, op.stream_));
     HXG_CUDA(cudaStreamWaitEvent(pp.h2d, pp.done_evt, 0));

@@ -63,7 +63,7 @@ struct Geometry {
 // Streams, events and device staging for the pipelined host-buffer apply
 // (H2D of z-chunks / compute / D2H overlapped).
 struct HostPipe {
-  static constexpr int kMaxChunks = 16;
+  static constexpr int kMaxChunks = 64;
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
   cudaEvent_t in_ready[kMaxChunks], out_ready[kMaxChunks], done_evt = nullptr;
   DevBuf<double> x, y;
