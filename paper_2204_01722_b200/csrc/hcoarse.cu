@@ -159,6 +159,60 @@ __global__ void restrict_kernel(BoxDev fbox, BoxDev cbox, const uint8_t* __restr
   }
 }
 
+// Lattice-stencil form of a level matrix: slot k = (s, cb), s = the
+// neighbour offset (dx, dy, dz) in {-1, 0, 1}^3 (x fastest), stored as
+// st[k n + r] (structure of arrays: every slot plane is read coalesced), no
+// column indices; absent couplings (box edges, constrained columns) are 0.
+__global__ void csr_to_stencil_kernel(BoxDev box, const int* __restrict__ rows,
+                                      const int* __restrict__ cols, const double* __restrict__ vals,
+                                      long long nnz, long long n, double* __restrict__ st) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nnz;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = rows[i], c = cols[i];
+    const long long a = r / 3, b = c / 3;
+    const int ax = (int)(a % box.npd[0]), ay = (int)((a / box.npd[0]) % box.npd[1]),
+              az = (int)(a / ((long long)box.npd[0] * box.npd[1]));
+    const int bx = (int)(b % box.npd[0]), by = (int)((b / box.npd[0]) % box.npd[1]),
+              bz = (int)(b / ((long long)box.npd[0] * box.npd[1]));
+    const int sl = ((bz - az + 1) * 3 + (by - ay + 1)) * 3 + (bx - ax + 1);
+    st[(long long)(sl * 3 + (int)(c % 3)) * n + r] = vals[i];
+  }
+}
+
+// y = A x on the stencil form: thread per row, the 81 couplings in fixed
+// (slot, component) order.
+__global__ void __launch_bounds__(256) stencil_matvec_kernel(BoxDev box, long long n,
+                                                             const double* __restrict__ st,
+                                                             const double* __restrict__ x,
+                                                             double* __restrict__ y) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+       r += (long long)gridDim.x * blockDim.x) {
+    const long long a = r / 3;
+    const int ax = (int)(a % box.npd[0]), ay = (int)((a / box.npd[0]) % box.npd[1]),
+              az = (int)(a / ((long long)box.npd[0] * box.npd[1]));
+    double sum = 0.0;
+#pragma unroll
+    for (int dz = -1; dz <= 1; ++dz) {
+      const bool okz = az + dz >= 0 && az + dz < box.npd[2];
+#pragma unroll
+      for (int dy = -1; dy <= 1; ++dy) {
+        const bool oky = okz && ay + dy >= 0 && ay + dy < box.npd[1];
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx) {
+          const bool ok = oky && ax + dx >= 0 && ax + dx < box.npd[0];
+          const int sl = ((dz + 1) * 3 + (dy + 1)) * 3 + (dx + 1);
+          // out-of-box neighbours have zero couplings: read the row's own node
+          const long long nb = ok ? a + dx + (long long)box.npd[0] * (dy + (long long)box.npd[1] * dz) : a;
+#pragma unroll
+          for (int cb = 0; cb < 3; ++cb)
+            sum += __ldg(st + (long long)(sl * 3 + cb) * n + r) * __ldg(x + 3 * nb + cb);
+        }
+      }
+    }
+    y[r] = sum;
+  }
+}
+
 __global__ void csr_diag_kernel(int n, const int* __restrict__ row_ptr, const int* __restrict__ cols,
                                 const double* __restrict__ vals, double* __restrict__ d) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
@@ -285,6 +339,7 @@ struct HmgCoarse::HLevel {
   const CsrMatrix* A = nullptr;
   std::unique_ptr<CoarseAssembly> asmb;  // levels >= 1
   DevBuf<double> elem;                   // levels >= 1: Galerkin element matrices
+  DevBuf<double> st;                     // the level matrix in lattice-stencil form (81 n)
   DevBuf<double> b, x, r;
   DevBuf<double> scaled;  // partitioned: interface-scaled residual for the restriction
   Chebyshev smoother;
@@ -469,6 +524,16 @@ void HmgCoarse::setup(const CsrMatrix& a0, const BoxDev& box0, const std::vector
     HXG_CUDA(cudaGetLastError());
     c.asmb->numeric_from_elements(c.elem.p, s);
   }
+  // stencil forms of the smoothed levels (their SpMV has no column indices)
+  for (size_t l = 0; l + 1 < levels_.size(); ++l) {
+    HLevel& lv = *levels_[l];
+    const long long n = lv.n(), nnz = lv.A->nnz();
+    if (lv.st.n != (size_t)(81 * n)) lv.st.alloc((size_t)(81 * n));
+    HXG_CUDA(cudaMemsetAsync(lv.st.p, 0, sizeof(double) * 81 * n, s));
+    csr_to_stencil_kernel<<<grid_for(nnz, 256), 256, 0, s>>>(lv.box, lv.A->rows.p, lv.A->cols.p,
+                                                              lv.A->vals.p, nnz, n, lv.st.p);
+    HXG_CUDA(cudaGetLastError());
+  }
   // smoothers on every level above the bottom
   for (size_t l = 0; l + 1 < levels_.size(); ++l) {
     HLevel& lv = *levels_[l];
@@ -499,7 +564,9 @@ void HmgCoarse::setup(const CsrMatrix& a0, const BoxDev& box0, const std::vector
 }
 
 void HmgCoarse::apply_level(HLevel& lv, const double* x, double* y, cudaStream_t s) {
-  csr_matvec(*lv.A, x, y, s);
+  const long long n = lv.n();
+  stencil_matvec_kernel<<<grid_for(n, 256), 256, 0, s>>>(lv.box, n, lv.st.p, x, y);
+  HXG_CUDA(cudaGetLastError());
   if (part_) part_->exchange(lv.lat, y, s, x, lv.m());  // constrained rows: identity
 }
 
