@@ -375,6 +375,11 @@ int hxg_setup_traction_load(const double extents[3], const int cells[3], int p, 
 
 /* Timing helper: `repeats` Jacobian applies of x into y on the op's stream,
  * bracketed by CUDA events after `warmup` applies; returns milliseconds. */
+/* Per-kernel split of the fused apply (instrumentation for the roofline):
+ * mean ms of the brick kernel (ms[0]) and of the boundary fix-up (ms[1]) over
+ * `repeats` applies, events on the operator's stream. */
+int hxg_op_time_jacobian_parts(hxg_op_t op, const double* x, double* y, int warmup, int repeats,
+                               double ms[2]);
 int hxg_op_time_jacobian(hxg_op_t op, const double* x, double* y, int warmup, int repeats,
                          double* ms);
 

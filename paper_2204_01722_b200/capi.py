@@ -197,6 +197,7 @@ SIGNATURES = {
     "hxg_setup_constraints": [_vp, _i, _i, _vp],
     "hxg_setup_traction_load": [_vp, _vp, _i, _i, _i, _vp, _vp],
     "hxg_op_time_jacobian": [_vp, _vp, _vp, _i, _i, _P(_d)],
+    "hxg_op_time_jacobian_parts": [_vp, _vp, _vp, _i, _i, _vp],
 }
 _RESTYPE = {"hxg_version": ctypes.c_char_p}
 

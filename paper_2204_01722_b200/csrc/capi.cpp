@@ -211,6 +211,37 @@ int hxg_op_scatter_add(hxg_op_t op, const double* e, double* l) {
   return guarded([&] { OP(op).scatter_add(e, l); });
 }
 
+int hxg_op_time_jacobian_parts(hxg_op_t op, const double* x, double* y, int warmup, int repeats,
+                               double ms[2]) {
+  return guarded([&] {
+    auto& o = OP(op);
+    if (!o.fused()) throw hxg::Error(HXG_ERR_UNSUPPORTED, "per-kernel timing needs the fused path");
+    if (repeats < 1 || repeats > 1000) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "repeats in 1..1000");
+    cudaStream_t s = o.stream();
+    for (int w = 0; w < warmup; ++w) o.apply_jacobian(x, y);
+    std::vector<cudaEvent_t> ev(3 * (size_t)repeats);
+    for (auto& e : ev) HXG_CUDA(cudaEventCreate(&e));
+    HXG_CUDA(cudaStreamSynchronize(s));
+    for (int r = 0; r < repeats; ++r) {
+      HXG_CUDA(cudaEventRecord(ev[3 * r], s));
+      o.set_split_event(ev[3 * r + 1]);
+      o.apply_jacobian(x, y);
+      HXG_CUDA(cudaEventRecord(ev[3 * r + 2], s));
+    }
+    HXG_CUDA(cudaEventSynchronize(ev.back()));
+    double a = 0.0, b = 0.0;
+    for (int r = 0; r < repeats; ++r) {
+      float f = 0.f, g = 0.f;
+      HXG_CUDA(cudaEventElapsedTime(&f, ev[3 * r], ev[3 * r + 1]));
+      HXG_CUDA(cudaEventElapsedTime(&g, ev[3 * r + 1], ev[3 * r + 2]));
+      a += f;
+      b += g;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    ms[0] = a / repeats;
+    ms[1] = b / repeats;
+  });
+}
 int hxg_op_time_jacobian(hxg_op_t op, const double* x, double* y, int warmup, int repeats,
                          double* ms) {
   return guarded([&] {

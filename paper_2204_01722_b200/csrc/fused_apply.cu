@@ -1046,6 +1046,10 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
     k<<<persistent_grid(k, D::T, smem, prm.nbricks), D::T, smem, op.stream_>>>(prm);
 #endif
     HXG_CUDA(cudaGetLastError());
+    if (op.split_evt_) {
+      HXG_CUDA(cudaEventRecord(op.split_evt_, op.stream_));
+      op.split_evt_ = nullptr;
+    }
     const unsigned fg = HXG_SKIP_FIXUP ? 0 : fixup_grid(prm.nbricks);
     if (fg) {
 #if HXG_FIXUP_PDL

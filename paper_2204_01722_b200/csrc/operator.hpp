@@ -159,6 +159,9 @@ class Operator {
   void apply_jacobian_host(const double* xh, double* yh);
 
   friend void fused_jacobian(Operator& op, const double* du, double* y);
+  // Instrumentation: when set, the next fused apply records this event on
+  // the stream between the brick kernel and the fix-up kernel (then clears it).
+  void set_split_event(cudaEvent_t e) { split_evt_ = e; }
   friend void fused_residual(Operator& op, const double* u, double* f);
   friend void fused_jacobian_host(Operator& op, const double* xh, double* yh);
 
@@ -183,6 +186,7 @@ class Operator {
   DevBuf<double> load_;
   DevBuf<double> evec_;    // E-vector scratch for the two-pass path
   DevBuf<double> partial_; // brick-boundary partial sums for the fused path
+  cudaEvent_t split_evt_ = nullptr;
   std::unique_ptr<HostPipe> pipe_;
   DevBuf<unsigned long long> fail_;
   std::shared_ptr<State> state_;

@@ -288,6 +288,13 @@ class MatrixFreeOperator:
         check(lib().hxg_op_scatter_add(self.h, _ptr(_dev(ev)), _ptr(_out(out, self._size))))
         return out
 
+    def time_jacobian_parts(self, x, y, warmup=3, repeats=20):
+        """(brick kernel ms, fix-up kernel ms) per fused apply, events on the stream."""
+        ms = np.zeros(2)
+        check(lib().hxg_op_time_jacobian_parts(self.h, _ptr(_dev(x, self.size())),
+                                               _ptr(_out(y, self.size())), warmup, repeats, _ptr(ms)))
+        return float(ms[0]), float(ms[1])
+
     def time_jacobian(self, x, y, warmup=3, repeats=20) -> float:
         ms = ctypes.c_double()
         x, y = _dev(x, self._size), _out(y, self._size)
