@@ -24,7 +24,10 @@
 // Every sum has a fixed order, so y is bitwise reproducible run to run.
 #include "fused_apply.cuh"
 
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "apply_kernels.cuh"
 #include "dispatch.hpp"
@@ -63,6 +66,10 @@
 #define HXG_HOST_CHUNKS_DEFAULT 8
 #endif
 constexpr int kHostChunks = HXG_HOST_CHUNKS_DEFAULT;
+#ifndef HXG_PIPE_GRID_PCT_DEFAULT
+#define HXG_PIPE_GRID_PCT_DEFAULT 100
+#endif
+constexpr int kPipeGridPct = HXG_PIPE_GRID_PCT_DEFAULT;
 #ifndef HXG_SKIP_FIXUP
 #define HXG_SKIP_FIXUP 0  // timing experiment only: results are wrong
 #endif
@@ -1172,6 +1179,18 @@ void fused_jacobian_host(Operator& op, const double* xh, double* yh) {
     int want = env_chunks > 0 ? env_chunks : kHostChunks;
     if (want > HostPipe::kMaxChunks) want = HostPipe::kMaxChunks;
     const int C = nbz < want ? nbz : want;
+    // HXG_PIPE_TRACE=1: per-chunk stage times to stderr (measurement only)
+    static const bool trace = std::getenv("HXG_PIPE_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto tmark = [&](cudaStream_t st) {
+      if (!trace) return;
+      cudaEvent_t e;
+      HXG_CUDA(cudaEventCreate(&e));
+      HXG_CUDA(cudaEventRecord(e, st));
+      tev.push_back(e);
+    };
+    const auto t_host0 = std::chrono::steady_clock::now();
+    tmark(op.stream_);
     // Order after earlier work on the operator's stream.
     HXG_CUDA(cudaEventRecord(pp.done_evt, op.stream_));
     HXG_CUDA(cudaStreamWaitEvent(pp.h2d, pp.done_evt, 0));
@@ -1185,6 +1204,7 @@ void fused_jacobian_host(Operator& op, const double* xh, double* yh) {
                                cudaMemcpyHostToDevice, pp.h2d));
       sent = upto;
       HXG_CUDA(cudaEventRecord(pp.in_ready[i], pp.h2d));
+      tmark(pp.h2d);
     }
     for (int i = 0; i < C; ++i) {
       const int lb = (int)((long long)i * nbz / C), le = (int)((long long)(i + 1) * nbz / C);
@@ -1192,21 +1212,44 @@ void fused_jacobian_host(Operator& op, const double* xh, double* yh) {
       FusedParams pc = prm;
       pc.brick0 = lb * layer;
       pc.nbricks = (le - lb) * layer;
-      k<<<persistent_grid(k, D::T, smem, pc.nbricks), D::T, smem, pp.comp>>>(pc);
+      // a fraction of the SMs is enough to keep up with PCIe and leaves the
+      // copy engines' memory traffic less contended (HXG_PIPE_GRID_PCT)
+      static const int grid_pct = [] {
+        const char* e = std::getenv("HXG_PIPE_GRID_PCT");
+        return e ? std::atoi(e) : kPipeGridPct;
+      }();
+      unsigned g = persistent_grid(k, D::T, smem, pc.nbricks);
+      g = grid_pct > 0 && grid_pct < 100 ? (g * (unsigned)grid_pct + 99) / 100 : g;
+      k<<<g, D::T, smem, pp.comp>>>(pc);
       HXG_CUDA(cudaGetLastError());
       const int zs = i == 0 ? 0 : pb2 * lb;
       const int ze = i == C - 1 ? npz : pb2 * le;
       fused_fixup_kernel<P, Q><<<fixup_grid(pc.nbricks), kFixupThreads, 0, pp.comp>>>(pc);
       HXG_CUDA(cudaGetLastError());
       HXG_CUDA(cudaEventRecord(pp.out_ready[i], pp.comp));
+      tmark(pp.comp);
       HXG_CUDA(cudaStreamWaitEvent(pp.d2h, pp.out_ready[i], 0));
       HXG_CUDA(cudaMemcpyAsync(yh + zs * plane, pp.y.p + zs * plane,
                                (size_t)(ze - zs) * plane * sizeof(double), cudaMemcpyDeviceToHost,
                                pp.d2h));
+      tmark(pp.d2h);
     }
     HXG_CUDA(cudaEventRecord(pp.done_evt, pp.d2h));
     HXG_CUDA(cudaStreamWaitEvent(op.stream_, pp.done_evt, 0));
+    const auto t_host1 = std::chrono::steady_clock::now();
     HXG_CUDA(cudaStreamSynchronize(pp.d2h));
+    if (trace) {
+      HXG_CUDA(cudaDeviceSynchronize());
+      std::fprintf(stderr, "[pipe] C=%d enqueue %.1f us |", C,
+                   std::chrono::duration<double, std::micro>(t_host1 - t_host0).count());
+      for (size_t i = 1; i < tev.size(); ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tev[0], tev[i]);
+        std::fprintf(stderr, " %.0f", ms * 1e3);
+      }
+      std::fprintf(stderr, " (us: h2d x C, then comp/d2h per chunk)\n");
+      for (auto e : tev) cudaEventDestroy(e);
+    }
   });
 }
 
