@@ -130,7 +130,7 @@ def test_partitioned_matches_whole_box(world, dims, order, tmp_path):
     _check_partitioned(world, dims, order, tmp_path, CELLS, "auto")
 
 
-@pytest.mark.parametrize("world,dims", [(1, (1, 1, 1)), (2, (2, 1, 1)), (4, (2, 2, 1))])
+@pytest.mark.parametrize("world,dims", [(1, (1, 1, 1)), (2, (2, 1, 1)), (4, (2, 2, 1)), (8, (2, 2, 2))])
 def test_partitioned_inexact_coarse_matches_whole_box(world, dims, tmp_path):
     """The inexact coarse mode distributed with the hierarchy (csrc/hcoarse.cu):
     h-levels on the blocks (32 x 16 x 16 Q2: the Q1 level and two Galerkin
