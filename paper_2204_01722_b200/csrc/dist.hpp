@@ -82,6 +82,15 @@ class Partition {
   const int* e0() const { return e0_; }        // first global element per direction
   const int* gcells() const { return gcells_; }
   int neighbour(int d, int step) const;  // rank, or -1 at the box boundary
+  // faces of this block shared with a neighbour (bits -x,+x,-y,+y,-z,+z)
+  int interface_faces() const {
+    int bits = 0;
+    for (int d = 0; d < 3; ++d) {
+      if (neighbour(d, -1) >= 0) bits |= 1 << (2 * d);
+      if (neighbour(d, +1) >= 0) bits |= 1 << (2 * d + 1);
+    }
+    return bits;
+  }
   // Global Dirichlet faces (bit f: -x,+x,-y,+y,-z,+z) -> the ones on this block.
   int local_faces(int global_faces) const;
 

@@ -137,6 +137,13 @@ struct FusedParams {
   // stored ones are the same products, Operator::make_box_geometry)
   int geo_box;
   double geo_g[3], geo_jac, geo_qw[kMaxQ];
+  // optional brick list: launch brick i is blist[brick0 + i] (the
+  // partitioned apply's interface layer / interior split)
+  const int* blist;
+  // fix-up node filter over the partition-interface faces iface (bits
+  // -x,+x,-y,+y,-z,+z of this block): 0 all nodes, 1 only nodes on an
+  // interface face, 2 all but those
+  int iface, ifilter;
   int brick0;   // first brick of this launch (pipelined host path)
   int nbricks;  // bricks in this launch
   int face_bits;  // >= 0: constraints are these whole faces (analytic), -1: mask array
@@ -335,7 +342,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
   if (pf_mode(Q) != 1 && tid == 0 && (int)blockIdx.x < prm.nbricks)
-    prefetch_state(prm.brick0 + blockIdx.x);
+    prefetch_state(prm.blist ? prm.blist[prm.brick0 + blockIdx.x] : prm.brick0 + blockIdx.x);
 #if HXG_EXPERIMENT == 4
   long long t_last = clock64();
   long long ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -414,17 +421,19 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  BrickXYZ bc = decompose(prm.brick0 + blockIdx.x);
+  auto brick_at = [&](int i) { return prm.blist ? prm.blist[prm.brick0 + i] : prm.brick0 + i; };
+  BrickXYZ bc = decompose(brick_at(blockIdx.x));
   if ((int)blockIdx.x < prm.nbricks) issue_block(bc, Xs);
   int cur = 0;
 #pragma unroll 1
   for (int bi = blockIdx.x; bi < prm.nbricks; bi += gridDim.x, cur ^= 1) {
-  const int brick = prm.brick0 + bi;
+  const int brick = brick_at(bi);
   const bool pf_next = tid == 0 && bi + (int)gridDim.x < prm.nbricks;
-  if (pf_mode(Q) == 0 && pf_next && !(kRes && prm.geo_box)) prefetch_state(brick + gridDim.x);
+  if (pf_mode(Q) == 0 && pf_next && !(kRes && prm.geo_box)) prefetch_state(brick_at(bi + gridDim.x));
   if (pf_mode(Q) == 1 && tid == 0 && !(kRes && prm.geo_box)) prefetch_state(brick);
   const int bx = bc.x, by = bc.y, bz = bc.z;
-  const BrickXYZ bnext = advance(bc);
+  const BrickXYZ bnext = prm.blist ? decompose(brick_at(min(bi + (int)gridDim.x, prm.nbricks - 1)))
+                                    : advance(bc);
   const double* st_brick = prm.state + (size_t)lay.brick_points() * brick * SP;
   const int ecx = min(BX, box.cells[0] - bx * BX);
   const int ecy = min(BY, box.cells[1] - by * BY);
@@ -869,7 +878,7 @@ __global__ void __launch_bounds__(kFixupThreads, HXG_FIXUP_MINB) fused_fixup_ker
   const unsigned long long pol = policy_evict_first();
   const int fb = prm.face_bits;
   for (int bi = blockIdx.x; bi < prm.nbricks; bi += gridDim.x) {
-    const int b = prm.brick0 + bi;
+    const int b = prm.blist ? prm.blist[prm.brick0 + bi] : prm.brick0 + bi;
     const int cx = b % lay.nb[0], cy = (b / lay.nb[0]) % lay.nb[1], cz = b / (lay.nb[0] * lay.nb[1]);
     const int fnx = P * min(BX, box.cells[0] - cx * BX) + 1;
     const int fny = P * min(BY, box.cells[1] - cy * BY) + 1;
@@ -899,6 +908,13 @@ __global__ void __launch_bounds__(kFixupThreads, HXG_FIXUP_MINB) fused_fixup_ker
         ix = u - r * nbx ? fnx - 1 : 0;
         iz = 1 + r / iyc;
         iy = 1 + r % iyc;
+      }
+      if (prm.ifilter) {  // the partitioned apply's split around the interface exchange
+        const int gx = gx0 + ix, gy = gy0 + iy, gz = gz0 + iz, fi = prm.iface;
+        const bool on = ((fi & 1) && gx == 0) || ((fi & 2) && gx == npx - 1) || ((fi & 4) && gy == 0) ||
+                        ((fi & 8) && gy == npy - 1) || ((fi & 16) && gz == 0) ||
+                        ((fi & 32) && gz == box.npd[2] - 1);
+        if (on != (prm.ifilter == 1)) continue;
       }
       // sharing bricks: one lower neighbour along d when the node sits on
       // the block's low plane and the brick is not the first along d
@@ -1075,6 +1091,93 @@ void fused_jacobian(Operator& op, const double* du, double* y) {
 #endif
     }
     HXG_CUDA(cudaGetLastError());
+  });
+}
+
+void fused_jacobian_split(Operator& op, const double* du, double* y, int iface, cudaStream_t side,
+                          const std::function<void()>& exchange) {
+  if (op.storage_ != kStorageCurrent && op.q_ != op.p_ + 1)
+    throw Error(HXG_ERR_UNSUPPORTED, "split apply: fused path only");
+  const QLayout& lay = op.lay_;
+  const int nbr = (int)lay.num_bricks();
+  if (op.blist_iface_ != iface) {  // brick lists: interface layer first, then the rest
+    std::vector<int> a, b;
+    for (int k = 0; k < nbr; ++k) {
+      const int bx = k % lay.nb[0], by = (k / lay.nb[0]) % lay.nb[1], bz = k / (lay.nb[0] * lay.nb[1]);
+      const bool on = ((iface & 1) && bx == 0) || ((iface & 2) && bx == lay.nb[0] - 1) ||
+                      ((iface & 4) && by == 0) || ((iface & 8) && by == lay.nb[1] - 1) ||
+                      ((iface & 16) && bz == 0) || ((iface & 32) && bz == lay.nb[2] - 1);
+      (on ? a : b).push_back(k);
+    }
+    op.blist_na_ = (int)a.size();
+    a.insert(a.end(), b.begin(), b.end());
+    op.blist_.upload(a);
+    op.blist_iface_ = iface;
+    if (!op.ev_a_) {
+      HXG_CUDA(cudaEventCreateWithFlags(&op.ev_a_, cudaEventDisableTiming));
+      HXG_CUDA(cudaEventCreateWithFlags(&op.ev_x_, cudaEventDisableTiming));
+    }
+  }
+  FusedParams prm{};
+  prm.box = op.box_;
+  prm.lay = op.lay_;
+  prm.x = du;
+  prm.y = y;
+  prm.mask = op.mask();
+  prm.face_bits = op.face_bits();
+  prm.tab = op.tab_.p;
+  prm.state = op.state_->data.p;
+  prm.geo = op.geometry_ ? op.geometry_->data.p : nullptr;
+  if (op.perturb_ != 0.0 && !prm.geo)
+    throw Error(HXG_ERR_INVALID_ARGUMENT, "the perturbation hook needs geometric factors");
+  prm.mu = op.mu_;
+  prm.lambda = op.lambda_;
+  prm.perturb = op.perturb_;
+  prm.blist = op.blist_.p;
+  prm.iface = iface;
+  for (size_t i = 0; i < op.interp_.size(); ++i) prm.B[i] = op.interp_[i];
+  for (size_t i = 0; i < op.deriv_.size(); ++i) prm.Bd[i] = op.deriv_[i];
+  const int na = op.blist_na_, nb = nbr - na;
+  dispatch_pq(op.p_, op.q_, [&](auto Pc, auto Qc) {
+    constexpr int P = decltype(Pc)::value, Q = decltype(Qc)::value;
+    using D = FDims<P, Q>;
+    size_t need = (size_t)op.lay_.num_bricks() * D::NB * 3;
+    if (op.partial_.n != need) op.partial_.alloc(need);
+    prm.partial = op.partial_.p;
+    size_t smem = sizeof(double) * D::SMEM;
+    auto k = select_fused<P, Q>(op.storage_);
+    HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+    cudaStream_t s = op.stream_;
+    // 1. the interface layer and its interface-node sums
+    FusedParams pa = prm;
+    pa.brick0 = 0;
+    pa.nbricks = na;
+    if (na > 0) {
+      k<<<persistent_grid(k, D::T, smem, na), D::T, smem, s>>>(pa);
+      pa.ifilter = 1;
+      fused_fixup_kernel<P, Q><<<fixup_grid(na), kFixupThreads, 0, s>>>(pa);
+      HXG_CUDA(cudaGetLastError());
+    }
+    HXG_CUDA(cudaEventRecord(op.ev_a_, s));
+    // 2. the interior bricks and every other boundary sum (enqueued before the
+    // exchange, so a host-staged communicator blocking in exchange() still
+    // overlaps with them)
+    FusedParams pb = prm;
+    pb.brick0 = na;
+    pb.nbricks = nb;
+    if (nb > 0) k<<<persistent_grid(k, D::T, smem, nb), D::T, smem, s>>>(pb);
+    pb.brick0 = 0;
+    pb.nbricks = nbr;
+    pb.ifilter = 2;
+    fused_fixup_kernel<P, Q><<<fixup_grid(nbr), kFixupThreads, 0, s>>>(pb);
+    HXG_CUDA(cudaGetLastError());
+    // 3. the exchange on the side stream, behind step 1 only
+    HXG_CUDA(cudaStreamWaitEvent(side, op.ev_a_, 0));
+    exchange();
+    HXG_CUDA(cudaEventRecord(op.ev_x_, side));
+    HXG_CUDA(cudaStreamWaitEvent(s, op.ev_x_, 0));
   });
 }
 

@@ -309,6 +309,16 @@ void Operator::apply_jacobian(const double* du, double* y) {
   launch_node_sum(evec_.p, y, du, kEpiJacobian);
 }
 
+void Operator::apply_jacobian_split(const double* du, double* y, int iface, cudaStream_t side,
+                                    const std::function<void()>& exchange) {
+  if (!state_->valid) throw Error(HXG_ERR_STATE_NOT_INITIALIZED,
+                                  "quadrature state not initialized: evaluate the residual at the "
+                                  "linearization point first");
+  if (!fused()) throw Error(HXG_ERR_UNSUPPORTED, "split apply needs the fused path");
+  ++jacobian_applies_;
+  fused_jacobian_split(*this, du, y, iface, side, exchange);
+}
+
 void Operator::extract_diagonal(double* d) {
   if (!state_->valid) throw Error(HXG_ERR_STATE_NOT_INITIALIZED,
                                   "quadrature state not initialized: evaluate the residual at the "

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -159,6 +160,12 @@ class Operator {
   void apply_jacobian_host(const double* xh, double* yh);
 
   friend void fused_jacobian(Operator& op, const double* du, double* y);
+  friend void fused_jacobian_split(Operator& op, const double* du, double* y, int iface,
+                                   cudaStream_t side, const std::function<void()>& exchange);
+  // Partitioned apply with the exchange overlapped (fused path only):
+  // see fused_jacobian_split.
+  void apply_jacobian_split(const double* du, double* y, int iface, cudaStream_t side,
+                            const std::function<void()>& exchange);
   // Instrumentation: when set, the next fused apply records this event on
   // the stream between the brick kernel and the fix-up kernel (then clears it).
   void set_split_event(cudaEvent_t e) { split_evt_ = e; }
@@ -187,6 +194,10 @@ class Operator {
   DevBuf<double> evec_;    // E-vector scratch for the two-pass path
   DevBuf<double> partial_; // brick-boundary partial sums for the fused path
   cudaEvent_t split_evt_ = nullptr;
+  // partitioned apply: bricks touching the interface faces first, then the rest
+  DevBuf<int> blist_;
+  int blist_iface_ = -1, blist_na_ = 0;
+  cudaEvent_t ev_a_ = nullptr, ev_x_ = nullptr;
   std::unique_ptr<HostPipe> pipe_;
   DevBuf<unsigned long long> fail_;
   std::shared_ptr<State> state_;

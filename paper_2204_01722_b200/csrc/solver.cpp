@@ -355,14 +355,30 @@ Hierarchy::Hierarchy(Operator* fine, int fixed_face_mask, std::vector<int> sched
   }
 }
 
-Hierarchy::~Hierarchy() = default;
+Hierarchy::~Hierarchy() {
+  if (side_) cudaStreamDestroy(side_);
+}
 
 void Hierarchy::level_apply(int k, const double* x, double* y) {
   Level& lv = level(k);
-  lv.op->apply_jacobian(x, y);
   // constrained rows are the identity on every block holding them, not
   // summed (operator.hpp:212-214): the interface sum keeps x there (only
   // shared-plane entries were summed; one rank: nothing to exchange)
+  static const bool overlap = [] {
+    const char* e = std::getenv("HXG_OVERLAP");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (part_ && overlap && part_->comm().world() > 1 && lv.op->fused()) {
+    // the interface layer first, its exchange on a side stream while the
+    // interior bricks run
+    if (!side_) HXG_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    const int order = lv.order;
+    const uint8_t* m = lv.op->mask();
+    lv.op->apply_jacobian_split(x, y, part_->interface_faces(), side_,
+                                [&]() { part_->exchange(order, y, side_, x, m); });
+    return;
+  }
+  lv.op->apply_jacobian(x, y);
   if (part_) part_->exchange(lv.order, y, stream(), x, lv.op->mask());
 }
 

@@ -124,6 +124,7 @@ class Hierarchy {
   int pre_ = 1, post_ = 1, degree_ = 2, coarse_mode_ = 0;
   Partition* part_ = nullptr;
   int global_faces_ = 0;
+  cudaStream_t side_ = nullptr;  // partitioned: the overlapped interface exchange
   DotWorkspace ws_;
   // Partitioned coarse level (the replicated fallback of SURVEY.md §8(e)):
   // the global p = 1 matrix summed from the blocks' assembled matrices (one
