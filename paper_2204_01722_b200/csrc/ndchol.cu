@@ -31,8 +31,14 @@ namespace hxg {
 
 namespace {
 
-constexpr int kLeafNodes = 128;
-constexpr int kLaneDepth = 4;
+#ifndef HXG_ND_LEAF
+#define HXG_ND_LEAF 256
+#endif
+constexpr int kLeafNodes = HXG_ND_LEAF;
+#ifndef HXG_ND_LANE_DEPTH
+#define HXG_ND_LANE_DEPTH 4
+#endif
+constexpr int kLaneDepth = HXG_ND_LANE_DEPTH;
 #ifndef HXG_CHOL_BASE
 #define HXG_CHOL_BASE 512
 #endif
