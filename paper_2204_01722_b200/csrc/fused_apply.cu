@@ -112,10 +112,16 @@ __host__ __device__ constexpr int pf_mode(int q) {
 #define HXG_FIXUP_THREADS 128
 #endif
 constexpr int kFixupThreads = HXG_FIXUP_THREADS;
-#ifndef HXG_FIXUP_MINB
-#define HXG_FIXUP_MINB 1
+#ifndef HXG_FIXUP_LD
+#define HXG_FIXUP_LD 0  // partial loads: 0 L1 no-allocate + L2 evict-first, 1 read-only path, 2 plain
 #endif
-constexpr int kFixupMaxGrid = 148 * 64;
+#ifndef HXG_FIXUP_MINB
+#define HXG_FIXUP_MINB 8  // 64 registers: 8 CTAs per SM (Q2 64^3 apply 316.9 -> 310.4 us)
+#endif
+#ifndef HXG_FIXUP_MAXGRID
+#define HXG_FIXUP_MAXGRID (148 * 64)
+#endif
+constexpr int kFixupMaxGrid = HXG_FIXUP_MAXGRID;
 
 struct FusedParams {
   BoxDev box;
@@ -931,7 +937,8 @@ __global__ void __launch_bounds__(kFixupThreads, HXG_FIXUP_MINB) fused_fixup_ker
           const double* a = base - (long long)(o0 + lay.nb[0] * (o1 + lay.nb[1] * o2)) * (D::NB * 3) +
                             3 * ((o2 * PB2 * D::NBY + o1 * PB1) * D::NBX + o0 * PB0);
 #pragma unroll
-          for (int c = 0; c < 3; ++c) v[q][c] = ld_once(a + c, pol);
+          for (int c = 0; c < 3; ++c)
+            v[q][c] = HXG_FIXUP_LD == 1 ? __ldg(a + c) : HXG_FIXUP_LD == 2 ? a[c] : ld_once(a + c, pol);
         }
       }
       const int gx = gx0 + ix, gy = gy0 + iy, gz = gz0 + iz;
