@@ -9,6 +9,7 @@
 
 #include "dispatch.hpp"
 #include "ndchol.hpp"
+#include "solver.hpp"
 
 namespace hxg {
 
@@ -168,10 +169,13 @@ void CoarseAssembly::numeric(Operator& op) {
     constexpr int P = decltype(Pc)::value, M = 3 * (P + 1) * (P + 1) * (P + 1);
     size_t need = (size_t)op.num_elements() * M * M;
     if (elem_.n != need) elem_.alloc(need);
+    PhaseTimer pt(op.stream());
     op.element_matrices(elem_.p);
+    pt.mark("  element matrices");
     long long nnz = a_.nnz();
     fill_csr_kernel<P><<<grid_for(nnz, 256), 256, 0, op.stream()>>>(box_, a_.rows.p, a_.cols.p,
                                                                      mask_.p, elem_.p, nnz, a_.vals.p);
+    pt.mark("  slot sums (fill csr)");
   });
   HXG_CUDA(cudaGetLastError());
 }

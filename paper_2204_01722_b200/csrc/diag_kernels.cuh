@@ -92,13 +92,29 @@ __global__ void diag_element_kernel(DiagParams prm) {
     sI[r] = prm.interp[r];
     sDv[r] = prm.deriv[r];
   }
-  for (int qpt = threadIdx.x; qpt < Q3; qpt += blockDim.x) {
-    double d81[81];
-    point_tensor(prm, e, qpt, d81);
-    for (int c = 0; c < 3; ++c)
-      for (int d1 = 0; d1 < 3; ++d1)
-        for (int d2 = 0; d2 < 3; ++d2)
-          sT[qpt * 27 + (c * 3 + d1) * 3 + d2] = d81[(c * 3 + d1) * 9 + c * 3 + d2];
+  // one q-function probe per thread (point, column u = (c, d2)): the
+  // diagonal blocks need D[(c, d1), (c, d2)], i.e. rows c of every column
+  const int S = device_state_stride(prm.storage);
+  for (int w = threadIdx.x; w < Q3 * 9; w += blockDim.x) {
+    const int qpt = w / 9, u = w - 9 * qpt, c = u / 3, d2 = u - 3 * c;
+    const long long off = state_offset(prm.lay, e, qpt, S);
+    double st[kMaxStateStride];
+    for (int s = 0; s < S; ++s) st[s] = prm.state[off + state_pair_off(s, prm.lay.T, prm.lay.Q)];
+    double G[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, H[9];
+    G[u] = 1.0;
+    switch (prm.storage) {
+      case kStorageInitialNative: jacobian_qf_initial<kStorageInitialNative>(prm.mu, prm.lambda, G, st, H); break;
+      case kStorageInitialTuned: jacobian_qf_initial<kStorageInitialTuned>(prm.mu, prm.lambda, G, st, H); break;
+      case kStorageInitialAD: jacobian_qf_initial<kStorageInitialAD>(prm.mu, prm.lambda, G, st, H); break;
+      default: jacobian_qf(prm.mu, prm.lambda, G, st, H);
+    }
+    if (prm.perturb != 0.0) {  // + eps w detJ G (as point_tensor)
+      const long long T = prm.lay.T, row = off / T / state_row(S, prm.lay.Q);
+      const long long t = state_paired(prm.lay.Q) ? (off % (2 * T)) / 2 : off % T;
+      H[u] += prm.perturb * prm.geo[(row * kGeoStride + 9) * T + t];
+    }
+#pragma unroll
+    for (int d1 = 0; d1 < 3; ++d1) sT[qpt * 27 + (c * 3 + d1) * 3 + d2] = H[c * 3 + d1];
   }
   __syncthreads();
   for (int r = threadIdx.x; r < 3 * N3; r += blockDim.x) {
@@ -152,40 +168,41 @@ __global__ void assemble_element_kernel(DiagParams prm) {
 }
 
 // p = 1 element matrices (the coarse level's, coo_numeric assembly.hpp:
-// 188-230), two-stage: per chunk of points, D_q by one q-function probe per
-// thread (point, column), T[q][(ca,i)][(b,cb)] = sum_j D_q[(ca,i),(cb,j)]
-// g_b,j(q), then K[(a,ca),(b,cb)] += sum_q sum_i g_a,i(q) T[q][(ca,i)][(b,cb)]
-// (each thread owns two entries of K).  ~90 k flops per element instead of
-// the generic kernel's ~500 k.
+// 188-230): K[(a,ca),(b,cb)] = sum_q sum_i g_a,i(q) sum_j D_q[(ca,i),(cb,j)]
+// g_b,j(q).  Per chunk of points, D_q by one q-function probe per thread
+// (point, column) and the node gradients into shared memory; then thread
+// (point group, column (ca, b, cb)) forms t_i = sum_j D_q[(ca,i),(cb,j)] g_b,j
+// and accumulates all 8 rows a (the g_a,i are warp-uniform broadcasts); the
+// 4 point groups are reduced in fixed order.  ~40 k flops per element and no
+// materialised intermediate (shared-memory traffic was the limiter).
 constexpr int kQ1AsmThreads = 288;
 constexpr int kQ1AsmChunk = 27;
-template <int Q>
-__global__ void __launch_bounds__(kQ1AsmThreads) assemble_element_q1_kernel(DiagParams prm) {
+template <int Q, int ST>
+__global__ void __launch_bounds__(kQ1AsmThreads, 2) assemble_element_q1_kernel(DiagParams prm) {
   constexpr int N = 2, N3 = 8, Q3 = Q * Q * Q, M = 3 * N3, QC = kQ1AsmChunk;
   extern __shared__ double smem[];
-  double* sD = smem;              // QC x 81
+  double* sD = smem;              // QC x 81; reused for the group reduction
   double* sG = sD + QC * 81;      // QC x 8 x 3
-  double* sT = sG + QC * N3 * 3;  // QC x 9 x 24
   const long long e = blockIdx.x;
   const int tid = threadIdx.x;
-  const int S = device_state_stride(prm.storage);
-  double acc[2] = {0.0, 0.0};
+  constexpr int S = device_state_stride(ST);
+  const int combo = tid % 72, grp = tid / 72;  // 72 columns (ca, b, cb) x 4 point groups
+  const int ca = combo / 24, bc = combo - 24 * ca, b = bc / 3, cb = bc - 3 * b;
+  double acc[N3] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int q0 = 0; q0 < Q3; q0 += QC) {
     const int qn = Q3 - q0 < QC ? Q3 - q0 : QC;
-    // D_q columns: one probe per (point, u)
-    for (int w = tid; w < qn * 9; w += kQ1AsmThreads) {
+    for (int w = tid; w < qn * 9; w += kQ1AsmThreads) {  // D_q column u of point ql
       const int ql = w / 9, u = w - 9 * ql, qpt = q0 + ql;
       const long long off = state_offset(prm.lay, e, qpt, S);
-      double st[kMaxStateStride];
+      double st[S];
+#pragma unroll
       for (int s = 0; s < S; ++s) st[s] = prm.state[off + state_pair_off(s, prm.lay.T, prm.lay.Q)];
       double G[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, H[9];
       G[u] = 1.0;
-      switch (prm.storage) {
-        case kStorageInitialNative: jacobian_qf_initial<kStorageInitialNative>(prm.mu, prm.lambda, G, st, H); break;
-        case kStorageInitialTuned: jacobian_qf_initial<kStorageInitialTuned>(prm.mu, prm.lambda, G, st, H); break;
-        case kStorageInitialAD: jacobian_qf_initial<kStorageInitialAD>(prm.mu, prm.lambda, G, st, H); break;
-        default: jacobian_qf(prm.mu, prm.lambda, G, st, H);
-      }
+      if constexpr (ST == kStorageCurrent)
+        jacobian_qf(prm.mu, prm.lambda, G, st, H);
+      else
+        jacobian_qf_initial<ST>(prm.mu, prm.lambda, G, st, H);
       if (prm.perturb != 0.0) {  // + eps w detJ G (as point_tensor)
         const long long T = prm.lay.T, row = off / T / state_row(S, prm.lay.Q);
         const long long t = state_paired(prm.lay.Q) ? (off % (2 * T)) / 2 : off % T;
@@ -206,30 +223,34 @@ __global__ void __launch_bounds__(kQ1AsmThreads) assemble_element_q1_kernel(Diag
       sG[(ql * N3 + a) * 3 + 2] = bi * bj * dk;
     }
     __syncthreads();
-    for (int w = tid; w < qn * 9 * M; w += kQ1AsmThreads) {
-      const int ql = w / (9 * M), r = w - ql * 9 * M, ki = r / M, bc = r - ki * M;
-      const int b = bc / 3, cb = bc - 3 * b;
-      const double* d = sD + ql * 81 + ki * 9 + cb * 3;
+    for (int ql = grp; ql < qn; ql += 4) {
+      const double* d = sD + ql * 81 + (ca * 3) * 9 + cb * 3;
       const double* gb = sG + (ql * N3 + b) * 3;
-      sT[w] = d[0] * gb[0] + d[1] * gb[1] + d[2] * gb[2];
-    }
-    __syncthreads();
+      const double g0 = gb[0], g1 = gb[1], g2 = gb[2];
+      const double t0 = d[0] * g0 + d[1] * g1 + d[2] * g2;
+      const double t1 = d[9] * g0 + d[10] * g1 + d[11] * g2;
+      const double t2 = d[18] * g0 + d[19] * g1 + d[20] * g2;
+      const double* g = sG + ql * N3 * 3;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int idx = tid + h * kQ1AsmThreads;  // (a ca) * 24 + (b cb)
-      const int rowi = idx / M, bc = idx - rowi * M, a = rowi / 3, ca = rowi - 3 * a;
-      double s = 0.0;
-      for (int ql = 0; ql < qn; ++ql) {
-        const double* ga = sG + (ql * N3 + a) * 3;
-        const double* t = sT + ql * 9 * M + (ca * 3) * M + bc;
-        s += ga[0] * t[0] + ga[1] * t[M] + ga[2] * t[2 * M];
-      }
-      acc[h] += s;
+      for (int a = 0; a < N3; ++a) acc[a] += g[a * 3 + 0] * t0 + g[a * 3 + 1] * t1 + g[a * 3 + 2] * t2;
     }
     __syncthreads();
   }
-  prm.out[e * (long long)(M * M) + tid] = acc[0];
-  prm.out[e * (long long)(M * M) + tid + kQ1AsmThreads] = acc[1];
+  // reduce the 4 point groups in fixed order ([grp][combo][a] over the D + G buffers)
+  double* red = sD;
+#pragma unroll
+  for (int a = 0; a < N3; ++a) red[(grp * 72 + combo) * N3 + a] = acc[a];
+  __syncthreads();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int idx = tid + h * kQ1AsmThreads;  // (a ca) * 24 + (b cb)
+    const int rowi = idx / M, col = idx - rowi * M, a = rowi / 3, car = rowi - 3 * a;
+    const int cmb = car * 24 + col;
+    double v = 0.0;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) v += red[(g * 72 + cmb) * N3 + a];
+    prm.out[e * (long long)(M * M) + idx] = v;
+  }
 }
 
 }  // namespace hxg

@@ -508,13 +508,14 @@ void HmgCoarse::setup(const CsrMatrix& a0, const BoxDev& box0, const std::vector
       HLevel& bl = *levels_.back();
       rep_ = std::make_unique<Replicated>();
       rep_->symbolic(*part_, bl.lat, *bl.A, bl.mask_h, s);
-      if (rep_->global->matrix().n > 4 * kHmgBottomMax)
+      if (rep_->global->matrix().n > kHmgBottomLimit)
         throw Error(HXG_ERR_UNSUPPORTED, "h-multigrid coarse mode: bottom level too large (block "
                                          "cells odd early: use even block sizes)");
-    } else if (levels_.back()->n() > 4 * kHmgBottomMax) {
+    } else if (levels_.back()->n() > kHmgBottomLimit) {
       throw Error(HXG_ERR_UNSUPPORTED, "h-multigrid coarse mode: bottom level too large (thin box)");
     }
   }
+  PhaseTimer pt(s);
   // numeric: Galerkin element matrices + slot sums, level by level
   for (size_t l = 0; l + 1 < levels_.size(); ++l) {
     HLevel& f = *levels_[l];
@@ -524,6 +525,7 @@ void HmgCoarse::setup(const CsrMatrix& a0, const BoxDev& box0, const std::vector
     HXG_CUDA(cudaGetLastError());
     c.asmb->numeric_from_elements(c.elem.p, s);
   }
+  pt.mark("  hmg galerkin + assembly");
   // stencil forms of the smoothed levels (their SpMV has no column indices)
   for (size_t l = 0; l + 1 < levels_.size(); ++l) {
     HLevel& lv = *levels_[l];
@@ -534,6 +536,7 @@ void HmgCoarse::setup(const CsrMatrix& a0, const BoxDev& box0, const std::vector
                                                               lv.A->vals.p, nnz, n, lv.st.p);
     HXG_CUDA(cudaGetLastError());
   }
+  pt.mark("  hmg stencils");
   // smoothers on every level above the bottom
   for (size_t l = 0; l + 1 < levels_.size(); ++l) {
     HLevel& lv = *levels_[l];
@@ -556,10 +559,12 @@ void HmgCoarse::setup(const CsrMatrix& a0, const BoxDev& box0, const std::vector
           return part_ ? part_->global_seed_slice(lv.lat, lv.mask_h) : rough_seed(n, lv.mask_h);
         });
   }
+  pt.mark("  hmg smoothers");
   if (part_)
     rep_->numeric(*part_, *levels_.back()->A, s);
   else
     bottom_.factorize(*levels_.back()->A, s);
+  pt.mark("  hmg bottom inverse");
   ready_ = true;
 }
 

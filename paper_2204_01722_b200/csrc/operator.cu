@@ -371,10 +371,21 @@ void Operator::element_matrices(double* out) {
   if (p_ == 1) {  // the coarse level: two-stage contraction
     dispatch_q(q_, [&](auto Qc) {
       constexpr int Q = decltype(Qc)::value;
-      constexpr size_t smem = sizeof(double) * kQ1AsmChunk * (81 + 24 + 9 * 24);
-      auto k = assemble_element_q1_kernel<Q>;
-      HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k<<<(unsigned)num_elements(), kQ1AsmThreads, smem, stream_>>>(prm);
+      // D (and the 4 x 72 x 8 group reduction) + node gradients
+      constexpr size_t smem = sizeof(double) * (kQ1AsmChunk * 81 + kQ1AsmChunk * 24);
+      static_assert(kQ1AsmChunk * (81 + 24) >= 4 * 72 * 8, "reduction fits the D + G buffers");
+      auto launch = [&](auto k) {
+        HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      cudaSharedmemCarveoutMaxShared));
+        k<<<(unsigned)num_elements(), kQ1AsmThreads, smem, stream_>>>(prm);
+      };
+      switch (storage_) {
+        case kStorageInitialNative: launch(assemble_element_q1_kernel<Q, kStorageInitialNative>); break;
+        case kStorageInitialTuned: launch(assemble_element_q1_kernel<Q, kStorageInitialTuned>); break;
+        case kStorageInitialAD: launch(assemble_element_q1_kernel<Q, kStorageInitialAD>); break;
+        default: launch(assemble_element_q1_kernel<Q, kStorageCurrent>);
+      }
     });
     HXG_CUDA(cudaGetLastError());
     return;

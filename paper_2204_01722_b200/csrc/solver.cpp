@@ -48,27 +48,6 @@ KrylovWork& krylov_work(size_t n) {
   return *pool->back().second;
 }
 
-// HXG_PROFILE=1: print the phases of setup_numeric (device-synchronised).
-struct PhaseTimer {
-  bool on;
-  cudaStream_t s;
-  std::chrono::steady_clock::time_point t;
-  explicit PhaseTimer(cudaStream_t st) : on(std::getenv("HXG_PROFILE") != nullptr), s(st) {
-    if (on) {
-      cudaStreamSynchronize(s);
-      t = std::chrono::steady_clock::now();
-    }
-  }
-  void mark(const char* what) {
-    if (!on) return;
-    cudaStreamSynchronize(s);
-    auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[hxg] %-28s %9.2f ms\n", what,
-                 std::chrono::duration<double, std::milli>(now - t).count());
-    t = now;
-  }
-};
-
 int sturm_count(const std::vector<double>& d, const std::vector<double>& e, double x) {
   int count = 0;
   double q = 1.0;
@@ -230,10 +209,13 @@ void Chebyshev::create(long long n, cudaStream_t s, int degree_, const DevOp& A,
     d.alloc((size_t)n);
     seed.upload(seed_fn());
   }
+  PhaseTimer pt(s);
   diag(d.p);  // d doubles as the diagonal scratch here
   if (!vreciprocal(inv_diag.p, d.p, n, s))
     throw Error(HXG_ERR_INVALID_SMOOTHER, "invalid smoother: zero diagonal entry");
+  pt.mark("  smoother diagonal");
   lambda_max = estimate_lambda_max(n, A, inv_diag.p, seed.p, 10, s, dotf);
+  pt.mark("  smoother lambda_max");
   lo = 0.1 * lambda_max;
   hi = 1.1 * lambda_max;
   ready = true;

@@ -4,6 +4,9 @@
 // come back to the host once per reduction, as in the reference.
 #pragma once
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <functional>
 #include <memory>
 #include <vector>
@@ -15,6 +18,27 @@
 #include "vector.hpp"
 
 namespace hxg {
+
+// HXG_PROFILE=1: print the phases of setup_numeric (device-synchronised).
+struct PhaseTimer {
+  bool on;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTimer(cudaStream_t st) : on(std::getenv("HXG_PROFILE") != nullptr), s(st) {
+    if (on) {
+      cudaStreamSynchronize(s);
+      t = std::chrono::steady_clock::now();
+    }
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hxg] %-28s %9.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 // LinearOperator (cg.hpp:16-19) over device vectors.
 using DevOp = std::function<void(const double*, double*)>;
