@@ -32,9 +32,11 @@ Error indefinite(double curvature) {
 // process-wide pool is enough.
 struct KrylovWork {
   DevBuf<double> v[5];
+  DevBuf<double> sc;  // device scalars of the Lanczos recurrence
   DotWorkspace ws;
   explicit KrylovWork(size_t n) {
     for (auto& b : v) b.alloc(n);
+    sc.alloc(128);
   }
 };
 KrylovWork& krylov_work(size_t n) {
@@ -173,9 +175,44 @@ double estimate_lambda_max(long long n, const DevOp& a, const double* inv_diag,
   vzero(x.p, n, s);
   vcopy(r.p, seed, n, s);
   vscale_mul(z.p, inv_diag, r.p, n, s);
-  double rz = dot(r.p, z.p, n, ws, s);
   std::vector<double> alphas, betas;
   double eig_min = 0.0, eig_max = 1.0;
+  if (!dotf && 2 * iterations + 1 <= (int)w.sc.n) {
+    // One process: the recurrence runs on device scalars (rz_k = sc[2k],
+    // p^T A p = sc[2k + 1]) and the host reads them once at the end,
+    // replaying the same breaks -- the same operations, no per-step syncs.
+    double* sc = w.sc.p;
+    dot_to(r.p, z.p, n, ws, sc, s);
+    vcopy(p.p, z.p, n, s);
+    for (int it = 0; it < iterations; ++it) {
+      a(p.p, ap.p);
+      dot_to(p.p, ap.p, n, ws, sc + 2 * it + 1, s);
+      cg_update_xr_dev(x.p, r.p, p.p, ap.p, sc + 2 * it, sc + 2 * it + 1, n, s);
+      vscale_mul(z.p, inv_diag, r.p, n, s);
+      dot_to(r.p, z.p, n, ws, sc + 2 * it + 2, s);
+      cg_update_p_dev(p.p, z.p, sc + 2 * it + 2, sc + 2 * it, n, s);
+    }
+    std::vector<double> h((size_t)(2 * iterations + 1));
+    HXG_CUDA(cudaMemcpyAsync(h.data(), sc, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+    HXG_CUDA(cudaStreamSynchronize(s));
+    double rz = h[0];
+    if (rz <= 0.0) return eig_max;
+    for (int it = 0; it < iterations; ++it) {
+      const double pap = h[(size_t)(2 * it + 1)];
+      if (pap <= 0.0) break;
+      alphas.push_back(rz / pap);
+      const double rz_new = h[(size_t)(2 * it + 2)];
+      if (rz_new <= 0.0) break;
+      if (it + 1 < iterations) betas.push_back(rz_new / rz);
+      rz = rz_new;
+    }
+    if (!alphas.empty()) {
+      betas.resize(alphas.size() - 1);
+      lanczos_eigs(alphas, betas, eig_min, eig_max);
+    }
+    return eig_max;
+  }
+  double rz = dot(r.p, z.p, n, ws, s);
   if (rz <= 0.0) return eig_max;
   vcopy(p.p, z.p, n, s);
   for (int it = 0; it < iterations; ++it) {

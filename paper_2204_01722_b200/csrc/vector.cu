@@ -96,6 +96,20 @@ __global__ void k_cg_xr(double* x, double* r, const double* p, const double* ap,
 __global__ void k_cg_p(double* p, const double* z, double beta, long long n) {
   GRID_STRIDE(i, n) p[i] = z[i] + beta * p[i];
 }
+// the same updates with the coefficient num / den read from device scalars
+__global__ void k_cg_xr_dev(double* x, double* r, const double* p, const double* ap,
+                            const double* num, const double* den, long long n) {
+  const double alpha = *num / *den;
+  GRID_STRIDE(i, n) {
+    x[i] += alpha * p[i];
+    r[i] -= alpha * ap[i];
+  }
+}
+__global__ void k_cg_p_dev(double* p, const double* z, const double* num, const double* den,
+                           long long n) {
+  const double beta = *num / *den;
+  GRID_STRIDE(i, n) p[i] = z[i] + beta * p[i];
+}
 __global__ void k_cheb_first(double* x, double* r, double* d, const double* b, const double* inv,
                              double theta, long long n) {
   GRID_STRIDE(i, n) {
@@ -160,6 +174,20 @@ double* dot_masked_device(const double* x, const double* y, const uint8_t* mask,
     dot_stage1<<<kDotBlocks, kDotThreads, 0, s>>>(x, y, n, ws.partial);
   dot_stage2<<<1, kDotThreads, 0, s>>>(ws.partial, kDotBlocks, ws.partial + kDotBlocks + slot);
   return ws.partial + kDotBlocks + slot;
+}
+
+void dot_to(const double* x, const double* y, long long n, DotWorkspace& ws, double* out,
+            cudaStream_t s) {
+  dot_stage1<<<kDotBlocks, kDotThreads, 0, s>>>(x, y, n, ws.partial);
+  dot_stage2<<<1, kDotThreads, 0, s>>>(ws.partial, kDotBlocks, out);
+}
+void cg_update_xr_dev(double* x, double* r, const double* p, const double* ap, const double* num,
+                      const double* den, long long n, cudaStream_t s) {
+  k_cg_xr_dev<<<grid(n), 256, 0, s>>>(x, r, p, ap, num, den, n);
+}
+void cg_update_p_dev(double* p, const double* z, const double* num, const double* den, long long n,
+                     cudaStream_t s) {
+  k_cg_p_dev<<<grid(n), 256, 0, s>>>(p, z, num, den, n);
 }
 
 double dot(const double* x, const double* y, long long n, DotWorkspace& ws, cudaStream_t s) {

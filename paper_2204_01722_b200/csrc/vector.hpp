@@ -21,6 +21,14 @@ struct DotWorkspace {
 // Launches the dot; result lands in ws.host[slot] after a stream sync.
 void dot_async(const double* x, const double* y, long long n, DotWorkspace& ws, int slot,
                cudaStream_t s);
+// x . y into the device scalar *out (same fixed-order reduction), no sync.
+void dot_to(const double* x, const double* y, long long n, DotWorkspace& ws, double* out,
+            cudaStream_t s);
+// CG updates with alpha = *num / *den, beta = *num / *den read on the device.
+void cg_update_xr_dev(double* x, double* r, const double* p, const double* ap, const double* num,
+                      const double* den, long long n, cudaStream_t s);
+void cg_update_p_dev(double* p, const double* z, const double* num, const double* den, long long n,
+                     cudaStream_t s);
 // Synchronous convenience: returns x . y.
 double dot(const double* x, const double* y, long long n, DotWorkspace& ws, cudaStream_t s);
 
