@@ -543,29 +543,19 @@ int hxg_pointer_is_device(const void* p, int* is_device) {
     *is_device = a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
   });
 }
-// Host-staged copies for caller communicators: complete on return (a
-// pageable H2D cudaMemcpy may return before its DMA lands) and independent of
-// the legacy default stream, so they neither race nor serialise with the
-// library's non-blocking streams.
-static cudaStream_t staging_stream() {
-  static cudaStream_t s = [] {
-    cudaStream_t t = nullptr;
-    HXG_CUDA(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
-    return t;
-  }();
-  return s;
-}
+// Host-staged copies (caller communicators, the C++ wrapper's host spans):
+// ordered after earlier work like cudaMemcpy on the legacy default stream,
+// and complete on return -- a pageable H2D cudaMemcpy may return before its
+// DMA lands, and the library's side stream (overlapped exchange) is
+// non-blocking, so the H2D also waits for the legacy stream.
 int hxg_memcpy_h2d(void* dst, const void* src, size_t bytes) {
   return guarded([&] {
-    HXG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, staging_stream()));
-    HXG_CUDA(cudaStreamSynchronize(staging_stream()));
+    HXG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    HXG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
   });
 }
 int hxg_memcpy_d2h(void* dst, const void* src, size_t bytes) {
-  return guarded([&] {
-    HXG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, staging_stream()));
-    HXG_CUDA(cudaStreamSynchronize(staging_stream()));
-  });
+  return guarded([&] { HXG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)); });
 }
 int hxg_device_synchronize(void) { return guarded([&] { HXG_CUDA(cudaDeviceSynchronize()); }); }
 
