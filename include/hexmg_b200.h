@@ -166,8 +166,8 @@ int hxg_mg_setup_numeric(hxg_mg_t mg);
  * hxg_mg_coarse_csr_host). */
 int hxg_mg_assemble_coarse(hxg_mg_t mg);
 /* Coarse Cholesky backend: 0 automatic (dense below a few thousand DoFs,
- * else nested-dissection multifrontal), 1 dense, 2 nested-dissection
- * multifrontal, 3 cuSOLVER csrchol on the ND-permuted matrix.  Takes effect
+ * else nested-dissection multifrontal), 1 dense (one front), 2
+ * nested-dissection multifrontal (3 is no longer accepted).  Takes effect
  * at the next setup_numeric.  4 = INEXACT coarse mode, a documented
  * deviation from the reference's exact SimplicialLLT (coarse_solver.hpp:
  * 16-47): the p = 1 level is solved by one Galerkin h-multigrid V-cycle

@@ -332,8 +332,8 @@ int hxg_mg_setup_numeric(hxg_mg_t mg) { return guarded([&] { MG(mg).setup_numeri
 int hxg_mg_assemble_coarse(hxg_mg_t mg) { return guarded([&] { MG(mg).assemble_coarse(); }); }
 int hxg_mg_set_coarse_mode(hxg_mg_t mg, int mode) {
   return guarded([&] {
-    if (mode < 0 || mode > 4)
-      throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "coarse mode must be 0, 1, 2, 3 or 4");
+    if (mode < 0 || mode > 4 || mode == 3)
+      throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "coarse mode must be 0, 1, 2 or 4");
     MG(mg).set_coarse_mode(mode);
   });
 }
@@ -630,6 +630,8 @@ int hxg_chol_create(int n, const int* row_ptr, const int* cols, const int npd[3]
     h->a.rows.upload(rows);
     h->a.vals.alloc((size_t)row_ptr[n]);
     for (int d = 0; d < 3; ++d) h->npd[d] = npd[d];
+    if (mode < 0 || mode > 2)
+      throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "coarse Cholesky mode must be 0, 1 or 2");
     h->solver.set_mode(mode);
     *out = h.release();
   });

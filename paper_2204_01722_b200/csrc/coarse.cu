@@ -1,9 +1,5 @@
 #include "coarse.hpp"
 
-#include <cusolverDn.h>
-#include <cusolverSp.h>
-#include <cusolverSp_LOWLEVEL_PREVIEW.h>
-#include <cusparse.h>
 
 #include <algorithm>
 
@@ -199,253 +195,53 @@ void csr_matvec(const CsrMatrix& a, const double* x, double* y, cudaStream_t s) 
 void CoarseAssembly::matvec(const double* x, double* y, cudaStream_t s) const { csr_matvec(a_, x, y, s); }
 
 // ---------------------------------------------------------------------------
-// Dense device Cholesky for coarse levels that fit (cuSOLVER potrf/potrs).
+// Dense coarse mode: the multifrontal solver with one front holding the whole
+// lattice (dense_chol_inv factor + inverse, GEMV solves; ndchol.cu).
 
 class CoarseSolverImpl {
  public:
-  ~CoarseSolverImpl() {
-    if (handle_) cusolverDnDestroy(handle_);
-  }
-  void factorize(const CsrMatrix& a, cudaStream_t s) {
-    n_ = a.n;
-    size_t bytes = (size_t)n_ * n_ * sizeof(double);
-    if (bytes > (size_t)48 << 30)
-      throw Error(HXG_ERR_UNSUPPORTED, "coarse problem too large for the dense factorization");
-    if (!handle_) {
-      if (cusolverDnCreate(&handle_) != CUSOLVER_STATUS_SUCCESS)
-        throw Error(HXG_ERR_CUDA, "cusolverDnCreate failed");
-    }
-    cusolverDnSetStream(handle_, s);
-    if (dense_.n != (size_t)n_ * n_) dense_.alloc((size_t)n_ * n_);
-    HXG_CUDA(cudaMemsetAsync(dense_.p, 0, bytes, s));
-    csr_to_dense_kernel<<<grid_for(a.nnz(), 256), 256, 0, s>>>(a.rows.p, a.cols.p, a.vals.p,
-                                                              a.nnz(), n_, dense_.p);
-    HXG_CUDA(cudaGetLastError());
-    int lwork = 0;
-    if (cusolverDnDpotrf_bufferSize(handle_, CUBLAS_FILL_MODE_LOWER, n_, dense_.p, n_, &lwork) !=
-        CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "potrf_bufferSize failed");
-    if (work_.n < (size_t)lwork) work_.alloc((size_t)lwork);
-    if (info_.n == 0) info_.alloc(1);
-    if (cusolverDnDpotrf(handle_, CUBLAS_FILL_MODE_LOWER, n_, dense_.p, n_, work_.p, lwork,
-                         info_.p) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "potrf failed");
-    int info = 0;
-    HXG_CUDA(cudaMemcpyAsync(&info, info_.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    HXG_CUDA(cudaStreamSynchronize(s));
-    if (info != 0) {
-      ready_ = false;
-      throw Error(HXG_ERR_NOT_SPD, "factorization failed, matrix not SPD: coarse Cholesky "
-                                   "factorization failed at level 0");
-    }
-    ready_ = true;
-  }
-  void solve(const double* b, double* x, cudaStream_t s) {
-    if (!ready_) throw Error(HXG_ERR_GENERIC, "coarse solver not factorized");
-    if (x != b) HXG_CUDA(cudaMemcpyAsync(x, b, sizeof(double) * n_, cudaMemcpyDeviceToDevice, s));
-    cusolverDnSetStream(handle_, s);
-    if (cusolverDnDpotrs(handle_, CUBLAS_FILL_MODE_LOWER, n_, 1, dense_.p, n_, x, n_, info_.p) !=
-        CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "potrs failed");
-  }
-  bool ready() const { return ready_; }
-
- private:
-  cusolverDnHandle_t handle_ = nullptr;
-  int n_ = 0;
-  bool ready_ = false;
-  DevBuf<double> dense_, work_;
-  DevBuf<int> info_;
-};
-
-// ---------------------------------------------------------------------------
-// Sparse device Cholesky for larger coarse levels: geometric nested dissection
-// of the Q1 node lattice (host, once per pattern), the permuted CSR refilled
-// on device by a gather, and cuSOLVER's device csrchol (symbolic once,
-// numeric per setup, triangular solves per V-cycle).
-
-namespace {
-
-// Nested-dissection order (new -> old) of the nx x ny x nz node lattice:
-// split the longest axis at its middle plane; order left, right, separator.
-void nd_nodes(const int npd[3], int lo0, int hi0, int lo1, int hi1, int lo2, int hi2,
-              std::vector<int>& order) {
-  const int n[3] = {hi0 - lo0, hi1 - lo1, hi2 - lo2};
-  if (n[0] <= 0 || n[1] <= 0 || n[2] <= 0) return;
-  const long long cnt = (long long)n[0] * n[1] * n[2];
-  int ax = 0;
-  if (n[1] > n[ax]) ax = 1;
-  if (n[2] > n[ax]) ax = 2;
-  if (cnt <= 64 || n[ax] < 3) {
-    for (int z = lo2; z < hi2; ++z)
-      for (int y = lo1; y < hi1; ++y)
-        for (int x = lo0; x < hi0; ++x) order.push_back(x + npd[0] * (y + npd[1] * z));
-    return;
-  }
-  int lo[3] = {lo0, lo1, lo2}, hi[3] = {hi0, hi1, hi2};
-  const int mid = lo[ax] + n[ax] / 2;
-  int a_hi[3] = {hi[0], hi[1], hi[2]}, b_lo[3] = {lo[0], lo[1], lo[2]};
-  a_hi[ax] = mid;
-  b_lo[ax] = mid + 1;
-  nd_nodes(npd, lo[0], a_hi[0], lo[1], a_hi[1], lo[2], a_hi[2], order);
-  nd_nodes(npd, b_lo[0], hi[0], b_lo[1], hi[1], b_lo[2], hi[2], order);
-  int s_lo[3] = {lo[0], lo[1], lo[2]}, s_hi[3] = {hi[0], hi[1], hi[2]};
-  s_lo[ax] = mid;
-  s_hi[ax] = mid + 1;
-  for (int z = s_lo[2]; z < s_hi[2]; ++z)
-    for (int y = s_lo[1]; y < s_hi[1]; ++y)
-      for (int x = s_lo[0]; x < s_hi[0]; ++x) order.push_back(x + npd[0] * (y + npd[1] * z));
-}
-
-__global__ void gather_kernel(const double* __restrict__ src, const int* __restrict__ idx,
-                              long long n, double* __restrict__ dst) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    dst[i] = src[idx[i]];
-}
-
-__global__ void scatter_kernel(const double* __restrict__ src, const int* __restrict__ idx,
-                               long long n, double* __restrict__ dst) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    dst[idx[i]] = src[i];
-}
-
-}  // namespace
-
-class SparseCholeskyImpl {
- public:
-  ~SparseCholeskyImpl() {
-    if (info_) cusolverSpDestroyCsrcholInfo(info_);
-    if (descr_) cusparseDestroyMatDescr(descr_);
-    if (handle_) cusolverSpDestroy(handle_);
-  }
   void factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s) {
-    if (!handle_) {
-      if (cusolverSpCreate(&handle_) != CUSOLVER_STATUS_SUCCESS)
-        throw Error(HXG_ERR_CUDA, "cusolverSpCreate failed");
-      cusparseCreateMatDescr(&descr_);
-      cusparseSetMatType(descr_, CUSPARSE_MATRIX_TYPE_GENERAL);
-      cusparseSetMatIndexBase(descr_, CUSPARSE_INDEX_BASE_ZERO);
-    }
-    cusolverSpSetStream(handle_, s);
-    if (!analyzed_) analyze(a, npd);
-    const long long nnz = a.nnz();
-    gather_kernel<<<grid_for(nnz, 256), 256, 0, s>>>(a.vals.p, slot_.p, nnz, pvals_.p);
-    HXG_CUDA(cudaGetLastError());
-    if (cusolverSpDcsrcholFactor(handle_, n_, (int)nnz, descr_, pvals_.p, prow_.p, pcol_.p,
-                                 info_, buffer_.p) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "csrcholFactor failed");
-    int pos = -1;
-    if (cusolverSpDcsrcholZeroPivot(handle_, info_, 0.0, &pos) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "csrcholZeroPivot failed");
-    if (pos >= 0) {
-      ready_ = false;
-      throw Error(HXG_ERR_NOT_SPD, "factorization failed, matrix not SPD: coarse Cholesky "
-                                   "factorization failed at level 0");
-    }
-    ready_ = true;
+    if ((size_t)a.n * a.n * sizeof(double) > (size_t)48 << 30)
+      throw Error(HXG_ERR_UNSUPPORTED, "coarse problem too large for the dense factorization");
+    if (!nd_ || n_ != a.n) nd_ = std::make_unique<NdCholesky>((long long)npd[0] * npd[1] * npd[2] + 1);
+    n_ = a.n;
+    nd_->factorize(a, npd, s);
   }
   void solve(const double* b, double* x, cudaStream_t s) {
-    if (!ready_) throw Error(HXG_ERR_GENERIC, "coarse solver not factorized");
-    cusolverSpSetStream(handle_, s);
-    gather_kernel<<<grid_for(n_, 256), 256, 0, s>>>(b, perm_.p, n_, pb_.p);
-    if (cusolverSpDcsrcholSolve(handle_, n_, pb_.p, px_.p, info_, buffer_.p) !=
-        CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "csrcholSolve failed");
-    scatter_kernel<<<grid_for(n_, 256), 256, 0, s>>>(px_.p, perm_.p, n_, x);
-    HXG_CUDA(cudaGetLastError());
+    if (!ready()) throw Error(HXG_ERR_GENERIC, "coarse solver not factorized");
+    nd_->solve(b, x, s);
   }
-  bool ready() const { return ready_; }
+  bool ready() const { return nd_ && nd_->ready(); }
 
  private:
-  void analyze(const CsrMatrix& a, const int npd[3]) {
-    n_ = a.n;
-    std::vector<int> nodes;
-    nodes.reserve((size_t)n_ / 3);
-    nd_nodes(npd, 0, npd[0], 0, npd[1], 0, npd[2], nodes);
-    if ((long long)nodes.size() * 3 != n_) throw Error(HXG_ERR_GENERIC, "ND ordering incomplete");
-    std::vector<int> perm((size_t)n_), inv((size_t)n_);
-    for (size_t k = 0; k < nodes.size(); ++k)
-      for (int c = 0; c < 3; ++c) perm[3 * k + c] = 3 * nodes[k] + c;
-    for (int i = 0; i < n_; ++i) inv[(size_t)perm[(size_t)i]] = i;
-    // Permuted CSR: new row i = old row perm[i], columns mapped by inv, sorted.
-    std::vector<int> prow((size_t)n_ + 1, 0), pcol, slot;
-    pcol.reserve(a.cols_h.size());
-    slot.reserve(a.cols_h.size());
-    std::vector<std::pair<int, int>> tmp;
-    for (int i = 0; i < n_; ++i) {
-      int r = perm[(size_t)i];
-      tmp.clear();
-      for (int k = a.row_ptr_h[(size_t)r]; k < a.row_ptr_h[(size_t)r + 1]; ++k)
-        tmp.emplace_back(inv[(size_t)a.cols_h[(size_t)k]], k);
-      std::sort(tmp.begin(), tmp.end());
-      for (auto& t : tmp) {
-        pcol.push_back(t.first);
-        slot.push_back(t.second);
-      }
-      prow[(size_t)i + 1] = (int)pcol.size();
-    }
-    perm_.upload(perm);
-    prow_.upload(prow);
-    pcol_.upload(pcol);
-    slot_.upload(slot);
-    pvals_.alloc(pcol.size());
-    pb_.alloc((size_t)n_);
-    px_.alloc((size_t)n_);
-    if (cusolverSpCreateCsrcholInfo(&info_) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "csrcholInfo create failed");
-    if (cusolverSpXcsrcholAnalysis(handle_, n_, (int)pcol.size(), descr_, prow_.p, pcol_.p,
-                                   info_) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "csrcholAnalysis failed");
-    size_t internal = 0, work = 0;
-    // BufferInfo needs values; a gather of the current ones gives valid data.
-    gather_kernel<<<grid_for((long long)pcol.size(), 256), 256>>>(a.vals.p, slot_.p,
-                                                                (long long)pcol.size(), pvals_.p);
-    if (cusolverSpDcsrcholBufferInfo(handle_, n_, (int)pcol.size(), descr_, pvals_.p, prow_.p,
-                                     pcol_.p, info_, &internal, &work) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "csrcholBufferInfo failed");
-    buffer_.alloc(work / sizeof(double) + 1);
-    analyzed_ = true;
-  }
-
-  cusolverSpHandle_t handle_ = nullptr;
-  cusparseMatDescr_t descr_ = nullptr;
-  csrcholInfo_t info_ = nullptr;
-  bool analyzed_ = false, ready_ = false;
   int n_ = 0;
-  DevBuf<int> perm_, prow_, pcol_, slot_;
-  DevBuf<double> pvals_, pb_, px_, buffer_;
+  std::unique_ptr<NdCholesky> nd_;
 };
 
 CoarseSolver::CoarseSolver() : impl_(new CoarseSolverImpl()) {}
 CoarseSolver::~CoarseSolver() = default;
-// Backends: 1 dense potrf, 2 nested-dissection multifrontal (ndchol.cu),
-// 3 cuSOLVER csrchol on the ND-permuted matrix.  Mode 0 picks dense for
-// small coarse levels and the multifrontal solver otherwise.
+// Backends: 1 dense (one front), 2 nested-dissection multifrontal
+// (ndchol.cu).  Mode 0 picks dense for small coarse levels and the
+// multifrontal solver otherwise.
 void CoarseSolver::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s) {
   active_ = mode_ != 0 ? mode_ : (a.n <= kDenseCoarseMax ? 1 : 2);
   if (active_ == 1) {
-    impl_->factorize(a, s);
+    impl_->factorize(a, npd, s);
   } else if (active_ == 2) {
     if (!nd_) nd_ = std::make_unique<NdCholesky>();
     nd_->factorize(a, npd, s);
   } else {
-    if (!sparse_) sparse_ = std::make_unique<SparseCholeskyImpl>();
-    sparse_->factorize(a, npd, s);
+    throw Error(HXG_ERR_INVALID_ARGUMENT, "coarse solver mode must be 0, 1 or 2");
   }
 }
 void CoarseSolver::solve(const double* b, double* x, cudaStream_t s) {
   if (active_ == 2)
     nd_->solve(b, x, s);
-  else if (active_ == 3)
-    sparse_->solve(b, x, s);
   else
     impl_->solve(b, x, s);
 }
 bool CoarseSolver::ready() const {
   if (active_ == 2) return nd_ && nd_->ready();
-  if (active_ == 3) return sparse_ && sparse_->ready();
   return impl_->ready();
 }
 

@@ -54,7 +54,6 @@ class CoarseAssembly {
 };
 
 class CoarseSolverImpl;
-class SparseCholeskyImpl;
 
 // Coarse levels up to this many DoFs use the dense device factorization.
 constexpr int kDenseCoarseMax = 6000;
@@ -74,7 +73,6 @@ class CoarseSolver {
   int mode_ = 0;
   int active_ = 0;  // backend used by the last factorize
   std::unique_ptr<CoarseSolverImpl> impl_;
-  std::unique_ptr<SparseCholeskyImpl> sparse_;
   std::unique_ptr<class NdCholesky> nd_;
 };
 

@@ -2,8 +2,9 @@
 // level (see hcoarse.hpp).  Every kernel is gather-based with fixed-order
 // sums, so the cycle is bitwise reproducible run to run.
 #include "hcoarse.hpp"
+#include "densechol.hpp"
 
-#include <cusolverDn.h>
+#include <cublas_v2.h>
 
 #include <algorithm>
 
@@ -230,7 +231,7 @@ __global__ void to_dense_kernel(const int* rows, const int* cols, const double* 
     dense[(size_t)cols[s] * n + rows[s]] = vals[s];
 }
 
-// potri leaves the lower triangle: mirror it so every row is contiguous.
+// The SYRK leaves the lower triangle: mirror it so every row is contiguous.
 __global__ void symmetrize_kernel(int n, double* a) {
   const long long total = (long long)n * n;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -285,41 +286,44 @@ __global__ void from_global(const double* __restrict__ g, const long long* __res
 // ---------------------------------------------------------------------------
 
 DenseInverse::~DenseInverse() {
-  if (handle_) cusolverDnDestroy((cusolverDnHandle_t)handle_);
+  if (handle_) cublasDestroy((cublasHandle_t)handle_);
 }
 
+// A = L L^T and W = L^-1 by dense_chol_inv (densechol.cu), then
+// A^-1 = W^T W (DSYRK, lower) mirrored to a full symmetric matrix.
 void DenseInverse::factorize(const CsrMatrix& a, cudaStream_t s) {
   n_ = a.n;
-  auto h = (cusolverDnHandle_t)handle_;
+  auto h = (cublasHandle_t)handle_;
   if (!h) {
-    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw Error(HXG_ERR_CUDA, "cusolverDnCreate failed");
+    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw Error(HXG_ERR_CUDA, "cublasCreate failed");
     handle_ = h;
   }
-  cusolverDnSetStream(h, s);
+  cublasSetStream(h, s);
   const size_t nn = (size_t)n_ * n_;
-  if (inv_.n != nn) inv_.alloc(nn);
-  HXG_CUDA(cudaMemsetAsync(inv_.p, 0, nn * sizeof(double), s));
+  if (inv_.n != nn) {
+    inv_.alloc(nn);
+    work_.alloc(nn);
+    wfac_.alloc(nn);
+  }
+  const size_t ns = dense_chol_inv_scratch(n_);
+  if (scratch_.n < ns) scratch_.alloc(ns);
+  HXG_CUDA(cudaMemsetAsync(work_.p, 0, nn * sizeof(double), s));
+  HXG_CUDA(cudaMemsetAsync(wfac_.p, 0, nn * sizeof(double), s));
   to_dense_kernel<<<grid_for(a.nnz(), 256), 256, 0, s>>>(a.rows.p, a.cols.p, a.vals.p, a.nnz(), n_,
-                                                         inv_.p);
+                                                         work_.p);
   HXG_CUDA(cudaGetLastError());
-  int l1 = 0, l2 = 0;
-  if (cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, n_, inv_.p, n_, &l1) != CUSOLVER_STATUS_SUCCESS ||
-      cusolverDnDpotri_bufferSize(h, CUBLAS_FILL_MODE_LOWER, n_, inv_.p, n_, &l2) != CUSOLVER_STATUS_SUCCESS)
-    throw Error(HXG_ERR_CUDA, "potrf/potri bufferSize failed");
-  const size_t lw = (size_t)std::max(l1, l2);
-  if (work_.n < lw) work_.alloc(lw);
   if (!info_.n) info_.alloc(1);
+  HXG_CUDA(cudaMemsetAsync(info_.p, 0, sizeof(int), s));
+  dense_chol_inv(h, s, work_.p, n_, wfac_.p, n_, n_, info_.p, scratch_.p);
   int info = 0;
-  if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, n_, inv_.p, n_, work_.p, (int)work_.n, info_.p) !=
-      CUSOLVER_STATUS_SUCCESS)
-    throw Error(HXG_ERR_CUDA, "potrf failed");
   HXG_CUDA(cudaMemcpyAsync(&info, info_.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   HXG_CUDA(cudaStreamSynchronize(s));
   if (info != 0)
     throw Error(HXG_ERR_NOT_SPD, "factorization failed, matrix not SPD: h-multigrid bottom level");
-  if (cusolverDnDpotri(h, CUBLAS_FILL_MODE_LOWER, n_, inv_.p, n_, work_.p, (int)work_.n, info_.p) !=
-      CUSOLVER_STATUS_SUCCESS)
-    throw Error(HXG_ERR_CUDA, "potri failed");
+  const double one = 1.0, zero = 0.0;
+  if (cublasDsyrk(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, n_, n_, &one, wfac_.p, n_, &zero, inv_.p, n_) !=
+      CUBLAS_STATUS_SUCCESS)
+    throw Error(HXG_ERR_CUDA, "syrk (W^T W) failed");
   symmetrize_kernel<<<grid_for((long long)nn, 256), 256, 0, s>>>(n_, inv_.p);
   HXG_CUDA(cudaGetLastError());
 }

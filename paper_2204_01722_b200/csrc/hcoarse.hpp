@@ -45,7 +45,7 @@ constexpr int kHmgBottomMax = 1000;
 // blocks whose cells turn odd): a 16000-DoF dense inverse is 2 GB.
 constexpr int kHmgBottomLimit = 16000;
 
-// Dense SPD inverse (potrf + potri once per setup), applied with a
+// Dense SPD inverse (dense_chol_inv + W^T W once per setup), applied with a
 // hand-written fixed-order GEMV.
 class DenseInverse {
  public:
@@ -55,9 +55,9 @@ class DenseInverse {
   int n() const { return n_; }
 
  private:
-  void* handle_ = nullptr;  // cusolverDnHandle_t
+  void* handle_ = nullptr;  // cublasHandle_t
   int n_ = 0;
-  DevBuf<double> inv_, work_;
+  DevBuf<double> inv_, work_, wfac_, scratch_;
   DevBuf<int> info_;
 };
 

@@ -8,7 +8,7 @@
 // region, all of which are ancestor pivots.  Numeric phase (device, per
 // setup): postorder over fronts, assemble original entries + children's
 // update matrices (extend-add, fixed order), then the
-// dense front in inverse form: L11 = potrf(A11), W = L11^-1 (trtri),
+// dense front in inverse form: (L11, W = L11^-1) by dense_chol_inv (densechol.cu),
 // L21 = A21 W^T and M = [W; L21 W] by GEMM, S = A22 - L21 L21^T by syrk.  Solve (per V-cycle): forward
 // sweep leaves -> root, z1 = L11^-1 y1 and u = y2 - L21 L11^-1 y1 in ONE
 // GEMV with M, update vectors passed up the tree; backward sweep root ->
@@ -25,6 +25,7 @@
 #include <cmath>
 #include <functional>
 
+#include "densechol.hpp"
 #include "dispatch.hpp"
 
 namespace hxg {
@@ -39,10 +40,6 @@ constexpr int kLeafNodes = HXG_ND_LEAF;
 #define HXG_ND_LANE_DEPTH 4
 #endif
 constexpr int kLaneDepth = HXG_ND_LANE_DEPTH;
-#ifndef HXG_CHOL_BASE
-#define HXG_CHOL_BASE 512
-#endif
-constexpr int kCholBase = HXG_CHOL_BASE;  // cuSOLVER potrf / trtri below this block size
 
 __global__ void assemble_kernel(const long long* __restrict__ dst, const int* __restrict__ src,
                                 long long n, const double* __restrict__ vals, double* front) {
@@ -280,7 +277,7 @@ void cublas_check(cublasStatus_t s, const char* what) {
 
 }  // namespace
 
-NdCholesky::NdCholesky() = default;
+NdCholesky::NdCholesky(long long leaf_nodes) : leaf_nodes_(leaf_nodes > 0 ? leaf_nodes : kLeafNodes) {}
 NdCholesky::~NdCholesky() {
   if (graph_) cudaGraphExecDestroy(graph_);
   if (gev_in_) cudaEventDestroy(gev_in_);
@@ -306,7 +303,7 @@ void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
     Front f;
     f.level = level;
     Box piv = r;
-    if (cnt > kLeafNodes && n[ax] >= 3) {
+    if (cnt > leaf_nodes_ && n[ax] >= 3) {
       int mid = r.lo[ax] + n[ax] / 2;
       Box left = r, right = r;
       left.hi[ax] = mid;
@@ -536,7 +533,7 @@ void NdCholesky::analyze(const CsrMatrix& a, const int npd[3]) {
   size_t maxnp = 1;
   for (const auto& f : fronts_) maxnp = std::max(maxnp, (size_t)f.np);
   wvec_.alloc((size_t)n_);
-  info_.alloc(2 * (size_t)nf);  // potrf, then trtri status per front
+  info_.alloc(2 * (size_t)nf);  // first failed pivot per front
   analyzed_ = true;
 }
 
@@ -550,15 +547,11 @@ struct NdCholesky::Lane {
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
   cublasHandle_t cublas = nullptr;
-  cusolverDnHandle_t cusolver = nullptr;
-  DevBuf<double> W, inv, tmp, potrf_ws, trtri_ws, stack, rscr;
-  DevBuf<int> info;  // base-block potrf / trtri status
-  std::vector<char> trtri_host;
+  DevBuf<double> W, inv, tmp, stack, rscr;
   std::vector<int> fronts;  // postorder
   bool own_stream = false;
   ~Lane() {
     if (cublas) cublasDestroy(cublas);
-    if (cusolver) cusolverDnDestroy(cusolver);
     if (done) cudaEventDestroy(done);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -617,9 +610,7 @@ void NdCholesky::plan_lanes() {
     }
     HXG_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
     cublas_check(cublasCreate(&L.cublas), "cublasCreate");
-    if (cusolverDnCreate(&L.cusolver) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "cusolverDnCreate failed");
-    size_t mw = 1, mi = 1, mt = 1, mp = 1, mtd = 1, mth = 1, cur = 0, peak = 1;
+    size_t mw = 1, mi = 1, mt = 1, ms = 1, cur = 0, peak = 1;
     std::vector<size_t> st;
     std::vector<int> mine = L.fronts;
     for (int t : top_)
@@ -630,18 +621,7 @@ void NdCholesky::plan_lanes() {
       mw = std::max(mw, m * m);
       mi = std::max(mi, (size_t)f.np * f.np);
       mt = std::max(mt, (size_t)f.np * f.ns);
-      int lwork = 0;
-      if (cusolverDnDpotrf_bufferSize(L.cusolver, CUBLAS_FILL_MODE_LOWER, f.np, nullptr, (int)m,
-                                      &lwork) != CUSOLVER_STATUS_SUCCESS)
-        throw Error(HXG_ERR_CUDA, "potrf_bufferSize failed");
-      mp = std::max(mp, (size_t)lwork);
-      size_t wdev = 0, whost = 0;
-      if (cusolverDnXtrtri_bufferSize(L.cusolver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT,
-                                      f.np, CUDA_R_64F, nullptr, f.np, &wdev, &whost) !=
-          CUSOLVER_STATUS_SUCCESS)
-        throw Error(HXG_ERR_CUDA, "trtri_bufferSize failed");
-      mtd = std::max(mtd, wdev);
-      mth = std::max(mth, whost);
+      ms = std::max(ms, dense_chol_inv_scratch(f.np));
       // private stack: children in this lane are popped, the front pushed
       // (unless its update is handed over)
       for (int q = 0; q < 2; ++q) {
@@ -660,61 +640,9 @@ void NdCholesky::plan_lanes() {
     L.W.alloc(mw);
     L.inv.alloc(mi);
     L.tmp.alloc(mt);
-    L.potrf_ws.alloc(mp);
-    L.trtri_ws.alloc(mtd / sizeof(double) + 1);
-    L.trtri_host.resize(mth + 1);
     L.stack.alloc(peak);
-    // recursion scratch n2 x n1 <= np^2 / 4 + 16 np
-    L.rscr.alloc(mi / 4 + 32 * (size_t)std::sqrt((double)mi) + 1024);
-    L.info.alloc(2);
+    L.rscr.alloc(ms);  // dense_chol_inv's n2 x n1 scratch
   }
-}
-
-// Recursive blocked Cholesky that also forms the inverse factor, with all
-// the level-3 work on tensor-core GEMM / SYRK:
-//   [A11 .; A21 A22]:  (L11, W11) = rec(A11);  L21 = A21 W11^T;
-//   S = A22 - L21 L21^T;  (L22, W22) = rec(S);  W21 = -W22 (L21 W11).
-// A (lower, leading dimension lda) is overwritten by L; W (zeroed upper
-// part, ldw) receives L^-1.  Blocks of <= kCholBase use cuSOLVER potrf +
-// trtri; a failed pivot block records its info in *info.
-void NdCholesky::chol_inv(Lane& L, double* A, int lda, double* W, int ldw, int n, int* info) {
-  cudaStream_t s = L.stream;
-  if (n <= kCholBase) {
-    if (cusolverDnDpotrf(L.cusolver, CUBLAS_FILL_MODE_LOWER, n, A, lda, L.potrf_ws.p,
-                         (int)L.potrf_ws.n, L.info.p) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "potrf failed");
-    accumulate_info<<<1, 1, 0, s>>>(info, L.info.p);
-    HXG_CUDA(cudaMemcpy2DAsync(W, sizeof(double) * ldw, A, sizeof(double) * lda,
-                               sizeof(double) * n, n, cudaMemcpyDeviceToDevice, s));
-    zero_strict_upper<<<grid_for((long long)n * n, 256), 256, 0, s>>>(W, ldw, n);
-    if (cusolverDnXtrtri(L.cusolver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F,
-                         W, ldw, L.trtri_ws.p, L.trtri_ws.n * sizeof(double),
-                         L.trtri_host.data(), L.trtri_host.size(), L.info.p + 1) !=
-        CUSOLVER_STATUS_SUCCESS)
-      throw Error(HXG_ERR_CUDA, "trtri failed");
-    return;
-  }
-  const double one = 1.0, minus_one = -1.0, zero = 0.0;
-  const int n1 = ((n / 2 + 31) / 32) * 32, n2 = n - n1;
-  double *A21 = A + n1, *A22 = A + n1 + (size_t)n1 * lda;
-  double *W21 = W + n1, *W22 = W + n1 + (size_t)n1 * ldw;
-  chol_inv(L, A, lda, W, ldw, n1, info);
-  double* T = L.rscr.p;  // n2 x n1 scratch
-  cublas_check(cublasDgemm(L.cublas, CUBLAS_OP_N, CUBLAS_OP_T, n2, n1, n1, &one, A21, lda, W, ldw,
-                           &zero, T, n2),
-               "gemm (L21)");
-  HXG_CUDA(cudaMemcpy2DAsync(A21, sizeof(double) * lda, T, sizeof(double) * n2,
-                             sizeof(double) * n2, n1, cudaMemcpyDeviceToDevice, s));
-  cublas_check(cublasDsyrk(L.cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, n2, n1, &minus_one, A21,
-                           lda, &one, A22, lda),
-               "syrk");
-  chol_inv(L, A22, lda, W22, ldw, n2, info);
-  cublas_check(cublasDgemm(L.cublas, CUBLAS_OP_N, CUBLAS_OP_N, n2, n1, n1, &one, A21, lda, W, ldw,
-                           &zero, T, n2),
-               "gemm (L21 W11)");
-  cublas_check(cublasDgemm(L.cublas, CUBLAS_OP_N, CUBLAS_OP_N, n2, n1, n2, &minus_one, W22, ldw, T,
-                           n2, &zero, W21, ldw),
-               "gemm (W21)");
 }
 
 void NdCholesky::factor_front(int t, Lane& L, const CsrMatrix& a,
@@ -757,7 +685,7 @@ void NdCholesky::factor_front(int t, Lane& L, const CsrMatrix& a,
   // L21 = A21 W^T; S = A22 - L21 L21^T (syrk); M = [W; L21 W] written
   // straight into the factor.
   HXG_CUDA(cudaMemsetAsync(L.inv.p, 0, sizeof(double) * (size_t)f.np * f.np, s));
-  chol_inv(L, W, m, L.inv.p, f.np, f.np, info_.p + t);
+  dense_chol_inv(L.cublas, s, W, m, L.inv.p, f.np, f.np, info_.p + t, L.rscr.p);
   double* Lp = L_.p + f.loff;
   if (f.ns > 0) {
     // L21 = A21 W^T straight into the factor panel, then S = A22 - L21 L21^T
@@ -814,7 +742,6 @@ void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s)
   top.stream = s;
   for (auto& l : lanes_) {
     cublasSetStream(l->cublas, l->stream);
-    cusolverDnSetStream(l->cusolver, l->stream);
   }
   HXG_CUDA(cudaMemsetAsync(info_.p, 0, 2 * sizeof(int) * fronts_.size(), s));
   // The subtree lanes start after earlier work on the caller's stream.

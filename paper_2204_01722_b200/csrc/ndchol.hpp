@@ -9,7 +9,6 @@
 
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
-#include <cusolverDn.h>
 
 #include <memory>
 #include <utility>
@@ -21,7 +20,10 @@ namespace hxg {
 
 class NdCholesky {
  public:
-  NdCholesky();
+  // leaf_nodes: dissection stops at regions of at most this many lattice
+  // nodes (0: the default); a leaf larger than the lattice gives one dense
+  // front (the dense coarse mode).
+  explicit NdCholesky(long long leaf_nodes = 0);
   ~NdCholesky();
   NdCholesky(const NdCholesky&) = delete;
   NdCholesky& operator=(const NdCholesky&) = delete;
@@ -57,6 +59,7 @@ class NdCholesky {
   };
   void analyze(const CsrMatrix& a, const int npd[3]);
 
+  long long leaf_nodes_;
   bool analyzed_ = false, ready_ = false;
   int n_ = 0;
   std::vector<Front> fronts_;           // postorder
@@ -72,7 +75,6 @@ class NdCholesky {
   DevBuf<double> L_;         // factor panels
   struct Lane;
   void plan_lanes();
-  void chol_inv(Lane& lane, double* A, int lda, double* W, int ldw, int n, int* info);
   void factor_front(int t, Lane& lane, const CsrMatrix& a,
                     std::vector<std::pair<size_t, int>>& stack);
   std::vector<std::unique_ptr<Lane>> lanes_;

@@ -190,7 +190,7 @@ class PartitionedProblem:
         check(lib().hxg_mg_setup_numeric(self.h))
 
     def set_coarse_mode(self, mode):
-        m = {"auto": 0, "dense": 1, "nd": 2, "csrchol": 3, "hmg": 4}.get(mode, mode)
+        m = {"auto": 0, "dense": 1, "nd": 2, "hmg": 4}.get(mode, mode)
         check(lib().hxg_mg_set_coarse_mode(self.h, int(m)))
 
     def lambda_max(self, k):

@@ -349,9 +349,9 @@ class MultigridHierarchy:
         check(lib().hxg_mg_assemble_coarse(self.h))
 
     def set_coarse_mode(self, mode):
-        """0 automatic, 1 dense, 2 nested-dissection multifrontal, 3 cuSOLVER csrchol,
+        """0 automatic, 1 dense (one front), 2 nested-dissection multifrontal,
         4 ("hmg") inexact: one Galerkin h-multigrid V-cycle on the p = 1 level."""
-        mode = {"auto": 0, "dense": 1, "sparse": 2, "nd": 2, "csrchol": 3, "hmg": 4}.get(mode, mode)
+        mode = {"auto": 0, "dense": 1, "sparse": 2, "nd": 2, "hmg": 4}.get(mode, mode)
         check(lib().hxg_mg_set_coarse_mode(self.h, int(mode)))
 
     def lambda_max(self, k):
@@ -471,7 +471,7 @@ class CoarseCholesky:
     solve(b) on device vectors."""
 
     def __init__(self, row_ptr, cols, npd, mode="auto"):
-        mode = {"auto": 0, "dense": 1, "sparse": 2, "nd": 2, "csrchol": 3}.get(mode, mode)
+        mode = {"auto": 0, "dense": 1, "sparse": 2, "nd": 2}.get(mode, mode)
         self._rp = np.ascontiguousarray(row_ptr, np.int32)
         self._cols = np.ascontiguousarray(cols, np.int32)
         self.n = len(self._rp) - 1
