@@ -475,16 +475,19 @@ def run_ours(args, rank, world, local_rank):
         op.apply_jacobian_host(xh_np, yh_np)
     torch.cuda.synchronize()
     e2e_steps = max(5, min(args.steps, 50))
-    t0 = time.perf_counter()
     xd, yd = torch.empty_like(x), torch.empty_like(x)
-    for _ in range(e2e_steps):
-        if dist is None:
-            op.apply_jacobian_host(xh_np, yh_np)
-        else:  # host x -> device, partitioned apply (interface sums), -> host y
-            xd.copy_(xh)
-            pp.apply(xd, yd)
-            yh.copy_(yd)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_rounds = []
+    for _ in range(3):  # the median of three rounds (host-side PCIe / page noise)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            if dist is None:
+                op.apply_jacobian_host(xh_np, yh_np)
+            else:  # host x -> device, partitioned apply (interface sums), -> host y
+                xd.copy_(xh)
+                pp.apply(xd, yd)
+                yh.copy_(yd)
+        e2e_rounds.append((time.perf_counter() - t0) / e2e_steps)
+    e2e_s = sorted(e2e_rounds)[1]
     if dist is not None:
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -703,6 +706,7 @@ def run_ours(args, rank, world, local_rank):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * N,
                     "d2h_bytes_per_step": 8 * N, "ms_per_step": e2e_s * 1e3,
+                    "rounds_ms": [round(t * 1e3, 3) for t in e2e_rounds],
                     "path": "hxg_op_apply_jacobian_host (pinned host buffers)"},
             "gpu_launches": args.steps * op.kernel_launches(),
             "clocks": sampler.summary(),

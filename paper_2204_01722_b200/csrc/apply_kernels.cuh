@@ -12,7 +12,7 @@
 
 namespace hxg {
 
-enum ApplyMode { kJacobian = 0, kResidual = 1, kEnergy = 2 };
+enum ApplyMode { kJacobian = 0, kResidual = 1, kEnergy = 2, kResidualBox = 3 };
 
 struct ElemParams {
   BoxDev box;

@@ -9,71 +9,151 @@ namespace hxg {
 
 namespace {
 
-constexpr int kBaseThreads = 512;
-constexpr int kBaseWarps = kBaseThreads / 32;
+// 32 x 32 threads, each owning one 4 x 4 tile of the (<= 128)^2 block.
+constexpr int kTile = 4;
+constexpr int kTiles = 32;
+constexpr int kBaseThreads = kTiles * kTiles;
+static_assert(kDenseBase <= kTile * kTiles, "dense base block larger than the thread tile grid");
 
 void cublas_ok(cublasStatus_t st, const char* what) {
   if (st != CUBLAS_STATUS_SUCCESS) throw Error(HXG_ERR_CUDA, std::string("cuBLAS ") + what + " failed");
 }
 
-// One CTA factors and inverts an n x n block (n <= kDenseBase) held in shared
-// memory, column-major with an odd stride (64-bit accesses along a row of
-// lanes stay bank-conflict free):
-//   1. right-looking Cholesky, column k: pivot, scale the column, rank-1
-//      update of the trailing lower triangle (one warp per column, lanes down
-//      the rows), L written back over A;
-//   2. in-place inversion of L (the unblocked lower, non-unit trti2 order:
-//      j = n-1 .. 0, column j below the diagonal = -(1 / L_jj) T x with T the
-//      already inverted trailing block; one warp per row, lanes over the
-//      columns, fixed-order butterfly), L^-1 written to W with zeros above.
-__global__ void __launch_bounds__(kBaseThreads) chol_inv_base_kernel(double* A, int lda, double* W,
-                                                                     int ldw, int n, int* info) {
+// One CTA factors and inverts an n x n block (n <= kDenseBase).  Thread
+// (ti, tj) keeps the 4 x 4 tile (rows 4 ti.., columns 4 tj..) of the lower
+// triangle in registers; every step is one barrier:
+//   1. right-looking Cholesky, step k: the owners of column k publish it
+//      (a double-buffered shared vector), every trailing entry i >= j > k
+//      takes a_ij -= a_ik a_jk / a_kk, and the column owners finalise
+//      l_kk = sqrt(a_kk), l_ik = a_ik / l_kk;
+//   2. L is staged in shared memory (written back over A) and the registers
+//      restart from B = I: forward elimination L W = I, step k: the owners of
+//      row k finalise W_kj = B_kj / L_kk (j <= k) and publish the row, every
+//      entry below takes B_ij -= L_ik W_kj;
+//   3. W (zero strict upper part) staged through shared memory to global.
+// A failed pivot (a_kk <= 0, the potrf convention) sets *info = k + 1.
+__global__ void __launch_bounds__(kBaseThreads, 1) chol_inv_base_kernel(double* A, int lda, double* W,
+                                                                        int ldw, int n, int* info) {
   extern __shared__ double sm[];
   const int LD = n | 1;
-  double* xs = sm + (size_t)n * LD;
+  double* vec = sm + (size_t)n * LD;  // two 128-entry buffers
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int c = warp; c < n; c += kBaseWarps)
+  const int ti = tid / kTiles, tj = tid % kTiles;
+  const int r0 = kTile * ti, c0 = kTile * tj;
+  const bool active = ti >= tj && c0 < n;
+  // coalesced load of the lower triangle, then each thread takes its tile
+  for (int c = warp; c < n; c += kBaseThreads / 32)
     for (int r = c + lane; r < n; r += 32) sm[c * LD + r] = A[r + (size_t)c * lda];
   __syncthreads();
+  double e[kTile][kTile];
+#pragma unroll
+  for (int a = 0; a < kTile; ++a)
+#pragma unroll
+    for (int b = 0; b < kTile; ++b) {
+      const int i = r0 + a, j = c0 + b;
+      e[a][b] = active && i < n && i >= j ? sm[j * LD + i] : 0.0;
+    }
   for (int k = 0; k < n; ++k) {
-    const double d = sm[k * LD + k];
+    double* cb = vec + (k & 1) * 128;
+    const int tk = k / kTile, kc = k % kTile;
+    if (active && tj == tk) {
+#pragma unroll
+      for (int a = 0; a < kTile; ++a)
+#pragma unroll
+        for (int b = 0; b < kTile; ++b)
+          if (b == kc && r0 + a >= k && r0 + a < n) cb[r0 + a] = e[a][b];
+    }
+    __syncthreads();
+    const double d = cb[k];
     if (!(d > 0.0)) {  // uniform: every thread read the same pivot
       if (tid == 0) atomicCAS(info, 0, k + 1);
       return;
     }
-    const double r = sqrt(d), ri = 1.0 / r;
-    __syncthreads();  // the pivot is read before it is overwritten
-    if (tid == 0) sm[k * LD + k] = r;
-    for (int i = k + 1 + tid; i < n; i += kBaseThreads) sm[k * LD + i] *= ri;
-    __syncthreads();
-    for (int j = k + 1 + warp; j < n; j += kBaseWarps) {
-      const double ljk = sm[k * LD + j];
-      for (int i = j + lane; i < n; i += 32) sm[j * LD + i] -= sm[k * LD + i] * ljk;
-    }
-    __syncthreads();
-  }
-  for (int c = warp; c < n; c += kBaseWarps)
-    for (int r = c + lane; r < n; r += 32) A[r + (size_t)c * lda] = sm[c * LD + r];
-  for (int j = n - 1; j >= 0; --j) {
-    const int m = n - j - 1;
-    const double inv = 1.0 / sm[j * LD + j];
-    for (int i = tid; i < m; i += kBaseThreads) xs[i] = sm[j * LD + j + 1 + i];
-    __syncthreads();
-    for (int i = warp; i < m; i += kBaseWarps) {
-      double acc = 0.0;
-      for (int k = lane; k <= i; k += 32) acc += sm[(j + 1 + k) * LD + j + 1 + i] * xs[k];
+    if (active && ti >= tk) {
+      const double rd = 1.0 / d;
+      double li[kTile], lj[kTile];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) sm[j * LD + j + 1 + i] = -inv * acc;
+      for (int a = 0; a < kTile; ++a) li[a] = r0 + a > k && r0 + a < n ? cb[r0 + a] * rd : 0.0;
+#pragma unroll
+      for (int b = 0; b < kTile; ++b) lj[b] = c0 + b > k && c0 + b < n ? cb[c0 + b] : 0.0;
+#pragma unroll
+      for (int a = 0; a < kTile; ++a)
+#pragma unroll
+        for (int b = 0; b < kTile; ++b)
+          if (c0 + b > k && r0 + a >= c0 + b) e[a][b] -= li[a] * lj[b];
+      if (tj == tk) {
+        const double r = sqrt(d);
+#pragma unroll
+        for (int a = 0; a < kTile; ++a)
+#pragma unroll
+          for (int b = 0; b < kTile; ++b)
+            if (b == kc && r0 + a >= k && r0 + a < n) e[a][b] = r0 + a == k ? r : cb[r0 + a] / r;
+      }
     }
-    if (tid == 0) sm[j * LD + j] = inv;
-    __syncthreads();
   }
-  for (int c = warp; c < n; c += kBaseWarps)
+  // L -> shared memory (kept for the inversion) and back over A
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int a = 0; a < kTile; ++a)
+#pragma unroll
+      for (int b = 0; b < kTile; ++b) {
+        const int i = r0 + a, j = c0 + b;
+        if (i < n && i >= j) sm[j * LD + i] = e[a][b];
+      }
+  }
+  __syncthreads();
+  for (int c = warp; c < n; c += kBaseThreads / 32)
+    for (int r = c + lane; r < n; r += 32) A[r + (size_t)c * lda] = sm[c * LD + r];
+#pragma unroll
+  for (int a = 0; a < kTile; ++a)
+#pragma unroll
+    for (int b = 0; b < kTile; ++b) e[a][b] = r0 + a == c0 + b ? 1.0 : 0.0;
+  for (int k = 0; k < n; ++k) {
+    double* rb = vec + (k & 1) * 128;
+    const int tk = k / kTile, kc = k % kTile;
+    if (active && ti == tk) {
+      const double lkk = sm[k * LD + k];
+#pragma unroll
+      for (int a = 0; a < kTile; ++a)
+#pragma unroll
+        for (int b = 0; b < kTile; ++b)
+          if (a == kc && c0 + b <= k) {
+            const double w = e[a][b] / lkk;
+            e[a][b] = w;
+            rb[c0 + b] = w;
+          }
+    }
+    __syncthreads();
+    if (active && ti >= tk) {
+      double lik[kTile], wk[kTile];
+#pragma unroll
+      for (int a = 0; a < kTile; ++a) lik[a] = r0 + a > k && r0 + a < n ? sm[k * LD + r0 + a] : 0.0;
+#pragma unroll
+      for (int b = 0; b < kTile; ++b) wk[b] = c0 + b <= k ? rb[c0 + b] : 0.0;
+#pragma unroll
+      for (int a = 0; a < kTile; ++a)
+#pragma unroll
+        for (int b = 0; b < kTile; ++b)
+          if (r0 + a > k && c0 + b <= k) e[a][b] -= lik[a] * wk[b];
+    }
+  }
+  __syncthreads();  // L no longer read: stage W in its place
+  if (active) {
+#pragma unroll
+    for (int a = 0; a < kTile; ++a)
+#pragma unroll
+      for (int b = 0; b < kTile; ++b) {
+        const int i = r0 + a, j = c0 + b;
+        if (i < n && i >= j) sm[j * LD + i] = e[a][b];
+      }
+  }
+  __syncthreads();
+  for (int c = warp; c < n; c += kBaseThreads / 32)
     for (int r = lane; r < n; r += 32) W[r + (size_t)c * ldw] = r >= c ? sm[c * LD + r] : 0.0;
 }
 
-size_t base_smem(int n) { return sizeof(double) * ((size_t)n * (n | 1) + n); }
+size_t base_smem(int n) { return sizeof(double) * ((size_t)n * (n | 1) + 256); }
 
 }  // namespace
 

@@ -27,6 +27,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "apply_kernels.cuh"
@@ -310,12 +311,15 @@ __device__ __forceinline__ double ld_once(const double* a, unsigned long long po
 // residual of operator.hpp:146-180 in one pass, Current storage).
 template <int P, int Q, int ST = kStorageCurrent, int MODE = kJacobian>
 __global__ void __launch_bounds__(Dims<P, Q>::T,
-                                  MODE == kResidual         ? fused_residual_min_blocks(P, Q)
+                                  MODE != kJacobian         ? fused_residual_min_blocks(P, Q)
                                   : ST == kStorageCurrent ? fused_min_blocks(P, Q)
                                                           : variant_min_blocks(ST))
     fused_jacobian_kernel(const __grid_constant__ FusedParams prm) {
-  static_assert(MODE == kJacobian || ST == kStorageCurrent, "fused residual: Current storage");
-  constexpr bool kRes = MODE == kResidual;
+  static_assert(MODE != kResidual || ST == kStorageCurrent, "fused residual: Current storage");
+  // kResidualBox: the residual on a box mesh, geometric factors formed in
+  // registers (diagonal dxi/dX)
+  constexpr bool kRes = MODE == kResidual || MODE == kResidualBox;
+  constexpr bool kBoxGeo = MODE == kResidualBox;
   constexpr int SS = device_state_stride(ST), SP = state_row(SS, Q);
   constexpr bool kStateV2 = state_paired(Q);  // 16-byte loads of the paired layout
   using D = FDims<P, Q>;
@@ -347,7 +351,7 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   // stream: nothing global is touched before the predecessor has completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-  if (pf_mode(Q) != 1 && tid == 0 && (int)blockIdx.x < prm.nbricks)
+  if (pf_mode(Q) != 1 && !kBoxGeo && tid == 0 && (int)blockIdx.x < prm.nbricks)
     prefetch_state(prm.blist ? prm.blist[prm.brick0 + blockIdx.x] : prm.brick0 + blockIdx.x);
 #if HXG_EXPERIMENT == 4
   long long t_last = clock64();
@@ -435,8 +439,8 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
   for (int bi = blockIdx.x; bi < prm.nbricks; bi += gridDim.x, cur ^= 1) {
   const int brick = brick_at(bi);
   const bool pf_next = tid == 0 && bi + (int)gridDim.x < prm.nbricks;
-  if (pf_mode(Q) == 0 && pf_next && !(kRes && prm.geo_box)) prefetch_state(brick_at(bi + gridDim.x));
-  if (pf_mode(Q) == 1 && tid == 0 && !(kRes && prm.geo_box)) prefetch_state(brick);
+  if (pf_mode(Q) == 0 && pf_next && !kBoxGeo) prefetch_state(brick_at(bi + gridDim.x));
+  if (pf_mode(Q) == 1 && tid == 0 && !kBoxGeo) prefetch_state(brick);
   const int bx = bc.x, by = bc.y, bz = bc.z;
   const BrickXYZ bnext = prm.blist ? decompose(brick_at(min(bi + (int)gridDim.x, prm.nbricks - 1)))
                                     : advance(bc);
@@ -644,47 +648,50 @@ __global__ void __launch_bounds__(Dims<P, Q>::T,
     if constexpr (kRes) {
       if (valid) {
         const size_t pt = (size_t)lay.brick_points() * brick + (size_t)qz * T;
-        double geo[kGeoStride];
-        if (prm.geo_box) {
-          const int qx = te % Q, qy = te / Q;
-#pragma unroll
-          for (int s = 0; s < 9; ++s) geo[s] = 0.0;
-          geo[0] = prm.geo_g[0];
-          geo[4] = prm.geo_g[1];
-          geo[8] = prm.geo_g[2];
-          geo[9] = prm.geo_qw[qx] * prm.geo_qw[qy] * prm.geo_qw[qz] * prm.geo_jac;
-        } else {
-          const double* gp = prm.geo + pt * kGeoStride + tid;
-#pragma unroll
-          for (int s = 0; s < kGeoStride; ++s) geo[s] = ld_stream(gp + s * T, pol_stream);
-        }
         double G[9];
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
           for (int d = 0; d < 3; ++d)
             G[3 * c + d] = qz < NSG ? slot[gslot(c, d, qz)] : g[c][d][qz - NSG];
-        double st[kRefStateScalars];
-        const double J = residual_qf(prm.mu, prm.lambda, G, geo, geo[9], H, st);
-        double* so = prm.state_out + pt * SP + state_lane(tid, Q);
-        if (!(J > 0.0)) {  // first inverted (e, q) in reference order (operator.hpp:166-168)
-          const int qx = te % Q, qy = te / Q;
-          const long long e = (bx * BX + lx) + (long long)box.cells[0] * ((by * BY + ly) +
-                                                                     (long long)box.cells[1] * (bz * BZ + lz));
-          atomicMin(prm.fail, (unsigned long long)e * (Q * Q * Q) + (unsigned long long)(qx + Q * (qy + Q * qz)));
-          so[0] = J;  // read back by the host for the error report
+        // the q-function, state stores and failure report for one set of
+        // geometric factors (inlined twice: the box branch's zero
+        // off-diagonal dxi/dX entries fold away)
+        auto qf_store = [&](const double* geo, auto diag) {
+          double st[kRefStateScalars];
+          const double J = residual_qf<decltype(diag)::value>(prm.mu, prm.lambda, G, geo, geo[9], H, st);
+          double* so = prm.state_out + pt * SP + state_lane(tid, Q);
+          if (!(J > 0.0)) {  // first inverted (e, q) in reference order (operator.hpp:166-168)
+            const int qx = te % Q, qy = te / Q;
+            const long long e = (bx * BX + lx) + (long long)box.cells[0] * ((by * BY + ly) +
+                                                                       (long long)box.cells[1] * (bz * BZ + lz));
+            atomicMin(prm.fail, (unsigned long long)e * (Q * Q * Q) + (unsigned long long)(qx + Q * (qy + Q * qz)));
+            so[0] = J;  // read back by the host for the error report
 #pragma unroll
-          for (int k = 0; k < 9; ++k) H[k] = 0.0;
-        } else {
-          double sp[kStateStride];
-          pack_state(prm.mu, st, sp);
-          if constexpr (kStateV2) {
-#pragma unroll
-            for (int s = 0; s < kStateStride; s += 2) st_stream2(so + s * T, sp[s], sp[s + 1], pol_stream);
+            for (int k = 0; k < 9; ++k) H[k] = 0.0;
           } else {
+            double sp[kStateStride];
+            pack_state(prm.mu, st, sp);
+            if constexpr (kStateV2) {
 #pragma unroll
-            for (int s = 0; s < kStateStride; ++s) st_stream(so + s * T, sp[s], pol_stream);
+              for (int s = 0; s < kStateStride; s += 2) st_stream2(so + s * T, sp[s], sp[s + 1], pol_stream);
+            } else {
+#pragma unroll
+              for (int s = 0; s < kStateStride; ++s) st_stream(so + s * T, sp[s], pol_stream);
+            }
           }
+        };
+        if constexpr (kBoxGeo) {
+          const int qx = te % Q, qy = te / Q;
+          const double geo[kGeoStride] = {prm.geo_g[0], 0.0, 0.0, 0.0, prm.geo_g[1], 0.0, 0.0, 0.0, prm.geo_g[2],
+                                          prm.geo_qw[qx] * prm.geo_qw[qy] * prm.geo_qw[qz] * prm.geo_jac};
+          qf_store(geo, std::true_type{});
+        } else {
+          double geo[kGeoStride];
+          const double* gp = prm.geo + pt * kGeoStride + tid;
+#pragma unroll
+          for (int s = 0; s < kGeoStride; ++s) geo[s] = ld_stream(gp + s * T, pol_stream);
+          qf_store(geo, std::false_type{});
         }
       } else {
 #pragma unroll
@@ -878,89 +885,101 @@ __global__ void __launch_bounds__(kFixupThreads, HXG_FIXUP_MINB) fused_fixup_ker
   using D = FDims<P, Q>;
   constexpr int BX = D::BX, BY = D::BY, BZ = D::BZ;
   constexpr int PB0 = P * BX, PB1 = P * BY, PB2 = P * BZ;
+  constexpr int NB3 = D::NB * 3;
   const QLayout& lay = prm.lay;
   const BoxDev& box = prm.box;
   const int npx = box.npd[0], npy = box.npd[1];
   const unsigned long long pol = policy_evict_first();
   const int fb = prm.face_bits;
+  // Offset of sharing brick o = o0 + 2 o1 + 4 o2 (o_d = 1: the lower
+  // neighbour along d) relative to this brick's partial of the same node:
+  // brick index - (o0 + nb0 (o1 + nb1 o2)), local coordinate + o_d P B_d.
+  __shared__ long long off[8];
+  if (threadIdx.x < 8) {
+    const int o0 = threadIdx.x & 1, o1 = (threadIdx.x >> 1) & 1, o2 = threadIdx.x >> 2;
+    off[threadIdx.x] = -(long long)(o0 + lay.nb[0] * (o1 + lay.nb[1] * o2)) * NB3 +
+                       3 * ((o2 * PB2 * D::NBY + o1 * PB1) * D::NBX + o0 * PB0);
+  }
+  __syncthreads();
   for (int bi = blockIdx.x; bi < prm.nbricks; bi += gridDim.x) {
     const int b = prm.blist ? prm.blist[prm.brick0 + bi] : prm.brick0 + bi;
     const int cx = b % lay.nb[0], cy = (b / lay.nb[0]) % lay.nb[1], cz = b / (lay.nb[0] * lay.nb[1]);
-    const int fnx = P * min(BX, box.cells[0] - cx * BX) + 1;
-    const int fny = P * min(BY, box.cells[1] - cy * BY) + 1;
-    const int fnz = P * min(BZ, box.cells[2] - cz * BZ) + 1;
     const bool lx = cx == lay.nb[0] - 1, ly = cy == lay.nb[1] - 1, lz = cz == lay.nb[2] - 1;
+    const int fnx = lx ? P * (box.cells[0] - cx * BX) + 1 : D::NBX;
+    const int fny = ly ? P * (box.cells[1] - cy * BY) + 1 : D::NBY;
+    const int fnz = lz ? P * (box.cells[2] - cz * BZ) + 1 : D::NBZ;
     const int nox = lx ? fnx : fnx - 1, noy = ly ? fny : fny - 1, noz = lz ? fnz : fnz - 1;
     const int nbx = lx ? 2 : 1, nby = ly ? 2 : 1, nbz = lz ? 2 : 1;  // boundary coords per axis
     const int iyc = noy - nby, izc = noz - nbz;                        // interior coords
     const int rowsA = nbz * noy + izc * nby;
     const int entA = rowsA * nox, entB = izc * iyc * nbx;  // nodes (3 components each)
+    // small exact divisions through float reciprocals (t, r < 2^12)
+    const float rnox = 1.0f / (float)nox, rnby = 1.0f / (float)nby, rnbx = 1.0f / (float)nbx,
+                riyc = 1.0f / (float)(iyc > 0 ? iyc : 1);
     const int gx0 = PB0 * cx, gy0 = PB1 * cy, gz0 = PB2 * cz;
+    const double* pbase = prm.partial + (size_t)b * NB3;
+    const int sb0 = cx > 0, sb1 = (cy > 0) << 1, sb2 = (cz > 0) << 2;
     for (int t = threadIdx.x; t < entA + entB; t += kFixupThreads) {
       int ix, iy, iz;
       if (t < entA) {
-        const int r = t / nox;
+        const int r = (int)(((float)t + 0.5f) * rnox);
         ix = t - r * nox;
         if (r < nbz * noy) {
-          iz = r >= noy ? fnz - 1 : 0;
-          iy = r >= noy ? r - noy : r;
+          const bool up = r >= noy;
+          iz = up ? fnz - 1 : 0;
+          iy = up ? r - noy : r;
         } else {
           const int q = r - nbz * noy;
-          iz = 1 + q / nby;
-          iy = (q % nby) ? fny - 1 : 0;
+          const int qz = (int)(((float)q + 0.5f) * rnby);
+          iz = 1 + qz;
+          iy = q - qz * nby ? fny - 1 : 0;
         }
       } else {
-        const int u = t - entA, r = u / nbx;
+        const int u = t - entA, r = (int)(((float)u + 0.5f) * rnbx);
         ix = u - r * nbx ? fnx - 1 : 0;
-        iz = 1 + r / iyc;
-        iy = 1 + r % iyc;
+        const int rz = (int)(((float)r + 0.5f) * riyc);
+        iz = 1 + rz;
+        iy = 1 + (r - rz * iyc);
       }
+      const int gx = gx0 + ix, gy = gy0 + iy, gz = gz0 + iz;
       if (prm.ifilter) {  // the partitioned apply's split around the interface exchange
-        const int gx = gx0 + ix, gy = gy0 + iy, gz = gz0 + iz, fi = prm.iface;
+        const int fi = prm.iface;
         const bool on = ((fi & 1) && gx == 0) || ((fi & 2) && gx == npx - 1) || ((fi & 4) && gy == 0) ||
                         ((fi & 8) && gy == npy - 1) || ((fi & 16) && gz == 0) ||
                         ((fi & 32) && gz == box.npd[2] - 1);
         if (on != (prm.ifilter == 1)) continue;
       }
-      // sharing bricks: one lower neighbour along d when the node sits on
-      // the block's low plane and the brick is not the first along d
-      const int s0 = ix == 0 && cx > 0, s1 = iy == 0 && cy > 0, s2 = iz == 0 && cz > 0;
-      const double* base = prm.partial + (size_t)b * (D::NB * 3) + ((iz * D::NBY + iy) * D::NBX + ix) * 3;
-      double v[8][3];
+      // sharing bricks: the lower neighbour along d when the node sits on the
+      // block's low plane and the brick is not the first along d; summed in
+      // increasing brick order (q = i0 + 2 i1 + 4 i2, i_d = s_d - o_d)
+      const int sidx = (ix == 0 ? sb0 : 0) | (iy == 0 ? sb1 : 0) | (iz == 0 ? sb2 : 0);
+      const double* a0 = pbase + ((iz * D::NBY + iy) * D::NBX + ix) * 3;
+      double sum[3] = {0.0, 0.0, 0.0};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int i0 = q & 1, i1 = (q >> 1) & 1, i2 = q >> 2;
-        if (i0 <= s0 && i1 <= s1 && i2 <= s2) {
-          // brick (c_d - s_d + i_d): index offset -(s_d - i_d) stride_d, local
-          // coordinate + (s_d - i_d) P B_d
-          const int o0 = s0 - i0, o1 = s1 - i1, o2 = s2 - i2;
-          const double* a = base - (long long)(o0 + lay.nb[0] * (o1 + lay.nb[1] * o2)) * (D::NB * 3) +
-                            3 * ((o2 * PB2 * D::NBY + o1 * PB1) * D::NBX + o0 * PB0);
+        if (q & ~sidx) continue;
+        const double* a = a0 + off[sidx - q];
+        double v[3];
 #pragma unroll
-          for (int c = 0; c < 3; ++c)
-            v[q][c] = HXG_FIXUP_LD == 1 ? __ldg(a + c) : HXG_FIXUP_LD == 2 ? a[c] : ld_once(a + c, pol);
-        }
+        for (int c = 0; c < 3; ++c)
+          v[c] = HXG_FIXUP_LD == 1 ? __ldg(a + c) : HXG_FIXUP_LD == 2 ? a[c] : ld_once(a + c, pol);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sum[c] += v[c];
       }
-      const int gx = gx0 + ix, gy = gy0 + iy, gz = gz0 + iz;
-      const size_t node = (size_t)gx + (size_t)npx * (gy + (size_t)npy * gz);
+      const size_t dof0 = 3 * ((size_t)gx + (size_t)npx * (gy + (size_t)npy * gz));
       const bool ffix = fb > 0 && (((fb & 1) && gx == 0) || ((fb & 2) && gx == npx - 1) ||
                                    ((fb & 4) && gy == 0) || ((fb & 8) && gy == npy - 1) ||
                                    ((fb & 16) && gz == 0) || ((fb & 32) && gz == box.npd[2] - 1));
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        double sum = 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int i0 = q & 1, i1 = (q >> 1) & 1, i2 = q >> 2;
-          if (i0 <= s0 && i1 <= s1 && i2 <= s2) sum += v[q][c];
-        }
-        const size_t dof = 3 * node + c;
+        const size_t dof = dof0 + c;
         const bool fixed = fb >= 0 ? ffix : prm.mask && prm.mask[dof];
+        double s = sum[c];
         if (MODE == kResidual) {  // f = r - s load; constrained: 0 (operator.hpp:175-179)
-          if (prm.load) sum -= prm.load_scale * prm.load[dof];
-          prm.y[dof] = fixed ? 0.0 : sum;
+          if (prm.load) s -= prm.load_scale * prm.load[dof];
+          prm.y[dof] = fixed ? 0.0 : s;
         } else {
-          prm.y[dof] = fixed ? prm.x[dof] : sum;  // pass x through (operator.hpp:212-214)
+          prm.y[dof] = fixed ? prm.x[dof] : s;  // pass x through (operator.hpp:212-214)
         }
       }
     }
@@ -1223,7 +1242,8 @@ void fused_residual(Operator& op, const double* u, double* f) {
     if (op.partial_.n != need) op.partial_.alloc(need);
     prm.partial = op.partial_.p;
     size_t smem = sizeof(double) * D::SMEM;
-    auto k = fused_jacobian_kernel<P, Q, kStorageCurrent, kResidual>;
+    auto k = prm.geo_box ? fused_jacobian_kernel<P, Q, kStorageCurrent, kResidualBox>
+                         : fused_jacobian_kernel<P, Q, kStorageCurrent, kResidual>;
     HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     HXG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));

@@ -81,6 +81,10 @@ __device__ __forceinline__ double det3(const double m[9]) {
 
 // Residual q-function (material.hpp:126-150).  Returns J; when J <= 0 the
 // outputs are unspecified and the caller records the inverted point.
+// DIAG: dxi/dX is diagonal (box meshes); only its diagonal is read and the
+// products with its zero entries are skipped (the same values: those terms
+// add exact zeros).
+template <bool DIAG = false>
 __device__ __forceinline__ double residual_qf(double mu, double lambda, const double G[9],
                                               const double dxidX[9], double wdet, double H[9],
                                               double st[kRefStateScalars]) {
@@ -89,9 +93,14 @@ __device__ __forceinline__ double residual_qf(double mu, double lambda, const do
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      double s = G[3 * i + 0] * dxidX[0 + j];
-      s = s + G[3 * i + 1] * dxidX[3 + j];
-      s = s + G[3 * i + 2] * dxidX[6 + j];
+      double s;
+      if constexpr (DIAG) {
+        s = G[3 * i + j] * dxidX[4 * j];
+      } else {
+        s = G[3 * i + 0] * dxidX[0 + j];
+        s = s + G[3 * i + 1] * dxidX[3 + j];
+        s = s + G[3 * i + 2] * dxidX[6 + j];
+      }
       F[3 * i + j] = s + (i == j ? 1.0 : 0.0);
     }
   const double J = det3(F);
@@ -109,10 +118,14 @@ __device__ __forceinline__ double residual_qf(double mu, double lambda, const do
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      double s = dxidX[3 * i + 0] * r[0 + j];
-      s = s + dxidX[3 * i + 1] * r[3 + j];
-      s = s + dxidX[3 * i + 2] * r[6 + j];
-      xi[3 * i + j] = s;
+      if constexpr (DIAG) {
+        xi[3 * i + j] = dxidX[4 * i] * r[3 * i + j];
+      } else {
+        double s = dxidX[3 * i + 0] * r[0 + j];
+        s = s + dxidX[3 * i + 1] * r[3 + j];
+        s = s + dxidX[3 * i + 2] * r[6 + j];
+        xi[3 * i + j] = s;
+      }
     }
   double tau[9];
 #pragma unroll
