@@ -19,29 +19,35 @@ void cublas_ok(cublasStatus_t st, const char* what) {
   if (st != CUBLAS_STATUS_SUCCESS) throw Error(HXG_ERR_CUDA, std::string("cuBLAS ") + what + " failed");
 }
 
-// One CTA factors and inverts an n x n block (n <= kDenseBase).  Thread
-// (ti, tj) keeps the 4 x 4 tile (rows 4 ti.., columns 4 tj..) of the lower
-// triangle in registers; every step is one barrier:
-//   1. right-looking Cholesky, step k: the owners of column k publish it
-//      (a double-buffered shared vector), every trailing entry i >= j > k
-//      takes a_ij -= a_ik a_jk / a_kk, and the column owners finalise
-//      l_kk = sqrt(a_kk), l_ik = a_ik / l_kk;
-//   2. L is staged in shared memory (written back over A) and the registers
-//      restart from B = I: forward elimination L W = I, step k: the owners of
-//      row k finalise W_kj = B_kj / L_kk (j <= k) and publish the row, every
-//      entry below takes B_ij -= L_ik W_kj;
+// One CTA factors and inverts an n x n block (n <= kDenseBase), blocked by
+// 4 x 4 tiles.  Thread (ti, tj) keeps tile (ti, tj) of the lower triangle in
+// registers; the block is padded to 4 T rows with the identity (T = ceil(n/4)),
+// which factors to itself and leaves the leading n x n part unchanged.
+//   1. right-looking blocked Cholesky, tile step K: the diagonal tile's owner
+//      factors it in registers (publishing L_KK, 1 / diag and a failed pivot);
+//      the panel tiles below solve X L_KK^T = A_iK and publish X; every
+//      trailing tile takes A_ij -= X_i X_j^T (64 FMAs);
+//   2. L is staged in shared memory (and written back over A); the registers
+//      restart from B = I for the forward elimination L W = I, tile step K:
+//      the row-K tiles finalise W_Kj = L_KK^-1 B_Kj and publish them (double
+//      buffered), every tile below takes B_ij -= L_iK W_Kj;
 //   3. W (zero strict upper part) staged through shared memory to global.
 // A failed pivot (a_kk <= 0, the potrf convention) sets *info = k + 1.
 __global__ void __launch_bounds__(kBaseThreads, 1) chol_inv_base_kernel(double* A, int lda, double* W,
                                                                         int ldw, int n, int* info) {
   extern __shared__ double sm[];
   const int LD = n | 1;
-  double* vec = sm + (size_t)n * LD;  // two 128-entry buffers
+  constexpr int kMax = kTile * kTiles;
+  double* pan = sm + (size_t)n * LD;  // panel X: [kMax][4]
+  double* rowb = pan + kMax * kTile;  // W row tiles, two buffers [2][4][kMax]
+  double* dia = rowb + 2 * kTile * kMax;  // L_KK (16) + its reciprocal diagonal (4)
+  double* rinv = dia + 20;                // 1 / L_kk (kMax)
+  __shared__ int fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ti = tid / kTiles, tj = tid % kTiles;
-  const int r0 = kTile * ti, c0 = kTile * tj;
-  const bool active = ti >= tj && c0 < n;
-  // coalesced load of the lower triangle, then each thread takes its tile
+  const int T = (n + kTile - 1) / kTile;
+  const bool active = ti >= tj && ti < T;
+  if (tid == 0) fail = 0;
   for (int c = warp; c < n; c += kBaseThreads / 32)
     for (int r = c + lane; r < n; r += 32) sm[c * LD + r] = A[r + (size_t)c * lda];
   __syncthreads();
@@ -50,44 +56,63 @@ __global__ void __launch_bounds__(kBaseThreads, 1) chol_inv_base_kernel(double* 
   for (int a = 0; a < kTile; ++a)
 #pragma unroll
     for (int b = 0; b < kTile; ++b) {
-      const int i = r0 + a, j = c0 + b;
-      e[a][b] = active && i < n && i >= j ? sm[j * LD + i] : 0.0;
+      const int i = kTile * ti + a, j = kTile * tj + b;
+      e[a][b] = !active || i < j ? 0.0 : (i < n ? sm[j * LD + i] : (i == j ? 1.0 : 0.0));
     }
-  for (int k = 0; k < n; ++k) {
-    double* cb = vec + (k & 1) * 128;
-    const int tk = k / kTile, kc = k % kTile;
-    if (active && tj == tk) {
+  for (int K = 0; K < T; ++K) {
+    if (ti == K && tj == K) {  // factor the diagonal tile
+#pragma unroll
+      for (int c = 0; c < kTile; ++c) {
+        const double d = e[c][c];
+        if (!(d > 0.0) && fail == 0) fail = kTile * K + c + 1;
+        const double r = sqrt(d), ir = 1.0 / r;
+        e[c][c] = r;
+        dia[16 + c] = ir;
+#pragma unroll
+        for (int a = c + 1; a < kTile; ++a) e[a][c] *= ir;
+#pragma unroll
+        for (int b = c + 1; b < kTile; ++b)
+#pragma unroll
+          for (int a = b; a < kTile; ++a) e[a][b] -= e[a][c] * e[b][c];
+      }
 #pragma unroll
       for (int a = 0; a < kTile; ++a)
 #pragma unroll
-        for (int b = 0; b < kTile; ++b)
-          if (b == kc && r0 + a >= k && r0 + a < n) cb[r0 + a] = e[a][b];
+        for (int b = 0; b < kTile; ++b) dia[a * kTile + b] = e[a][b];
     }
     __syncthreads();
-    const double d = cb[k];
-    if (!(d > 0.0)) {  // uniform: every thread read the same pivot
-      if (tid == 0) atomicCAS(info, 0, k + 1);
+    if (fail) {  // uniform
+      if (tid == 0) atomicCAS(info, 0, fail);
       return;
     }
-    if (active && ti >= tk) {
-      const double rd = 1.0 / d;
-      double li[kTile], lj[kTile];
+    if (active && tj == K && ti > K) {  // X = A_iK L_KK^-T, row by row
 #pragma unroll
-      for (int a = 0; a < kTile; ++a) li[a] = r0 + a > k && r0 + a < n ? cb[r0 + a] * rd : 0.0;
+      for (int a = 0; a < kTile; ++a) {
 #pragma unroll
-      for (int b = 0; b < kTile; ++b) lj[b] = c0 + b > k && c0 + b < n ? cb[c0 + b] : 0.0;
+        for (int b = 0; b < kTile; ++b) {
+          double x = e[a][b];
 #pragma unroll
-      for (int a = 0; a < kTile; ++a)
+          for (int c = 0; c < b; ++c) x -= e[a][c] * dia[b * kTile + c];
+          e[a][b] = x * dia[16 + b];
+        }
 #pragma unroll
-        for (int b = 0; b < kTile; ++b)
-          if (c0 + b > k && r0 + a >= c0 + b) e[a][b] -= li[a] * lj[b];
-      if (tj == tk) {
-        const double r = sqrt(d);
+        for (int b = 0; b < kTile; ++b) pan[(kTile * ti + a) * kTile + b] = e[a][b];
+      }
+    }
+    __syncthreads();
+    if (active && tj > K) {  // trailing update A_ij -= X_i X_j^T, one rank-1 term per c
+#pragma unroll
+      for (int c = 0; c < kTile; ++c) {
+        double xi[kTile], xj[kTile];
+#pragma unroll
+        for (int a = 0; a < kTile; ++a) {
+          xi[a] = pan[(kTile * ti + a) * kTile + c];
+          xj[a] = pan[(kTile * tj + a) * kTile + c];
+        }
 #pragma unroll
         for (int a = 0; a < kTile; ++a)
 #pragma unroll
-          for (int b = 0; b < kTile; ++b)
-            if (b == kc && r0 + a >= k && r0 + a < n) e[a][b] = r0 + a == k ? r : cb[r0 + a] / r;
+          for (int b = 0; b < kTile; ++b) e[a][b] -= xi[a] * xj[b];
       }
     }
   }
@@ -98,44 +123,54 @@ __global__ void __launch_bounds__(kBaseThreads, 1) chol_inv_base_kernel(double* 
     for (int a = 0; a < kTile; ++a)
 #pragma unroll
       for (int b = 0; b < kTile; ++b) {
-        const int i = r0 + a, j = c0 + b;
+        const int i = kTile * ti + a, j = kTile * tj + b;
         if (i < n && i >= j) sm[j * LD + i] = e[a][b];
       }
   }
   __syncthreads();
   for (int c = warp; c < n; c += kBaseThreads / 32)
     for (int r = c + lane; r < n; r += 32) A[r + (size_t)c * lda] = sm[c * LD + r];
+  for (int k = tid; k < kMax; k += kBaseThreads) rinv[k] = k < n ? 1.0 / sm[k * LD + k] : 1.0;
+  // L entry (i, j), identity padding beyond n
+  auto Lat = [&](int i, int j) { return i < n && j < n ? sm[j * LD + i] : (i == j ? 1.0 : 0.0); };
 #pragma unroll
   for (int a = 0; a < kTile; ++a)
 #pragma unroll
-    for (int b = 0; b < kTile; ++b) e[a][b] = r0 + a == c0 + b ? 1.0 : 0.0;
-  for (int k = 0; k < n; ++k) {
-    double* rb = vec + (k & 1) * 128;
-    const int tk = k / kTile, kc = k % kTile;
-    if (active && ti == tk) {
-      const double lkk = sm[k * LD + k];
+    for (int b = 0; b < kTile; ++b) e[a][b] = active && kTile * ti + a == kTile * tj + b ? 1.0 : 0.0;
+  __syncthreads();
+  for (int K = 0; K < T; ++K) {
+    double* rb = rowb + (K & 1) * kTile * kMax;
+    if (active && ti == K) {  // W_Kj = L_KK^-1 B_Kj, column by column
+#pragma unroll
+      for (int b = 0; b < kTile; ++b) {
+#pragma unroll
+        for (int a = 0; a < kTile; ++a) {
+          double w = e[a][b];
+#pragma unroll
+          for (int c = 0; c < a; ++c) w -= Lat(kTile * K + a, kTile * K + c) * e[c][b];
+          e[a][b] = w * rinv[kTile * K + a];
+        }
+      }
 #pragma unroll
       for (int a = 0; a < kTile; ++a)
 #pragma unroll
-        for (int b = 0; b < kTile; ++b)
-          if (a == kc && c0 + b <= k) {
-            const double w = e[a][b] / lkk;
-            e[a][b] = w;
-            rb[c0 + b] = w;
-          }
+        for (int b = 0; b < kTile; ++b) rb[a * kMax + kTile * tj + b] = e[a][b];
     }
     __syncthreads();
-    if (active && ti >= tk) {
-      double lik[kTile], wk[kTile];
+    if (active && ti > K && tj <= K) {  // B_ij -= L_iK W_Kj, one rank-1 term per c
 #pragma unroll
-      for (int a = 0; a < kTile; ++a) lik[a] = r0 + a > k && r0 + a < n ? sm[k * LD + r0 + a] : 0.0;
+      for (int c = 0; c < kTile; ++c) {
+        double l[kTile], w[kTile];
 #pragma unroll
-      for (int b = 0; b < kTile; ++b) wk[b] = c0 + b <= k ? rb[c0 + b] : 0.0;
+        for (int a = 0; a < kTile; ++a) {
+          l[a] = Lat(kTile * ti + a, kTile * K + c);
+          w[a] = rb[c * kMax + kTile * tj + a];
+        }
 #pragma unroll
-      for (int a = 0; a < kTile; ++a)
+        for (int a = 0; a < kTile; ++a)
 #pragma unroll
-        for (int b = 0; b < kTile; ++b)
-          if (r0 + a > k && c0 + b <= k) e[a][b] -= lik[a] * wk[b];
+          for (int b = 0; b < kTile; ++b) e[a][b] -= l[a] * w[b];
+      }
     }
   }
   __syncthreads();  // L no longer read: stage W in its place
@@ -144,8 +179,8 @@ __global__ void __launch_bounds__(kBaseThreads, 1) chol_inv_base_kernel(double* 
     for (int a = 0; a < kTile; ++a)
 #pragma unroll
       for (int b = 0; b < kTile; ++b) {
-        const int i = r0 + a, j = c0 + b;
-        if (i < n && i >= j) sm[j * LD + i] = e[a][b];
+        const int i = kTile * ti + a, j = kTile * tj + b;
+        if (i < n && j < n && i >= j) sm[j * LD + i] = e[a][b];
       }
   }
   __syncthreads();
@@ -153,7 +188,10 @@ __global__ void __launch_bounds__(kBaseThreads, 1) chol_inv_base_kernel(double* 
     for (int r = lane; r < n; r += 32) W[r + (size_t)c * ldw] = r >= c ? sm[c * LD + r] : 0.0;
 }
 
-size_t base_smem(int n) { return sizeof(double) * ((size_t)n * (n | 1) + 256); }
+size_t base_smem(int n) {
+  constexpr int kMax = kTile * kTiles;
+  return sizeof(double) * ((size_t)n * (n | 1) + kMax * kTile + 2 * kTile * kMax + 20 + kMax);
+}
 
 }  // namespace
 
