@@ -641,6 +641,9 @@ int hxg_chol_factorize(hxg_chol_t h, const double* vals_host) {
     if (!h) throw hxg::Error(HXG_ERR_INVALID_ARGUMENT, "null Cholesky handle");
     HXG_CUDA(cudaMemcpy(h->a.vals.p, vals_host, sizeof(double) * h->a.cols_h.size(),
                         cudaMemcpyHostToDevice));
+    // a pageable H2D copy may return before its DMA lands; the handle's
+    // stream may be non-blocking
+    HXG_CUDA(cudaDeviceSynchronize());
     h->solver.factorize(h->a, h->npd, h->stream);
   });
 }

@@ -239,4 +239,32 @@ void dense_chol_inv(cublasHandle_t h, cudaStream_t s, double* A, int lda, double
             "gemm (W21)");
 }
 
+namespace {
+__global__ void spd_fill_kernel(double* a, int n) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const int r = e % n, c = e / n;
+    a[e] = r == c ? (double)n : 1.0 / (1.0 + r + c);
+  }
+}
+}  // namespace
+
+void dense_chol_inv_warmup(cublasHandle_t h, cudaStream_t s) {
+  constexpr int n = 2 * kDenseBase + 64;  // two recursion levels
+  double *a = nullptr, *w = nullptr, *t = nullptr;
+  int* info = nullptr;
+  HXG_CUDA(cudaMalloc(&a, sizeof(double) * n * n));
+  HXG_CUDA(cudaMalloc(&w, sizeof(double) * n * n));
+  HXG_CUDA(cudaMalloc(&t, sizeof(double) * dense_chol_inv_scratch(n)));
+  HXG_CUDA(cudaMalloc(&info, sizeof(int)));
+  spd_fill_kernel<<<64, 256, 0, s>>>(a, n);
+  HXG_CUDA(cudaMemsetAsync(w, 0, sizeof(double) * n * n, s));
+  HXG_CUDA(cudaMemsetAsync(info, 0, sizeof(int), s));
+  dense_chol_inv(h, s, a, n, w, n, n, info, t);
+  HXG_CUDA(cudaStreamSynchronize(s));
+  cudaFree(a);
+  cudaFree(w);
+  cudaFree(t);
+  cudaFree(info);
+}
+
 }  // namespace hxg

@@ -35,6 +35,10 @@ size_t dense_chol_inv_scratch(int n);
 void dense_chol_inv(cublasHandle_t h, cudaStream_t s, double* A, int lda, double* W, int ldw,
                     int n, int* info, double* scratch);
 
+// One small eager factorisation through every code path (kernel attributes,
+// lazily loaded library kernels), so later calls can be graph-captured.
+void dense_chol_inv_warmup(cublasHandle_t h, cudaStream_t s);
+
 // The shared-memory kernel alone (n <= kDenseBase).
 void dense_chol_inv_base(cudaStream_t s, double* A, int lda, double* W, int ldw, int n, int* info);
 

@@ -280,6 +280,7 @@ void cublas_check(cublasStatus_t s, const char* what) {
 NdCholesky::NdCholesky(long long leaf_nodes) : leaf_nodes_(leaf_nodes > 0 ? leaf_nodes : kLeafNodes) {}
 NdCholesky::~NdCholesky() {
   if (graph_) cudaGraphExecDestroy(graph_);
+  if (fgraph_) cudaGraphExecDestroy(fgraph_);
   if (gev_in_) cudaEventDestroy(gev_in_);
   if (gev_out_) cudaEventDestroy(gev_out_);
   if (gstream_) cudaStreamDestroy(gstream_);
@@ -547,7 +548,7 @@ struct NdCholesky::Lane {
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
   cublasHandle_t cublas = nullptr;
-  DevBuf<double> W, inv, tmp, stack, rscr;
+  DevBuf<double> W, inv, tmp, stack, rscr, cublas_ws;
   std::vector<int> fronts;  // postorder
   bool own_stream = false;
   ~Lane() {
@@ -610,6 +611,11 @@ void NdCholesky::plan_lanes() {
     }
     HXG_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
     cublas_check(cublasCreate(&L.cublas), "cublasCreate");
+    L.cublas_ws.alloc((size_t)4 << 20);  // 32 MiB: no lazy allocation inside a capture
+    cublas_check(cublasSetWorkspace(L.cublas, L.cublas_ws.p, L.cublas_ws.n * sizeof(double)),
+                 "cublasSetWorkspace");
+    cublasSetStream(L.cublas, L.stream);
+    dense_chol_inv_warmup(L.cublas, L.stream);  // module loads / attributes outside any capture
     size_t mw = 1, mi = 1, mt = 1, ms = 1, cur = 0, peak = 1;
     std::vector<size_t> st;
     std::vector<int> mine = L.fronts;
@@ -738,6 +744,66 @@ void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s)
                    std::chrono::duration<double, std::milli>(t2 - t1).count());
   }
   ready_ = false;
+  // The numeric factorisation is ~40 k launches over 16 streams, fixed per
+  // pattern: it is captured once into a graph (first call) and replayed,
+  // which removes the host launch cost (HXG_NO_GRAPH=1 or HXG_PROFILE keep
+  // it eager; a failed capture falls back to eager launches).
+  static const bool no_fgraph = std::getenv("HXG_NO_GRAPH") != nullptr || std::getenv("HXG_PROFILE") != nullptr;
+  if (!no_fgraph && !fgraph_failed_) {
+    if (fgraph_ && fgraph_vals_ != a.vals.p) {
+      cudaGraphExecDestroy(fgraph_);
+      fgraph_ = nullptr;
+    }
+    if (!gstream_) {
+      HXG_CUDA(cudaStreamCreateWithFlags(&gstream_, cudaStreamNonBlocking));
+      HXG_CUDA(cudaEventCreateWithFlags(&gev_in_, cudaEventDisableTiming));
+      HXG_CUDA(cudaEventCreateWithFlags(&gev_out_, cudaEventDisableTiming));
+    }
+    if (!fgraph_) {
+      cudaGraph_t g = nullptr;
+      try {
+        HXG_CUDA(cudaStreamBeginCapture(gstream_, cudaStreamCaptureModeThreadLocal));
+        factor_launch(a, gstream_);
+        HXG_CUDA(cudaStreamEndCapture(gstream_, &g));
+        HXG_CUDA(cudaGraphInstantiate(&fgraph_, g, 0));
+        cudaGraphDestroy(g);
+        fgraph_vals_ = a.vals.p;
+      } catch (const Error&) {
+        cudaGraph_t junk = nullptr;
+        cudaStreamEndCapture(gstream_, &junk);
+        if (junk) cudaGraphDestroy(junk);
+        if (g) cudaGraphDestroy(g);
+        fgraph_ = nullptr;
+        cudaGetLastError();
+        fgraph_failed_ = true;
+      }
+    }
+    if (fgraph_) {
+      HXG_CUDA(cudaEventRecord(gev_in_, s));
+      HXG_CUDA(cudaStreamWaitEvent(gstream_, gev_in_, 0));
+      HXG_CUDA(cudaGraphLaunch(fgraph_, gstream_));
+      HXG_CUDA(cudaEventRecord(gev_out_, gstream_));
+      HXG_CUDA(cudaStreamWaitEvent(s, gev_out_, 0));
+    } else {
+      factor_launch(a, s);
+    }
+  } else {
+    factor_launch(a, s);
+  }
+  std::vector<int> info(fronts_.size());
+  HXG_CUDA(cudaMemcpyAsync(info.data(), info_.p, sizeof(int) * info.size(),
+                           cudaMemcpyDeviceToHost, s));
+  HXG_CUDA(cudaStreamSynchronize(s));
+  for (int v : info)
+    if (v != 0)
+      throw Error(HXG_ERR_NOT_SPD, "factorization failed, matrix not SPD: coarse Cholesky "
+                                   "factorization failed at level 0");
+  ready_ = true;
+}
+
+// Every launch of one numeric factorisation, ordered after earlier work on s
+// and joined back into s.
+void NdCholesky::factor_launch(const CsrMatrix& a, cudaStream_t s) {
   Lane& top = *lanes_[0];
   top.stream = s;
   for (auto& l : lanes_) {
@@ -791,15 +857,6 @@ void NdCholesky::factorize(const CsrMatrix& a, const int npd[3], cudaStream_t s)
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
                      .count());
   }
-  std::vector<int> info(fronts_.size());
-  HXG_CUDA(cudaMemcpyAsync(info.data(), info_.p, sizeof(int) * info.size(),
-                           cudaMemcpyDeviceToHost, s));
-  HXG_CUDA(cudaStreamSynchronize(s));
-  for (int v : info)
-    if (v != 0)
-      throw Error(HXG_ERR_NOT_SPD, "factorization failed, matrix not SPD: coarse Cholesky "
-                                   "factorization failed at level 0");
-  ready_ = true;
 }
 
 void NdCholesky::solve(const double* b, double* x, cudaStream_t s) {

@@ -46,6 +46,11 @@ class NdCholesky {
   cudaStream_t gstream_ = nullptr;
   cudaEvent_t gev_in_ = nullptr, gev_out_ = nullptr;
   cudaGraphExec_t graph_ = nullptr;
+  // the captured numeric factorisation (per pattern and value buffer)
+  void factor_launch(const CsrMatrix& a, cudaStream_t s);
+  cudaGraphExec_t fgraph_ = nullptr;
+  const double* fgraph_vals_ = nullptr;
+  bool fgraph_failed_ = false;
   struct Front {
     int parent = -1;
     int child[2] = {-1, -1};

@@ -634,3 +634,9 @@ def test_coarse_cholesky_lattice_matrix(npd, mode):
     bad.sort_indices()
     with pytest.raises(NotSpdError):
         ch.factorize(bad.data)
+    # later factorisations replay the captured launch graph with new values
+    for scale in (2.0, 0.5):
+        ch.factorize(scale * A.data)
+        assert rel(ch.solve(cuda(b)).cpu().numpy(), xh / scale) < 1e-12
+    ch.factorize(cuda(A.data))  # device-resident values
+    assert rel(ch.solve(cuda(b)).cpu().numpy(), xh) < 1e-12
