@@ -1,7 +1,7 @@
-tag=r2s5
-out=gpurun_out/$tag; mkdir -p $out
+# One round-trip: GPU tests, smoke, bench line (under gpurun).
+out=gpurun_out/quick; mkdir -p $out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $out/smi.txt 2>&1
-timeout 1200 python -m pytest tests -x -q -m gpu > $out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $out/pytest_gpu.log
+timeout 1200 python -m pytest tests -q -m gpu > $out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 2>&1; echo "smoke rc=$?" >> $out/smoke.log
-timeout 900 python bench.py > $out/bench.json 2> $out/bench.err
+timeout 900 python bench.py > $out/bench_n1.json 2> $out/bench.err
 echo done
